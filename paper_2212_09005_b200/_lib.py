@@ -1,0 +1,128 @@
+"""ctypes binding of libfkb200.so (the C ABI in include/filterkit_b200.h).
+
+The product path has exactly one backend: these sm_100a kernels.  If the
+library or a CUDA device is missing, every filter constructor raises
+immediately -- there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfkb200.so")
+
+FK_ORDERED, FK_CONCURRENT = 0, 1
+FK_E_INVARIANT = -9
+FK_E_ARG = -1000
+
+c_i64, c_i32, c_u64, c_vp, c_sz = ctypes.c_int64, ctypes.c_int32, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_size_t
+
+
+class TcfGeom(ctypes.Structure):
+    _fields_ = [("num_blocks", c_i64), ("backing_slots", c_i64), ("block_slots", c_i32),
+                ("tag_bits", c_i32), ("slot_bytes", c_i32), ("cut_slots", c_i32),
+                ("probe_limit", c_i32), ("group_width", c_i32), ("seed", c_u64)]
+
+
+_SIGS = {
+    "fk_version": (ctypes.c_char_p, []),
+    "fk_abi_version": (c_i32, []),
+    "fk_hash_streams": (c_i32, [c_vp, c_i64, c_u64, c_i32, c_u64, c_u64, c_vp, c_vp]),
+    "fk_fastmod_check": (c_i32, [c_vp, c_i64, c_u64, c_vp, c_vp]),
+    "fk_tcf_workspace_bytes": (c_sz, [ctypes.POINTER(TcfGeom), c_i64, c_i32]),
+    "fk_tcf_insert": (c_i32, [ctypes.POINTER(TcfGeom), c_vp, c_vp, c_vp, c_i32, c_vp, c_i64, c_vp,
+                              c_vp, c_i32, c_vp, c_sz, c_vp]),
+    "fk_tcf_query": (c_i32, [ctypes.POINTER(TcfGeom), c_vp, c_vp, c_vp, c_i32, c_i64, c_vp, c_vp, c_vp]),
+    "fk_tcf_delete": (c_i32, [ctypes.POINTER(TcfGeom), c_vp, c_vp, c_vp, c_i32, c_i64, c_vp, c_vp,
+                              c_i32, c_vp, c_sz, c_vp]),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def exported_symbols():
+    """Names the Python side binds (tests check the .so exports all of them)."""
+    return sorted(_SIGS)
+
+
+def load():
+    """Load libfkb200.so and bind every entry point; raises if unavailable."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise RuntimeError(
+                    "libfkb200.so is not built (%s); run __graft_entry__.build() -- "
+                    "there is no CPU fallback" % LIB_PATH)
+            lib = ctypes.CDLL(LIB_PATH)
+            for name, (res, args) in _SIGS.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+    return _lib
+
+
+class KernelError(RuntimeError):
+    pass
+
+
+def check(rc, what):
+    """Map a C-ABI return code to an exception (never silently ignored)."""
+    if rc == 0:
+        return 0
+    if rc == FK_E_INVARIANT:
+        raise RuntimeError("%s: invariant violation" % what)
+    if rc == FK_E_ARG:
+        raise ValueError("%s: invalid arguments" % what)
+    if rc < 0:
+        raise KernelError("%s: CUDA error %d" % (what, -rc))
+    return rc
+
+
+def require_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("the B200 filter kernels need a CUDA device; none is visible "
+                           "(there is no CPU fallback)")
+    load()
+    return torch
+
+
+def dptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None and t.numel() else ctypes.c_void_p(0)
+
+
+def stream_ptr(torch):
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def to_device_u64(torch, keys, device):
+    """numpy/torch/sequence of 64-bit keys -> contiguous int64 CUDA tensor (bit view)."""
+    if isinstance(keys, torch.Tensor):
+        t = keys
+        if t.dtype in (torch.int64, torch.uint64):
+            t = t.view(torch.int64)
+        else:
+            t = t.to(torch.int64)
+        return t.to(device).contiguous()
+    arr = np.ascontiguousarray(np.asarray(keys, dtype=np.uint64).reshape(-1))
+    return torch.from_numpy(arr.view(np.int64)).to(device)
+
+
+def host_view(torch, t, dtype):
+    """Device byte tensor -> numpy array of `dtype` (synchronous D2H)."""
+    return t.detach().cpu().numpy().view(dtype)
+
+
+def to_device_bytes(torch, arr, device):
+    a = np.ascontiguousarray(arr)
+    return torch.from_numpy(a.view(np.uint8).reshape(-1).copy()).to(device)

@@ -1,0 +1,57 @@
+// abi_misc.cu -- version + hashing-parity entry points of the C ABI.
+#include "../../include/filterkit_b200.h"
+#include "fk_common.cuh"
+
+namespace fk {
+
+// fp, b1, b2, backing start, backing step per key (hashing.py:66-117).
+__global__ void k_hash_streams(const uint64_t *__restrict__ keys, int64_t n, uint64_t seed, uint64_t fpmask,
+                               uint64_t nb, FastMod nbm, uint64_t bs, FastMod bsm, uint64_t *__restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t fp = mix64(keys[i] ^ seed) & fpmask;
+    out[5 * i] = fp;
+    out[5 * i + 1] = nb ? fmod64(mix64(fp ^ kBlock1), nbm) : 0;
+    out[5 * i + 2] = nb ? fmod64(mix64(fp ^ kBlock2), nbm) : 0;
+    out[5 * i + 3] = bs ? fmod64(mix64(fp ^ kBackStart), bsm) : 0;
+    out[5 * i + 4] = bs ? fmod64(mix64(fp ^ kBackStep) | 1, bsm) : 0;
+  }
+}
+
+__global__ void k_fastmod(const uint64_t *__restrict__ x, int64_t n, FastMod m, uint64_t *__restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = fmod64(x[i], m);
+}
+
+}  // namespace fk
+
+using namespace fk;
+
+extern "C" {
+
+const char *fk_version(void) { return "filterkit-b200 0.1.0 (sm_100a)"; }
+int fk_abi_version(void) { return FK_ABI_VERSION; }
+
+int fk_hash_streams(const uint64_t *keys, int64_t n, uint64_t seed, int bits, uint64_t nb, uint64_t bsize,
+                    uint64_t *out5, void *stream) {
+  if (n < 0 || bits < 1 || bits > 64) return FK_E_ARG;
+  if (n == 0) return 0;
+  uint64_t m = bits >= 64 ? ~0ULL : ((1ULL << bits) - 1);
+  int grid = (int)((n + 255) / 256);
+  if (grid > num_sms() * 16) grid = num_sms() * 16;
+  k_hash_streams<<<grid, 256, 0, (cudaStream_t)stream>>>(keys, n, seed, m, nb, make_fastmod(nb ? nb : 1), bsize,
+                                                         make_fastmod(bsize ? bsize : 1), out5);
+  FK_CHECK_LAUNCH();
+  return 0;
+}
+
+int fk_fastmod_check(const uint64_t *x, int64_t n, uint64_t d, uint64_t *out, void *stream) {
+  if (n < 0 || d == 0) return FK_E_ARG;
+  if (n == 0) return 0;
+  int grid = (int)((n + 255) / 256);
+  if (grid > num_sms() * 16) grid = num_sms() * 16;
+  k_fastmod<<<grid, 256, 0, (cudaStream_t)stream>>>(x, n, make_fastmod(d), out);
+  FK_CHECK_LAUNCH();
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,135 @@
+// tcf_point.cu -- C-ABI entry points of the point two-choice filter.
+// Kernels: tcf_point_impl.cuh (instantiated per slot width in tcf_point_s*.cu).
+#include "tcf_point_impl.cuh"
+
+namespace fk {
+extern template int tcf_run<uint8_t>(int, int, int, const TcfDev &, const TcfCall &, cudaStream_t);
+extern template int tcf_run<uint16_t>(int, int, int, const TcfDev &, const TcfCall &, cudaStream_t);
+extern template int tcf_run<uint32_t>(int, int, int, const TcfDev &, const TcfCall &, cudaStream_t);
+extern template int tcf_run<uint64_t>(int, int, int, const TcfDev &, const TcfCall &, cudaStream_t);
+
+static int geom_ok(const fk_tcf_geom *g) {
+  if (!g || g->num_blocks < 1 || g->num_blocks > 0xFFFFFFF0LL) return 0;
+  if (g->block_slots < 1 || g->backing_slots < 0) return 0;
+  int w = g->slot_bytes;
+  if (w != 1 && w != 2 && w != 4 && w != 8) return 0;
+  if (g->tag_bits <= 2 || g->tag_bits > 8 * w) return 0;
+  if (g->block_slots * 8 * w > 1024) return 0;
+  int G = g->group_width;
+  if (G != 1 && G != 2 && G != 4 && G != 8 && G != 16 && G != 32) return 0;
+  if (G > g->block_slots) return 0;
+  return 1;
+}
+
+static TcfDev make_dev(const fk_tcf_geom *g, const void *blocks, const void *backing, int keys_are_fps) {
+  TcfDev P;
+  P.blocks = const_cast<void *>(blocks);
+  P.backing = const_cast<void *>(backing);
+  P.nb = (uint64_t)g->num_blocks;
+  P.nbm = make_fastmod(P.nb);
+  P.bsize = (uint64_t)g->backing_slots;
+  P.bsm = make_fastmod(P.bsize ? P.bsize : 1);
+  P.B = g->block_slots;
+  P.f = g->tag_bits;
+  P.cut = g->cut_slots;
+  P.probe_limit = g->probe_limit;
+  P.fmask = g->tag_bits >= 64 ? ~0ULL : ((1ULL << g->tag_bits) - 1);
+  P.seed = g->seed;
+  P.keys_are_fps = keys_are_fps;
+  return P;
+}
+
+static int run(const fk_tcf_geom *g, int op, const TcfDev &P, const TcfCall &c, cudaStream_t st) {
+  switch (g->slot_bytes) {
+    case 1: return tcf_run<uint8_t>(op, g->group_width, g->block_slots, P, c, st);
+    case 4: return tcf_run<uint32_t>(op, g->group_width, g->block_slots, P, c, st);
+    case 8: return tcf_run<uint64_t>(op, g->group_width, g->block_slots, P, c, st);
+    default: return tcf_run<uint16_t>(op, g->group_width, g->block_slots, P, c, st);
+  }
+}
+
+static size_t ord_ws_layout(const fk_tcf_geom *g, int64_t n, size_t *off) {
+  // off[]: res, bres, defer_idx, defer_fp, defer_word, defer_pend, ctl
+  size_t a = 0;
+  auto take = [&](size_t bytes) { size_t o = a; a += (bytes + 255) & ~(size_t)255; return o; };
+  int64_t cap = n < 1 ? 1 : n;
+  off[0] = take((size_t)g->num_blocks * 4);
+  off[1] = take((size_t)(g->backing_slots ? g->backing_slots : 1) * 4);
+  off[2] = take((size_t)cap * 8);
+  off[3] = take((size_t)cap * 8);
+  off[4] = take((size_t)cap * 8);
+  off[5] = take((size_t)cap);
+  off[6] = take(64);
+  return a;
+}
+
+static int prep_ordered(const fk_tcf_geom *g, int64_t n, void *ws, size_t ws_bytes, OrdScratch *X,
+                        cudaStream_t st) {
+  size_t off[7];
+  size_t need = ord_ws_layout(g, n, off);
+  if (!ws || ws_bytes < need) return FK_E_ARG;
+  char *b = (char *)ws;
+  X->res = (uint32_t *)(b + off[0]);
+  X->bres = (uint32_t *)(b + off[1]);
+  X->defer_idx = (int64_t *)(b + off[2]);
+  X->defer_fp = (uint64_t *)(b + off[3]);
+  X->defer_word = (uint64_t *)(b + off[4]);
+  X->defer_pend = (uint8_t *)(b + off[5]);
+  X->ctl = (unsigned int *)(b + off[6]);
+  X->defer_cap = n < 1 ? 1 : n;
+  FK_TRY(cudaMemsetAsync(X->res, 0xFF, (size_t)g->num_blocks * 4, st));
+  FK_TRY(cudaMemsetAsync(X->bres, 0xFF, (size_t)(g->backing_slots ? g->backing_slots : 1) * 4, st));
+  FK_TRY(cudaMemsetAsync(X->ctl, 0, 64, st));
+  return 0;
+}
+
+}  // namespace fk
+
+using namespace fk;
+
+extern "C" {
+
+size_t fk_tcf_workspace_bytes(const fk_tcf_geom *g, int64_t n, int mode) {
+  if (!g || mode != FK_ORDERED) return 0;
+  size_t off[7];
+  return ord_ws_layout(g, n, off);
+}
+
+int fk_tcf_insert(const fk_tcf_geom *g, void *blocks, void *backing, const uint64_t *keys, int keys_are_fps,
+                  const uint64_t *values, int64_t n, uint8_t *codes, int64_t *counters, int mode, void *ws,
+                  size_t ws_bytes, void *stream) {
+  if (!geom_ok(g) || n < 0 || !counters) return FK_E_ARG;
+  if (n == 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  TcfDev P = make_dev(g, blocks, backing, keys_are_fps);
+  TcfCall c = {keys, values, n, codes, nullptr, counters, OrdScratch{}};
+  if (mode == FK_CONCURRENT) return run(g, kOpInsCas, P, c, st);
+  if (n > 0xFFFFFFF0LL) return FK_E_ARG;
+  int rc = prep_ordered(g, n, ws, ws_bytes, &c.X, st);
+  return rc ? rc : run(g, kOpInsOrd, P, c, st);
+}
+
+int fk_tcf_query(const fk_tcf_geom *g, const void *blocks, const void *backing, const uint64_t *keys,
+                 int keys_are_fps, int64_t n, uint8_t *found, uint64_t *values_out, void *stream) {
+  if (!geom_ok(g) || n < 0) return FK_E_ARG;
+  if (n == 0) return 0;
+  TcfDev P = make_dev(g, blocks, backing, keys_are_fps);
+  TcfCall c = {keys, nullptr, n, found, values_out, nullptr, OrdScratch{}};
+  return run(g, kOpQuery, P, c, (cudaStream_t)stream);
+}
+
+int fk_tcf_delete(const fk_tcf_geom *g, void *blocks, void *backing, const uint64_t *keys, int keys_are_fps,
+                  int64_t n, uint8_t *removed, int64_t *counters, int mode, void *ws, size_t ws_bytes,
+                  void *stream) {
+  if (!geom_ok(g) || n < 0 || !counters) return FK_E_ARG;
+  if (n == 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  TcfDev P = make_dev(g, blocks, backing, keys_are_fps);
+  TcfCall c = {keys, nullptr, n, removed, nullptr, counters, OrdScratch{}};
+  if (mode == FK_CONCURRENT) return run(g, kOpDelCas, P, c, st);
+  if (n > 0xFFFFFFF0LL) return FK_E_ARG;
+  int rc = prep_ordered(g, n, ws, ws_bytes, &c.X, st);
+  return rc ? rc : run(g, kOpDelOrd, P, c, st);
+}
+
+}  // extern "C"

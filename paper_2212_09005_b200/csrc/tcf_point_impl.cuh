@@ -1,0 +1,697 @@
+#pragma once
+// tcf_point.cu -- point two-choice filter on sm_100a.
+//
+// Replaces the reference kernel contract functions tcf_insert_batch,
+// tcf_query_batch and tcf_delete_batch (_ckernels.pyx:193-355,
+// _pykernels.py:120-236).  One cooperative-group tile of G lanes (1..32)
+// serves one key: the tile loads the key's 16-bit-tag block with 128-bit
+// vector loads split across its lanes, and votes with warp ballots (the
+// paper's Alg. 1).
+//
+// Two insert/delete semantics:
+//   * concurrent (FK_CONCURRENT): every key at once, slot claims by atomicCAS,
+//     a lost CAS moves to the next candidate -- the reference's free-threaded
+//     semantics.
+//   * ordered (FK_ORDERED): bit-identical to one caller thread streaming the
+//     batch through the reference.  A persistent cooperative kernel walks the
+//     batch in windows; within a window keys take deterministic reservations
+//     on both candidate blocks (atomicMin of the input index) and a key
+//     commits only when it holds both, i.e. when every earlier key that could
+//     change its blocks has already committed.  Backing-table work, which
+//     never feeds back into block decisions (ck:228-233), is deferred to a
+//     second reservation phase over probe positions.
+#include "../../include/filterkit_b200.h"
+#include "fk_common.cuh"
+
+namespace fk {
+
+constexpr uint32_t kNoRes = 0xFFFFFFFFu;
+
+struct TcfDev {
+  void *blocks;
+  void *backing;
+  uint64_t nb;
+  FastMod nbm;
+  uint64_t bsize;
+  FastMod bsm;
+  int B, f, cut, probe_limit;
+  uint64_t fmask;
+  uint64_t seed;
+  int keys_are_fps;
+};
+
+struct KeyInfo {
+  uint64_t fp, tag, b1, b2;
+};
+
+__device__ __forceinline__ KeyInfo key_info(const TcfDev &P, uint64_t key) {
+  KeyInfo k;
+  k.fp = P.keys_are_fps ? key : mix64(key ^ P.seed);  // tcf.py:118-120
+  k.tag = remap_tag(k.fp, P.fmask);
+  k.b1 = fmod64(mix64(k.fp ^ kBlock1), P.nbm);  // hashing.py:92-99
+  k.b2 = fmod64(mix64(k.fp ^ kBlock2), P.nbm);
+  return k;
+}
+
+// G lanes of an aligned warp sub-group serve one key.
+template <int G>
+struct Tile {
+  unsigned lane, base, mask;
+  __device__ __forceinline__ Tile() {
+    unsigned l = threadIdx.x & 31;
+    lane = l % G;
+    base = l - lane;
+    mask = G == 32 ? 0xFFFFFFFFu : (((1u << G) - 1u) << base);
+  }
+  __device__ __forceinline__ unsigned ballot(bool p) const {
+    if constexpr (G == 1) return p ? 1u : 0u;
+    unsigned b = __ballot_sync(mask, p);
+    return G == 32 ? b : ((b >> base) & ((1u << G) - 1u));
+  }
+  template <typename T>
+  __device__ __forceinline__ T bcast(T v, int src) const {
+    if constexpr (G == 1) return v;
+    return __shfl_sync(mask, v, (int)base + src);
+  }
+  __device__ __forceinline__ int sum(int v) const {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(mask, v, o);
+    return v;
+  }
+};
+
+// One lane's contiguous share of a block: slots [lo, lo+cnt).
+// BF = compile-time block size (vector loads), 0 = runtime B (scalar loads).
+template <typename S, int G, int BF>
+struct Chunk {
+  static constexpr int MAXB = BF ? BF : (1024 / (8 * (int)sizeof(S)));
+  static constexpr int C = (MAXB + G - 1) / G;
+  static constexpr int NREG = (C * (int)sizeof(S) + 3) / 4;
+  uint32_t r[NREG];
+  int lo, cnt;
+
+  template <bool CGL>
+  __device__ __forceinline__ void load(const S *blk, int B, unsigned lane) {
+    if constexpr (BF != 0) {
+      lo = (int)lane * C;
+      cnt = C;
+      load_chunk<C * (int)sizeof(S), CGL>(blk + lo, r);
+    } else {
+      int c = (B + G - 1) / G;
+      lo = (int)lane * c;
+      cnt = B - lo < c ? B - lo : c;
+      if (cnt < 0) cnt = 0;
+#pragma unroll
+      for (int j = 0; j < NREG; j++) r[j] = 0;
+#pragma unroll
+      for (int j = 0; j < C; j++)
+        if (j < cnt) set_reg_slot<S>(r, j, load_slot<S, CGL>(blk + lo + j));
+    }
+  }
+  __device__ __forceinline__ uint64_t at(int j) const { return reg_slot<S>(r, j); }
+  __device__ __forceinline__ int used() const {
+    int n = 0;
+#pragma unroll
+    for (int j = 0; j < C; j++) n += (j < cnt && live_word(at(j))) ? 1 : 0;
+    return n;
+  }
+  // first index >= j0 that is free (EMPTY or TOMBSTONE), else -1
+  __device__ __forceinline__ int first_free(int j0) const {
+#pragma unroll
+    for (int j = 0; j < C; j++)
+      if (j >= j0 && j < cnt && !live_word(at(j))) return j;
+    return -1;
+  }
+  // first index >= j0 holding a live word whose tag bits equal tag, else -1
+  __device__ __forceinline__ int first_match(int j0, uint64_t tag, uint64_t fmask) const {
+#pragma unroll
+    for (int j = 0; j < C; j++) {
+      uint64_t w = at(j);
+      if (j >= j0 && j < cnt && live_word(w) && (w & fmask) == tag) return j;
+    }
+    return -1;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// query (pure function of table + keys: bit-exact in every mode)
+// ---------------------------------------------------------------------------
+template <typename S, int G, int BF>
+__global__ void __launch_bounds__(256) k_tcf_query(TcfDev P, const uint64_t *__restrict__ keys, int64_t n,
+                                                   uint8_t *__restrict__ found, uint64_t *__restrict__ vals) {
+  Tile<G> t;
+  const S *blocks = reinterpret_cast<const S *>(P.blocks);
+  const S *backing = reinterpret_cast<const S *>(P.backing);
+  int64_t tiles = (int64_t)gridDim.x * (blockDim.x / G);
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G; i < n; i += tiles) {
+    KeyInfo k = key_info(P, keys[i]);
+    bool hit = false;
+    uint64_t val = 0;
+    // b1, then b2: first live match in ascending slot order (pk:152-177)
+#pragma unroll 1
+    for (int which = 0; which < 2 && !hit; which++) {
+      uint64_t b = which ? k.b2 : k.b1;
+      Chunk<S, G, BF> c;
+      c.template load<false>(blocks + b * (uint64_t)P.B, P.B, t.lane);
+      int j = c.first_match(0, k.tag, P.fmask);
+      unsigned bal = t.ballot(j >= 0);
+      if (bal) {
+        int leader = __ffs(bal) - 1;
+        uint64_t w = t.bcast(j >= 0 ? c.at(j) : 0ull, leader);
+        hit = true;
+        val = P.f >= 64 ? 0 : (w >> P.f);
+      }
+    }
+    if (!hit && P.bsize && t.lane == 0) {  // backing chain (pk:178-189)
+      uint64_t p = fmod64(mix64(k.fp ^ kBackStart), P.bsm);
+      uint64_t step = fmod64(mix64(k.fp ^ kBackStep) | 1, P.bsm);
+      for (int q = 0; q < P.probe_limit; q++) {
+        uint64_t w = backing[p];
+        if (w == 0) break;
+        if (w != 1 && (w & P.fmask) == k.tag) {
+          hit = true;
+          val = P.f >= 64 ? 0 : (w >> P.f);
+          break;
+        }
+        p += step;
+        p = p >= P.bsize ? p - P.bsize : p;
+      }
+    }
+    if (t.lane == 0) {
+      found[i] = hit ? 1 : 0;
+      if (vals) vals[i] = hit ? val : 0;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// concurrent (free-threaded CAS) insert / delete
+// ---------------------------------------------------------------------------
+
+// Claim the lowest free slot of a block snapshot by CAS, ascending; a lost CAS
+// moves on to the next candidate (ck:150-171).  Returns true on success.
+template <typename S, int G, int BF>
+__device__ __forceinline__ bool tile_claim_cas(const Tile<G> &t, const Chunk<S, G, BF> &c, S *blk,
+                                               uint64_t word) {
+  int j0 = 0;
+  for (;;) {
+    int j = c.first_free(j0);
+    unsigned bal = t.ballot(j >= 0);
+    if (!bal) return false;
+    int leader = __ffs(bal) - 1;
+    int ok = 0;
+    if ((int)t.lane == leader) {
+      ok = cas_slot<S>(blk + c.lo + j, (S)c.at(j), (S)word) ? 1 : 0;
+      j0 = j + 1;
+    }
+    ok = t.bcast(ok, leader);
+    if (ok) return true;
+  }
+}
+
+template <typename S>
+__device__ __forceinline__ bool backing_claim_cas(const TcfDev &P, uint64_t fp, uint64_t word) {
+  if (!P.bsize) return false;
+  S *bk = reinterpret_cast<S *>(P.backing);
+  uint64_t p = fmod64(mix64(fp ^ kBackStart), P.bsm);
+  uint64_t step = fmod64(mix64(fp ^ kBackStep) | 1, P.bsm);
+  for (int q = 0; q < P.probe_limit; q++) {
+    uint64_t w = *(volatile S *)(bk + p);
+    if (!live_word(w) && cas_slot<S>(bk + p, (S)w, (S)word)) return true;
+    p += step;
+    p = p >= P.bsize ? p - P.bsize : p;
+  }
+  return false;
+}
+
+template <typename S, int G, int BF>
+__global__ void __launch_bounds__(256)
+    k_tcf_insert_cas(TcfDev P, const uint64_t *__restrict__ keys, const uint64_t *__restrict__ values, int64_t n,
+                     uint8_t *__restrict__ codes, int64_t *__restrict__ counters) {
+  Tile<G> t;
+  S *blocks = reinterpret_cast<S *>(P.blocks);
+  int64_t tiles = (int64_t)gridDim.x * (blockDim.x / G);
+  long long n_ok = 0, n_back = 0;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G; i < n; i += tiles) {
+    KeyInfo k = key_info(P, keys[i]);
+    uint64_t word = (P.f >= 64 ? 0 : ((values ? values[i] : 0) << P.f)) | k.tag;
+    S *blk1 = blocks + k.b1 * (uint64_t)P.B;
+    S *blk2 = blocks + k.b2 * (uint64_t)P.B;
+    uint8_t code = kFull;
+    Chunk<S, G, BF> c1;
+    c1.template load<true>(blk1, P.B, t.lane);
+    int u1 = t.sum(c1.used());
+    if (u1 < P.cut && tile_claim_cas<S, G, BF>(t, c1, blk1, word)) {
+      code = kPrimary;  // shortcut (ck:216-218)
+    } else {
+      c1.template load<true>(blk1, P.B, t.lane);
+      Chunk<S, G, BF> c2;
+      c2.template load<true>(blk2, P.B, t.lane);
+      int o1 = t.sum(c1.used()), o2 = t.sum(c2.used());
+      bool first1 = o1 <= o2;  // tie -> primary (ck:222-227)
+      if (tile_claim_cas<S, G, BF>(t, first1 ? c1 : c2, first1 ? blk1 : blk2, word)) {
+        code = (first1 || k.b1 == k.b2) ? kPrimary : kSecondary;
+      } else if (tile_claim_cas<S, G, BF>(t, first1 ? c2 : c1, first1 ? blk2 : blk1, word)) {
+        code = (!first1 || k.b1 == k.b2) ? kPrimary : kSecondary;
+      } else {
+        int ok = 0;
+        if (t.lane == 0) ok = backing_claim_cas<S>(P, k.fp, word) ? 1 : 0;
+        if (t.bcast(ok, 0)) code = kBacking;
+      }
+    }
+    if (t.lane == 0) {
+      codes[i] = code;
+      n_ok += code != kFull;
+      n_back += code == kBacking;
+    }
+  }
+  if (n_ok) atomicAdd((unsigned long long *)&counters[0], (unsigned long long)n_ok);
+  if (n_back) atomicAdd((unsigned long long *)&counters[1], (unsigned long long)n_back);
+}
+
+template <typename S, int G, int BF>
+__global__ void __launch_bounds__(256)
+    k_tcf_delete_cas(TcfDev P, const uint64_t *__restrict__ keys, int64_t n, uint8_t *__restrict__ removed,
+                     int64_t *__restrict__ counters) {
+  Tile<G> t;
+  S *blocks = reinterpret_cast<S *>(P.blocks);
+  int64_t tiles = (int64_t)gridDim.x * (blockDim.x / G);
+  long long n_del = 0;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G; i < n; i += tiles) {
+    KeyInfo k = key_info(P, keys[i]);
+    bool done = false;
+#pragma unroll 1
+    for (int which = 0; which < 2 && !done; which++) {
+      S *blk = blocks + (which ? k.b2 : k.b1) * (uint64_t)P.B;
+      Chunk<S, G, BF> c;
+      c.template load<true>(blk, P.B, t.lane);
+      int j0 = 0;
+      for (;;) {  // first live match, CAS to TOMBSTONE, next match on a lost race (ck:328-339)
+        int j = c.first_match(j0, k.tag, P.fmask);
+        unsigned bal = t.ballot(j >= 0);
+        if (!bal) break;
+        int leader = __ffs(bal) - 1;
+        int ok = 0;
+        if ((int)t.lane == leader) {
+          ok = cas_slot<S>(blk + c.lo + j, (S)c.at(j), (S)1) ? 1 : 0;
+          j0 = j + 1;
+        }
+        if (t.bcast(ok, leader)) {
+          done = true;
+          break;
+        }
+      }
+    }
+    if (!done && P.bsize && t.lane == 0) {
+      S *bk = reinterpret_cast<S *>(P.backing);
+      uint64_t p = fmod64(mix64(k.fp ^ kBackStart), P.bsm);
+      uint64_t step = fmod64(mix64(k.fp ^ kBackStep) | 1, P.bsm);
+      for (int q = 0; q < P.probe_limit; q++) {
+        uint64_t w = *(volatile S *)(bk + p);
+        if (w == 0) break;
+        if (w != 1 && (w & P.fmask) == k.tag && cas_slot<S>(bk + p, (S)w, (S)1)) {
+          done = true;
+          break;
+        }
+        p += step;
+        p = p >= P.bsize ? p - P.bsize : p;
+      }
+    }
+    if (t.lane == 0) {
+      removed[i] = done ? 1 : 0;
+      n_del += done;
+    }
+  }
+  if (n_del) atomicAdd((unsigned long long *)&counters[2], (unsigned long long)n_del);
+}
+
+// ---------------------------------------------------------------------------
+// ordered (sequential-semantics) insert / delete: persistent cooperative kernel
+// ---------------------------------------------------------------------------
+
+struct OrdScratch {
+  uint32_t *res;        // per-block reservation word (min pending input index)
+  uint32_t *bres;       // per-backing-slot reservation word
+  int64_t *defer_idx;   // keys deferred to the backing phase (unordered list)
+  uint64_t *defer_fp;
+  uint64_t *defer_word;
+  uint8_t *defer_pend;
+  unsigned int *ctl;    // [0..1] round counters, [2] defer count
+  int64_t defer_cap;
+};
+
+template <int OP>  // 0 insert, 1 delete
+struct OrdKey {
+  uint32_t b1, b2;
+  uint64_t word;  // insert: packed slot word; delete: remapped tag
+  bool pend;
+};
+
+// CTA-wide OR of a predicate (all threads of the CTA must call).
+__device__ __forceinline__ bool cta_any(bool p) { return __syncthreads_or(p ? 1 : 0) != 0; }
+
+template <typename S, int G, int BF>
+__device__ __forceinline__ int tile_first_free(const Tile<G> &t, const Chunk<S, G, BF> &c, int *slot) {
+  int j = c.first_free(0);
+  unsigned bal = t.ballot(j >= 0);
+  if (!bal) return 0;
+  int leader = __ffs(bal) - 1;
+  *slot = t.bcast(j >= 0 ? c.lo + j : 0, leader);
+  return 1;
+}
+
+// The sequential insert policy (pk:126-148) on exclusively reserved blocks.
+// Returns the placement code, or 4 = "both blocks full, defer to backing".
+template <typename S, int G, int BF>
+__device__ __forceinline__ uint8_t commit_insert(const TcfDev &P, const Tile<G> &t, uint32_t b1, uint32_t b2,
+                                                 uint64_t word) {
+  S *blocks = reinterpret_cast<S *>(P.blocks);
+  S *blk1 = blocks + (uint64_t)b1 * P.B, *blk2 = blocks + (uint64_t)b2 * P.B;
+  Chunk<S, G, BF> c1;
+  c1.template load<true>(blk1, P.B, t.lane);
+  int u1 = t.sum(c1.used());
+  int slot;
+  if (u1 < P.cut) {
+    tile_first_free<S, G, BF>(t, c1, &slot);  // cut <= B, so a free slot exists
+    if (t.lane == 0) blk1[slot] = (S)word;
+    return kPrimary;
+  }
+  Chunk<S, G, BF> c2;
+  c2.template load<true>(blk2, P.B, t.lane);
+  int u2 = t.sum(c2.used());
+  bool first1 = u1 <= u2;
+  if (tile_first_free<S, G, BF>(t, first1 ? c1 : c2, &slot)) {
+    if (t.lane == 0) (first1 ? blk1 : blk2)[slot] = (S)word;
+    return (first1 || b1 == b2) ? kPrimary : kSecondary;
+  }
+  if (tile_first_free<S, G, BF>(t, first1 ? c2 : c1, &slot)) {
+    if (t.lane == 0) (first1 ? blk2 : blk1)[slot] = (S)word;
+    return (!first1 || b1 == b2) ? kPrimary : kSecondary;
+  }
+  return 4;
+}
+
+// The sequential delete (pk:207-222) on exclusively reserved blocks:
+// tombstone the first live match of b1, else of b2.  1 = done, 0 = defer.
+template <typename S, int G, int BF>
+__device__ __forceinline__ int commit_delete(const TcfDev &P, const Tile<G> &t, uint32_t b1, uint32_t b2,
+                                             uint64_t tag) {
+  S *blocks = reinterpret_cast<S *>(P.blocks);
+#pragma unroll 1
+  for (int which = 0; which < 2; which++) {
+    S *blk = blocks + (uint64_t)(which ? b2 : b1) * P.B;
+    Chunk<S, G, BF> c;
+    c.template load<true>(blk, P.B, t.lane);
+    int j = c.first_match(0, tag, P.fmask);
+    unsigned bal = t.ballot(j >= 0);
+    if (bal) {
+      int leader = __ffs(bal) - 1;
+      if ((int)t.lane == leader) blk[c.lo + j] = (S)1;
+      return 1;
+    }
+  }
+  return 0;
+}
+
+template <typename S, int G, int BF, int K, int OP>
+__global__ void __launch_bounds__(256)
+    k_tcf_ordered(TcfDev P, const uint64_t *__restrict__ keys, const uint64_t *__restrict__ values, int64_t n,
+                  uint8_t *__restrict__ out, int64_t *__restrict__ counters, OrdScratch X) {
+  cg::grid_group grid = cg::this_grid();
+  Tile<G> t;
+  const int64_t tiles = (int64_t)gridDim.x * (blockDim.x / G);
+  const int64_t tid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+  const int64_t W = tiles * K;
+  long long n_a = 0;  // insert: placed in a block; delete: removed
+  unsigned round = 0;
+
+  for (int64_t w0 = 0; w0 < n; w0 += W) {
+    OrdKey<OP> ks[K];
+#pragma unroll
+    for (int k = 0; k < K; k++) {
+      int64_t i = w0 + tid + (int64_t)k * tiles;
+      ks[k].pend = i < n;
+      if (ks[k].pend) {
+        KeyInfo ki = key_info(P, keys[i]);
+        ks[k].b1 = (uint32_t)ki.b1;
+        ks[k].b2 = (uint32_t)ki.b2;
+        ks[k].word = OP == 0 ? ((P.f >= 64 ? 0 : ((values ? values[i] : 0) << P.f)) | ki.tag) : ki.tag;
+      }
+    }
+    for (;;) {
+      // reserve: every pending key bids its input index on both blocks
+      if (t.lane == 0) {
+#pragma unroll
+        for (int k = 0; k < K; k++) {
+          if (!ks[k].pend) continue;
+          uint32_t idx = (uint32_t)(w0 + tid + (int64_t)k * tiles - w0);
+          atomicMin(&X.res[ks[k].b1], idx);
+          if (ks[k].b2 != ks[k].b1) atomicMin(&X.res[ks[k].b2], idx);
+        }
+      }
+      grid.sync();
+      bool left = false;
+#pragma unroll
+      for (int k = 0; k < K; k++) {
+        if (!ks[k].pend) continue;
+        int64_t i = w0 + tid + (int64_t)k * tiles;
+        uint32_t idx = (uint32_t)(i - w0);
+        int mine = 0;
+        if (t.lane == 0) mine = __ldcg(&X.res[ks[k].b1]) == idx && __ldcg(&X.res[ks[k].b2]) == idx;
+        mine = t.bcast(mine, 0);
+        if (!mine) {
+          left = true;
+          continue;
+        }
+        if (OP == 0) {
+          uint8_t code = commit_insert<S, G, BF>(P, t, ks[k].b1, ks[k].b2, ks[k].word);
+          if (t.lane == 0) {
+            if (code == 4) {
+              int64_t slot = atomicAdd(&X.ctl[2], 1u);
+              if (slot < X.defer_cap) {
+                X.defer_idx[slot] = i;
+                X.defer_fp[slot] = P.keys_are_fps ? keys[i] : mix64(keys[i] ^ P.seed);
+                X.defer_word[slot] = ks[k].word;
+                X.defer_pend[slot] = 1;
+              }
+            } else {
+              out[i] = code;
+              n_a++;
+            }
+          }
+        } else {
+          int ok = commit_delete<S, G, BF>(P, t, ks[k].b1, ks[k].b2, ks[k].word);
+          if (t.lane == 0) {
+            if (!ok && P.bsize) {
+              int64_t slot = atomicAdd(&X.ctl[2], 1u);
+              if (slot < X.defer_cap) {
+                X.defer_idx[slot] = i;
+                X.defer_fp[slot] = P.keys_are_fps ? keys[i] : mix64(keys[i] ^ P.seed);
+                X.defer_word[slot] = ks[k].word;
+                X.defer_pend[slot] = 1;
+              }
+            } else {
+              out[i] = ok ? 1 : 0;
+              n_a += ok;
+            }
+          }
+        }
+        if (t.lane == 0) {  // release both reservations (only the holder writes them now)
+          X.res[ks[k].b1] = kNoRes;
+          X.res[ks[k].b2] = kNoRes;
+        }
+        ks[k].pend = false;
+      }
+      bool any = cta_any(left);
+      if (threadIdx.x == 0) {
+        if (any) atomicAdd(&X.ctl[round & 1], 1u);
+        if (blockIdx.x == 0) X.ctl[(round + 1) & 1] = 0;
+      }
+      grid.sync();
+      unsigned cnt = __ldcg(&X.ctl[round & 1]);
+      round++;
+      if (cnt == 0) break;
+    }
+  }
+
+  // ---- backing phase: deferred keys in input-index order -------------------
+  grid.sync();
+  int64_t nd = (int64_t)__ldcg(&X.ctl[2]);
+  if (nd > X.defer_cap) nd = X.defer_cap;
+  S *bk = reinterpret_cast<S *>(P.backing);
+  long long n_b = 0;
+  if (nd > 0) {
+    for (;;) {
+      // reserve every position this key could still take: for inserts all
+      // free probe positions, for deletes all live matches before the chain
+      // ends (pk:104-117, pk:223-233)
+      for (int64_t e = tid; e < nd; e += tiles) {
+        if (t.lane != 0 || !X.defer_pend[e]) continue;
+        uint32_t idx = (uint32_t)X.defer_idx[e];
+        uint64_t fp = X.defer_fp[e], word = X.defer_word[e];
+        if (!P.bsize) continue;
+        uint64_t p = fmod64(mix64(fp ^ kBackStart), P.bsm);
+        uint64_t step = fmod64(mix64(fp ^ kBackStep) | 1, P.bsm);
+        for (int q = 0; q < P.probe_limit; q++) {
+          uint64_t w = load_slot<S, true>(bk + p);
+          if (OP == 0) {
+            if (!live_word(w)) atomicMin(&X.bres[p], idx);
+          } else {
+            if (w == 0) break;
+            if (w != 1 && (w & P.fmask) == word) atomicMin(&X.bres[p], idx);
+          }
+          p += step;
+          p = p >= P.bsize ? p - P.bsize : p;
+        }
+      }
+      grid.sync();
+      bool left = false;
+      for (int64_t e = tid; e < nd; e += tiles) {
+        if (t.lane != 0 || !X.defer_pend[e]) continue;
+        int64_t i = X.defer_idx[e];
+        uint32_t idx = (uint32_t)i;
+        uint64_t fp = X.defer_fp[e], word = X.defer_word[e];
+        int64_t target = -1;
+        if (P.bsize) {
+          uint64_t p = fmod64(mix64(fp ^ kBackStart), P.bsm);
+          uint64_t step = fmod64(mix64(fp ^ kBackStep) | 1, P.bsm);
+          for (int q = 0; q < P.probe_limit; q++) {
+            uint64_t w = load_slot<S, true>(bk + p);
+            if (OP == 0) {
+              if (!live_word(w)) { target = (int64_t)p; break; }
+            } else {
+              if (w == 0) break;
+              if (w != 1 && (w & P.fmask) == word) { target = (int64_t)p; break; }
+            }
+            p += step;
+            p = p >= P.bsize ? p - P.bsize : p;
+          }
+        }
+        if (target < 0) {  // nothing claimable now, nor ever in this batch
+          out[i] = OP == 0 ? kFull : 0;
+          X.defer_pend[e] = 0;
+          continue;
+        }
+        if (__ldcg(&X.bres[target]) != idx) {
+          left = true;
+          continue;
+        }
+        bk[target] = (S)(OP == 0 ? word : 1);
+        out[i] = OP == 0 ? kBacking : 1;
+        n_a++;
+        n_b += OP == 0;
+        X.defer_pend[e] = 0;
+        // release every reservation still carrying our index
+        uint64_t p = fmod64(mix64(fp ^ kBackStart), P.bsm);
+        uint64_t step = fmod64(mix64(fp ^ kBackStep) | 1, P.bsm);
+        for (int q = 0; q < P.probe_limit; q++) {
+          atomicCAS(&X.bres[p], idx, kNoRes);
+          p += step;
+          p = p >= P.bsize ? p - P.bsize : p;
+        }
+      }
+      bool any = cta_any(left);
+      if (threadIdx.x == 0) {
+        if (any) atomicAdd(&X.ctl[round & 1], 1u);
+        if (blockIdx.x == 0) X.ctl[(round + 1) & 1] = 0;
+      }
+      grid.sync();
+      unsigned cnt = __ldcg(&X.ctl[round & 1]);
+      round++;
+      if (cnt == 0) break;
+    }
+  }
+  if (t.lane == 0) {
+    if (OP == 0) {
+      if (n_a) atomicAdd((unsigned long long *)&counters[0], (unsigned long long)n_a);
+      if (n_b) atomicAdd((unsigned long long *)&counters[1], (unsigned long long)n_b);
+    } else if (n_a) {
+      atomicAdd((unsigned long long *)&counters[2], (unsigned long long)n_a);
+    }
+  }
+}
+
+// Dispatch over (G, compile-time B) for one slot type -------------------------
+// BF=16 is the vectorised fast path for the default/benchmarked geometry
+// (B=16); BF=32 the CG-32 sweep point (B=32, u16); everything else BF=0.
+constexpr int kOrdK = 4;
+
+template <typename S, int G, int BF, int OP>
+static int launch_ordered(const TcfDev &P, const uint64_t *keys, const uint64_t *values, int64_t n, uint8_t *out,
+                          int64_t *counters, OrdScratch X, cudaStream_t st) {
+  auto kern = k_tcf_ordered<S, G, BF, kOrdK, OP>;
+  int per_sm = 0;
+  FK_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
+  if (per_sm < 1) return FK_E_ARG;
+  int grid = per_sm * num_sms();
+  void *args[] = {(void *)&P, (void *)&keys, (void *)&values, (void *)&n, (void *)&out, (void *)&counters, (void *)&X};
+  FK_TRY(cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(256), args, 0, st));
+  return 0;
+}
+
+static inline int grid_for(int64_t n, int G) {
+  int64_t tiles_per_cta = 256 / G;
+  int64_t need = (n + tiles_per_cta - 1) / tiles_per_cta;
+  int64_t cap = (int64_t)num_sms() * 8;
+  if (need > cap) need = cap;
+  return (int)(need < 1 ? 1 : need);
+}
+
+enum TcfOp { kOpQuery = 0, kOpInsCas = 1, kOpDelCas = 2, kOpInsOrd = 3, kOpDelOrd = 4 };
+
+struct TcfCall {
+  const uint64_t *keys;
+  const uint64_t *values;
+  int64_t n;
+  uint8_t *out;
+  uint64_t *vals_out;
+  int64_t *counters;
+  OrdScratch X;
+};
+
+template <typename S, int G, int BF>
+static int tcf_run_gb(int op, const TcfDev &P, const TcfCall &c, cudaStream_t st) {
+  int grid = grid_for(c.n, G);
+  switch (op) {
+    case kOpQuery:
+      k_tcf_query<S, G, BF><<<grid, 256, 0, st>>>(P, c.keys, c.n, c.out, c.vals_out);
+      break;
+    case kOpInsCas:
+      k_tcf_insert_cas<S, G, BF><<<grid, 256, 0, st>>>(P, c.keys, c.values, c.n, c.out, c.counters);
+      break;
+    case kOpDelCas:
+      k_tcf_delete_cas<S, G, BF><<<grid, 256, 0, st>>>(P, c.keys, c.n, c.out, c.counters);
+      break;
+    case kOpInsOrd:
+      return launch_ordered<S, G, BF, 0>(P, c.keys, c.values, c.n, c.out, c.counters, c.X, st);
+    default:
+      return launch_ordered<S, G, BF, 1>(P, c.keys, nullptr, c.n, c.out, c.counters, c.X, st);
+  }
+  FK_CHECK_LAUNCH();
+  return 0;
+}
+
+template <typename S, int BF>
+static int tcf_run_b(int op, int G, const TcfDev &P, const TcfCall &c, cudaStream_t st) {
+  switch (G) {
+    case 1: return tcf_run_gb<S, 1, BF>(op, P, c, st);
+    case 2: return tcf_run_gb<S, 2, BF>(op, P, c, st);
+    case 4: return tcf_run_gb<S, 4, BF>(op, P, c, st);
+    case 8: return tcf_run_gb<S, 8, BF>(op, P, c, st);
+    case 16: return tcf_run_gb<S, 16, BF>(op, P, c, st);
+    default: return tcf_run_gb<S, 32, (BF == 16 ? 0 : BF)>(op, P, c, st);
+  }
+}
+
+// One explicit instantiation per slot type lives in tcf_point_s{1,2,4,8}.cu so
+// the (type x G x B) kernel matrix compiles in parallel.
+template <typename S>
+int tcf_run(int op, int G, int B, const TcfDev &P, const TcfCall &c, cudaStream_t st) {
+  if constexpr (sizeof(S) == 2) {
+    if (B == 16) return tcf_run_b<S, 16>(op, G, P, c, st);
+    if (B == 32) return tcf_run_b<S, 32>(op, G, P, c, st);
+  }
+  return tcf_run_b<S, 0>(op, G, P, c, st);
+}
+
+}  // namespace fk

@@ -1,0 +1,373 @@
+"""Two-choice filter, point API, on the B200.
+
+Drop-in for filterkit.tcf (/root/reference/pkg/src/filterkit/tcf.py:31-249):
+same ``Placement`` codes, ``TcfParams`` fields/validation/derivations, and
+``Tcf`` methods.  Table state lives in HBM as torch CUDA tensors; every
+insert/query/delete is one launch of the sm_100a kernels in
+csrc/tcf_point*.cu through the C ABI (include/filterkit_b200.h).
+
+Semantics of a batch call:
+
+* ``mode="ordered"`` (default): the result -- codes, table bit image, query
+  answers including false positives -- is bit-identical to the reference
+  processing the batch from one caller thread (``tcf_insert_batch`` loop,
+  _ckernels.pyx:210-237).
+* ``mode="concurrent"``: the paper's free-threaded CAS insert (Alg. 1): the
+  same placement policy applied by every key at once, i.e. the reference's
+  behaviour under many concurrent caller threads.  Faster; the placement
+  of keys that compete for a block is a race.
+
+Inputs may be numpy arrays (synchronous, results come back as numpy) or
+int64/uint64 CUDA tensors (asynchronous on the current stream, results stay
+on the device).
+"""
+
+from __future__ import annotations
+
+import math
+import threading
+from dataclasses import dataclass
+from enum import IntEnum
+
+import numpy as np
+
+from . import _lib
+from .errors import FilterFullError, ValidationError
+from .hashing import EMPTY, TOMBSTONE
+
+__all__ = ["Placement", "TcfParams", "Tcf"]
+
+
+class Placement(IntEnum):
+    """Where an insert landed (tcf.py:31-37)."""
+
+    PRIMARY = 0
+    SECONDARY = 1
+    BACKING = 2
+    FULL = 3
+
+
+def _slot_dtype(bits):
+    for dt in (np.uint8, np.uint16, np.uint32, np.uint64):
+        if bits <= np.dtype(dt).itemsize * 8:
+            return np.dtype(dt)
+    raise ValueError("slot width over 64 bits")
+
+
+@dataclass(frozen=True)
+class TcfParams:
+    """Geometry and hashing parameters (tcf.py:47-92, same defaults/checks)."""
+
+    num_blocks: int
+    block_slots: int = 16
+    tag_bits: int = 16
+    slot_bits: int = 16
+    seed: int = 0
+    backing_fraction: float = 0.01
+    probe_limit: int = 20
+    shortcut_fraction: float = 0.75
+    group_width: int = 1
+
+    def __post_init__(self):
+        if self.num_blocks < 1:
+            raise ValueError("num_blocks must be positive")
+        if self.block_slots < 1:
+            raise ValueError("block_slots must be positive")
+        if not 2 < self.tag_bits <= self.slot_bits:
+            raise ValueError("need 2 < tag_bits <= slot_bits")
+        if self.block_slots * self.slot_bits > 1024:
+            raise ValueError("block exceeds 1024 bits (block_slots * slot_bits)")
+        if not 1 <= self.group_width <= self.block_slots:
+            raise ValueError("group_width must be in [1, block_slots]")
+        if not 0.0 <= self.backing_fraction <= 1.0:
+            raise ValueError("backing_fraction must be in [0, 1]")
+        if not 0.0 < self.shortcut_fraction <= 1.0:
+            raise ValueError("shortcut_fraction must be in (0, 1]")
+
+    @property
+    def value_bits(self):
+        return self.slot_bits - self.tag_bits
+
+    @property
+    def main_slots(self):
+        return self.num_blocks * self.block_slots
+
+    @property
+    def backing_slots(self):
+        # Python round() (half-to-even) on a float, exactly as tcf.py:86-87
+        return int(round(self.main_slots * self.backing_fraction))
+
+    @property
+    def cut_slots(self):
+        return math.ceil(self.shortcut_fraction * self.block_slots)
+
+    @property
+    def tile_width(self):
+        """Cooperative-group tile the kernels use: group_width rounded down to
+        a power of two (results never depend on it, _pykernels.py:86-91)."""
+        g = 1
+        while g * 2 <= min(self.group_width, 32):
+            g *= 2
+        return g
+
+
+_MODES = {"ordered": _lib.FK_ORDERED, "concurrent": _lib.FK_CONCURRENT}
+
+
+def _check_backend(backend):
+    if backend not in ("auto", "cuda", "c"):
+        if backend == "py":
+            raise RuntimeError("the pure-Python backend does not exist in the B200 build")
+        raise ValueError("unknown backend %r (expected 'auto' or 'cuda')" % (backend,))
+
+
+class _DeviceTables:
+    """Named device byte buffers with lazily synced host mirrors.
+
+    Reading ``_blocks`` & co. returns a host numpy copy (D2H on first access
+    after a device write).  Tests in the reference mutate those arrays in
+    place; a handed-out mirror is therefore pushed back (H2D)
+    before the next device operation.
+    """
+
+    def __init__(self, torch, device, spec):
+        self.torch, self.device = torch, device
+        self.spec = dict(spec)  # name -> (dtype, count)
+        self.dev = {n: torch.zeros(max(1, c * np.dtype(dt).itemsize), dtype=torch.uint8, device=device)
+                    for n, (dt, c) in self.spec.items()}
+        self.mirror = {}
+        self.lent = set()
+
+    def ptr(self, name):
+        dt, c = self.spec[name]
+        return _lib.dptr(self.dev[name]) if c else _lib.c_vp(0)
+
+    def host(self, name):
+        if name not in self.mirror:
+            dt, c = self.spec[name]
+            self.mirror[name] = _lib.host_view(self.torch, self.dev[name], dt)[:c] if c else \
+                np.zeros(0, dtype=dt)
+        self.lent.add(name)
+        return self.mirror[name]
+
+    def before_device_op(self):
+        for name in self.lent:
+            dt, c = self.spec[name]
+            if c:
+                src = self.torch.from_numpy(np.ascontiguousarray(self.mirror[name]).view(np.uint8).copy())
+                self.dev[name][: src.numel()].copy_(src.to(self.device))
+        self.lent.clear()
+
+    def after_device_write(self):
+        self.mirror.clear()
+
+
+class Tcf:
+    """Two-choice filter with point (per-key) operations on the B200."""
+
+    def __init__(self, params=None, *, backend="auto", mode="ordered", device=None, **kwargs):
+        if params is None:
+            params = TcfParams(**kwargs)
+        elif kwargs:
+            raise TypeError("pass either params or keyword fields, not both")
+        _check_backend(backend)
+        if mode not in _MODES:
+            raise ValueError("mode must be 'ordered' or 'concurrent'")
+        self.params = params
+        self.mode = mode
+        torch = _lib.require_cuda()
+        self._torch = torch
+        self._device = torch.device(device) if device is not None else \
+            torch.device("cuda", torch.cuda.current_device())
+        self._lib = _lib.load()
+        p = params
+        dt = _slot_dtype(p.slot_bits)
+        self._dtype = dt
+        self._t = _DeviceTables(torch, self._device, {
+            "blocks": (dt, p.main_slots), "backing": (dt, p.backing_slots)})
+        self._counters_dev = torch.zeros(3, dtype=torch.int64, device=self._device)
+        self._geom = _lib.TcfGeom(p.num_blocks, p.backing_slots, p.block_slots, p.tag_bits,
+                                  dt.itemsize, p.cut_slots, p.probe_limit, p.tile_width,
+                                  p.seed & ((1 << 64) - 1))
+        self._op_lock = threading.Lock()
+
+    @property
+    def backend(self):
+        return "cuda"
+
+    # -- private host mirrors (reference tests read/mutate these) -----------
+    @property
+    def _blocks(self):
+        return self._t.host("blocks")
+
+    @property
+    def _backing(self):
+        return self._t.host("backing")
+
+    # -- plumbing -------------------------------------------------------------
+    def _keys_in(self, keys):
+        torch = self._torch
+        on_dev = isinstance(keys, torch.Tensor) and keys.is_cuda
+        return _lib.to_device_u64(torch, keys, self._device), on_dev
+
+    def _check_values(self, values, n, on_dev):
+        torch = self._torch
+        if values is None:
+            return None
+        vb = self.params.value_bits
+        if isinstance(values, torch.Tensor):
+            v = _lib.to_device_u64(torch, values, self._device)
+            if v.numel() != n:
+                raise ValueError("values length does not match keys length")
+            if vb < 64 and n:
+                bad = (v.view(torch.int64) >> vb) != 0 if vb > 0 else v != 0
+                if bool(bad.any()):
+                    raise ValueError("value does not fit in %d bits" % vb)
+            return v
+        vals = np.ascontiguousarray(values, dtype=np.uint64).reshape(-1)
+        if len(vals) != n:
+            raise ValueError("values length does not match keys length")
+        if vb < 64 and len(vals) and int(vals.max()) >> vb:
+            raise ValueError("value does not fit in %d bits" % vb)
+        return _lib.to_device_u64(torch, vals, self._device)
+
+    def _workspace(self, n, mode):
+        nbytes = self._lib.fk_tcf_workspace_bytes(ctypes_byref(self._geom), n, mode)
+        if not nbytes:
+            return None, 0
+        return self._torch.empty(nbytes, dtype=self._torch.uint8, device=self._device), nbytes
+
+    def _out(self, t, on_dev, dtype=None):
+        if on_dev:
+            return t
+        a = t.cpu().numpy()
+        return a if dtype is None else a.view(dtype)
+
+    # -- point operations -------------------------------------------------------
+    def insert(self, key, value=0):
+        code = int(self.insert_many([key], [value])[0])
+        if code == Placement.FULL:
+            raise FilterFullError("no free slot in either block or backing table")
+        return Placement(code)
+
+    def insert_many(self, keys, values=None):
+        """Insert a batch; returns a Placement code per key (no raise)."""
+        torch = self._torch
+        k, on_dev = self._keys_in(keys)
+        n = k.numel()
+        v = self._check_values(values, n, on_dev)
+        codes = torch.empty(n, dtype=torch.uint8, device=self._device)
+        if n:
+            mode = _MODES[self.mode]
+            with self._op_lock:
+                self._t.before_device_op()
+                ws, wsb = self._workspace(n, mode)
+                rc = self._lib.fk_tcf_insert(
+                    ctypes_byref(self._geom), self._t.ptr("blocks"), self._t.ptr("backing"),
+                    _lib.dptr(k), 0, _lib.dptr(v), n, _lib.dptr(codes), _lib.dptr(self._counters_dev),
+                    mode, _lib.dptr(ws), wsb, _lib.stream_ptr(torch))
+                _lib.check(rc, "tcf insert")
+                self._t.after_device_write()
+        return self._out(codes, on_dev)
+
+    def query(self, key):
+        return bool(self.query_many([key])[0])
+
+    def query_value(self, key):
+        found, values = self.query_values_many([key])
+        return bool(found[0]), int(values[0])
+
+    def query_many(self, keys):
+        return self.query_values_many(keys)[0]
+
+    def query_values_many(self, keys):
+        torch = self._torch
+        k, on_dev = self._keys_in(keys)
+        n = k.numel()
+        found = torch.empty(n, dtype=torch.uint8, device=self._device)
+        vals = torch.empty(n, dtype=torch.int64, device=self._device)
+        if n:
+            with self._op_lock:
+                self._t.before_device_op()
+                rc = self._lib.fk_tcf_query(
+                    ctypes_byref(self._geom), self._t.ptr("blocks"), self._t.ptr("backing"),
+                    _lib.dptr(k), 0, n, _lib.dptr(found), _lib.dptr(vals), _lib.stream_ptr(torch))
+                _lib.check(rc, "tcf query")
+        if on_dev:
+            return found.bool(), vals
+        return found.cpu().numpy().astype(bool), vals.cpu().numpy().view(np.uint64)
+
+    def delete(self, key):
+        return bool(self.delete_many([key])[0])
+
+    def delete_many(self, keys):
+        torch = self._torch
+        k, on_dev = self._keys_in(keys)
+        n = k.numel()
+        removed = torch.empty(n, dtype=torch.uint8, device=self._device)
+        if n:
+            mode = _MODES[self.mode]
+            with self._op_lock:
+                self._t.before_device_op()
+                ws, wsb = self._workspace(n, mode)
+                rc = self._lib.fk_tcf_delete(
+                    ctypes_byref(self._geom), self._t.ptr("blocks"), self._t.ptr("backing"),
+                    _lib.dptr(k), 0, n, _lib.dptr(removed), _lib.dptr(self._counters_dev), mode,
+                    _lib.dptr(ws), wsb, _lib.stream_ptr(torch))
+                _lib.check(rc, "tcf delete")
+                self._t.after_device_write()
+        if on_dev:
+            return removed.bool()
+        return removed.cpu().numpy().astype(bool)
+
+    # -- inspection (quiescent; host mirrors) ------------------------------------
+    def items(self):
+        p = self.params
+        fmask = (1 << p.tag_bits) - 1
+        out = []
+        blocks, backing = self._blocks, self._backing
+        for i in np.flatnonzero(blocks > TOMBSTONE).tolist():
+            w = int(blocks[i])
+            out.append((i // p.block_slots, w & fmask, w >> p.tag_bits))
+        for i in np.flatnonzero(backing > TOMBSTONE).tolist():
+            w = int(backing[i])
+            out.append((-1, w & fmask, w >> p.tag_bits))
+        return out
+
+    def occupancy(self, block_index):
+        p = self.params
+        blk = self._blocks[block_index * p.block_slots:(block_index + 1) * p.block_slots]
+        return int((blk > TOMBSTONE).sum())
+
+    def load_factor(self):
+        return float((self._blocks > TOMBSTONE).sum()) / self.params.main_slots
+
+    def size_bits(self):
+        p = self.params
+        return (p.main_slots + p.backing_slots) * self._dtype.itemsize * 8
+
+    @property
+    def counters(self):
+        c = self._counters_dev.cpu().tolist()
+        return {"inserts_ok": int(c[0]), "inserts_backing": int(c[1]), "deletes_ok": int(c[2])}
+
+    def validate(self):
+        """Structural invariants (tcf.py:232-249); raises ValidationError."""
+        p = self.params
+        fmask = np.uint64((1 << p.tag_bits) - 1 if p.tag_bits < 64 else (1 << 64) - 1)
+        used_total = 0
+        for name, arr in (("main", self._blocks), ("backing", self._backing)):
+            used = arr[arr > TOMBSTONE].astype(np.uint64)
+            if len(used) and int((used & fmask).min()) < 2:
+                raise ValidationError("%s table holds a used slot with a reserved tag" % name)
+            used_total += len(used)
+        c = self.counters
+        expect = c["inserts_ok"] - c["deletes_ok"]
+        if used_total != expect:
+            raise ValidationError("stored slots (%d) do not match inserts-deletes (%d)"
+                                  % (used_total, expect))
+
+
+def ctypes_byref(x):
+    import ctypes
+    return ctypes.byref(x)

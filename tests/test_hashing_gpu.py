@@ -1,0 +1,65 @@
+"""Device hashing is bit-identical to the reference's host hashing."""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _run_streams(keys, seed, bits, nb, bs):
+    import torch
+    from paper_2212_09005_b200 import _lib
+    lib = _lib.load()
+    k = torch.from_numpy(np.ascontiguousarray(keys, np.uint64).view(np.int64)).cuda()
+    out = torch.empty(5 * len(keys), dtype=torch.int64, device="cuda")
+    _lib.check(lib.fk_hash_streams(_lib.dptr(k), len(keys), seed, bits, nb, bs, _lib.dptr(out), None), "hash")
+    torch.cuda.synchronize()
+    return out.cpu().numpy().view(np.uint64).reshape(-1, 5)
+
+
+def test_streams_match_golden(golden):
+    h = golden("hashing")
+    ks = h["keys"]
+    for nb in (1, 100, 8192, 65536, 2 ** 24, 1000003):
+        for bs in (10486, 2684355, 7):
+            got = _run_streams(ks, 9, 64, nb, bs)
+            assert np.array_equal(got[:, 0], h["fp_s9"])
+            assert np.array_equal(got[:, 1], h["b1_%d" % nb])
+            assert np.array_equal(got[:, 2], h["b2_%d" % nb])
+            assert np.array_equal(got[:, 3], h["bstart_%d" % bs])
+            assert np.array_equal(got[:, 4], h["bstep_%d" % bs])
+    for bits in (30, 36, 40):
+        assert np.array_equal(_run_streams(ks, 0, bits, 0, 0)[:, 0], h["fpbits_%d" % bits])
+
+
+def test_streams_match_oracle_10m(oracle):
+    from conftest import counter_keys
+    ks = counter_keys(77, 10_000_000)
+    got = _run_streams(ks, 12345, 64, 2 ** 24, 2684355)
+    fp = oracle.fingerprint_many(ks, 12345)
+    b1, b2 = oracle.potc_pair_many(fp, 2 ** 24)
+    assert np.array_equal(got[:, 0], fp)
+    assert np.array_equal(got[:, 1], b1) and np.array_equal(got[:, 2], b2)
+    with np.errstate(over="ignore"):
+        st = oracle.mix64_many(fp ^ np.uint64(oracle.C_BACK_START)) % np.uint64(2684355)
+        sp = (oracle.mix64_many(fp ^ np.uint64(oracle.C_BACK_STEP)) | np.uint64(1)) % np.uint64(2684355)
+    assert np.array_equal(got[:, 3], st) and np.array_equal(got[:, 4], sp)
+
+
+@pytest.mark.parametrize("d", [1, 2, 3, 7, 100, 10486, 65536, 2684355, 1000003, 2 ** 32 - 1, 2 ** 32 + 1,
+                               2 ** 63 + 12345, 2 ** 64 - 1, 0x9E3779B97F4A7C15])
+def test_fastmod_exact(d):
+    import torch
+    from paper_2212_09005_b200 import _lib
+    lib = _lib.load()
+    rng = np.random.default_rng(d % 1000)
+    x = np.concatenate([rng.integers(0, 2 ** 64, 1_000_000, dtype=np.uint64, endpoint=False),
+                        np.array([v % 2 ** 64 for v in (0, 1, d - 1, d, d + 1, 2 ** 64 - 1, 2 ** 64 - 2,
+                                                        (2 ** 64 - 1) // d * d)], dtype=np.uint64)])
+    xt = torch.from_numpy(x.view(np.int64)).cuda()
+    out = torch.empty_like(xt)
+    _lib.check(lib.fk_fastmod_check(_lib.dptr(xt), len(x), d, _lib.dptr(out), None), "fastmod")
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy().view(np.uint64), x % np.uint64(d))
