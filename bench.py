@@ -1,0 +1,404 @@
+#!/usr/bin/env python
+"""Benchmark: point TCF insert/query/delete ops/s at 0.9 load on B200.
+
+Workload (BASELINE.json configs[2], "C3"): a point two-choice filter with
+2^28 slots per GPU (num_blocks = 2^24, B = 16, 16-bit tags, 1% backing),
+uniform 64-bit keys (the reference's counter_stream).  One step =
+  reset table -> insert 0.9*2^28 keys -> query them (positive) ->
+  query 0.9*2^28 fresh keys (negative) -> delete the inserted keys
+so a step is 4 * 241,591,910 = 966,367,640 ops per GPU.  `value` is whole-job
+ops/s over all ranks with keys already resident in HBM; `e2e` is the same
+step through the public API from pinned host buffers (H2D of every key batch
+and D2H of every result inside the timed region).  Inputs (1.9 GB key
+arrays) and the 512 MiB table are larger than the 126 MB L2, so no flush is
+needed between steps.
+
+Multi-GPU (torchrun, one rank per GPU): weak scaling -- each rank owns a
+2^28-slot sub-filter; keys are generated per rank and routed by the top
+log2(N) fingerprint bits with an NCCL all-to-all.
+
+`--impl reference` times the reference's own compiled kernels
+(oracle/_ref, built from /root/reference/pkg/src/filterkit/_ckernels.pyx)
+on the host's cores for the same metric.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "insert/query/delete ops/sec at 0.9 load (1/2/4/8 B200) + % HBM random-access roofline"
+UNIT = "ops/s"
+TAG_UNIFORM = 0x5851F42D4C957F2D
+TAG_FPR = 0xB504F32D4F2D8C21
+
+# Algorithmic bytes per op at 0.9 load: 8-B key, 32-B block
+# sectors (b2 read on 26.0% of inserts, 14.37% of positive queries), one
+# dirty 32-B sector written back per insert/delete, 1-B result.
+BYTES_PER_OP = {
+    "insert": 8 + 32 * (1 + 0.260) + 32 + 1,       # 81.3
+    "query_pos": 8 + 32 * (1 + 0.1437) + 1,         # 45.6
+    "query_neg": 8 + 64 + 1,                        # 73
+    "delete": 8 + 32 * (1 + 0.1437) + 32 + 1,       # 77.6
+}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown," \
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, index):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS, "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def counter_stream(seed, tag, n):
+    from paper_2212_09005_b200.workloads import counter_stream as cs
+    return cs(seed, tag, n)
+
+
+def device_keys(torch, seed, tag, n, device):
+    """Same keys as counter_stream, generated on the device (chunked numpy
+    would take seconds at 2^28 scale; this is setup, not timed)."""
+    from paper_2212_09005_b200.hashing import mix64
+    base = mix64((seed ^ tag) & ((1 << 64) - 1))
+    out = torch.empty(n, dtype=torch.int64, device=device)
+    step = 1 << 26
+    for lo in range(0, n, step):
+        m = min(step, n - lo)
+        x = torch.arange(lo, lo + m, dtype=torch.int64, device=device) + np.int64(np.uint64(base).view(np.int64))
+        # SplitMix64 finalizer in int64 arithmetic (wrapping), logical shifts via masks
+        def lsr(v, s):
+            return (v >> s) & ((1 << (64 - s)) - 1)
+        x = x ^ lsr(x, 30)
+        x = x * np.int64(np.uint64(0xBF58476D1CE4E5B9).view(np.int64))
+        x = x ^ lsr(x, 27)
+        x = x * np.int64(np.uint64(0x94D049BB133111EB).view(np.int64))
+        x = x ^ lsr(x, 31)
+        out[lo:lo + m] = x
+    return out
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    from paper_2212_09005_b200 import Tcf
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    log_slots = args.log_slots
+    nb = (1 << log_slots) // 16
+    n = int(args.load * (1 << log_slots))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+    # per-rank disjoint key streams
+    keys = device_keys(torch, 1 + 1000 * rank, TAG_UNIFORM, n, dev)
+    negs = device_keys(torch, 2 + 1000 * rank, TAG_FPR, n, dev)
+
+    if world > 1:
+        from paper_2212_09005_b200.sharding import ShardedTcf
+        filt = ShardedTcf(num_blocks=nb, group_width=args.group_width, mode=args.mode)
+    else:
+        filt = Tcf(num_blocks=nb, group_width=args.group_width, mode=args.mode)
+
+    ops = ("insert", "query_pos", "query_neg", "delete")
+    stream = torch.cuda.current_stream()
+
+    def step(ev=None):
+        filt._reset()
+        if ev:
+            ev[0].record(stream)
+        codes = filt.insert_many(keys)
+        if ev:
+            ev[1].record(stream)
+        fpos = filt.query_many(keys)
+        if ev:
+            ev[2].record(stream)
+        fneg = filt.query_many(negs)
+        if ev:
+            ev[3].record(stream)
+        rem = filt.delete_many(keys)
+        if ev:
+            ev[4].record(stream)
+        return codes, fpos, fneg, rem
+
+    for _ in range(args.warmup):
+        codes, fpos, fneg, rem = step()
+    torch.cuda.synchronize()
+    # sanity (outside timing): nothing FULL, no false negatives
+    n_full = int((codes == 3).sum())
+    n_fn = int((~fpos).sum())
+    fpr = float(fneg.float().mean())
+    n_rem = int(rem.sum())
+
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        t0.record(stream)
+        for s in range(args.steps):
+            step(evs[s])
+        t1.record(stream)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ms_total = t0.elapsed_time(t1)
+    per_op_ms = {op: float(np.mean([evs[s][i].elapsed_time(evs[s][i + 1]) for s in range(args.steps)]))
+                 for i, op in enumerate(ops)}
+    if dist:
+        t = torch.tensor([ms_total], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    total_ops = 4 * n * world
+    value = total_ops / (ms_step / 1e3)
+
+    # ---- end to end through the public API from pinned host memory ----------
+    e2e = None
+    if not args.no_e2e:
+        hk = torch.empty(n, dtype=torch.int64, pin_memory=True)
+        hn = torch.empty(n, dtype=torch.int64, pin_memory=True)
+        hk.copy_(keys.cpu())
+        hn.copy_(negs.cpu())
+        e2e_steps = max(1, min(args.steps, 3))
+
+        def e2e_step():
+            filt._reset()
+            c = filt.insert_many(hk)
+            fp_ = filt.query_many(hk)
+            fn_ = filt.query_many(hn)
+            r = filt.delete_many(hk)
+            return c, fp_, fn_, r
+        e2e_step()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ts = time.perf_counter()
+        for _ in range(e2e_steps):
+            e2e_step()
+        torch.cuda.synchronize()
+        te = (time.perf_counter() - ts) / e2e_steps
+        if dist:
+            t = torch.tensor([te], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            te = float(t.item())
+        e2e = {"value": total_ops / te, "unit": UNIT, "h2d_bytes_per_step": 4 * 8 * n,
+               "d2h_bytes_per_step": 4 * n, "ms_per_step": te * 1e3}
+        del hk, hn
+
+    peak, peak_kind = peaks()
+    dom = max(per_op_ms, key=per_op_ms.get)
+    per_op = {}
+    for op in ops:
+        gbs = BYTES_PER_OP[op] * n / (per_op_ms[op] / 1e3) / 1e9
+        per_op[op] = {"ops_per_s": n / (per_op_ms[op] / 1e3), "ms": per_op_ms[op],
+                      "achieved_gbs": gbs, "frac_of_%s_hbm" % peak_kind: gbs / peak}
+    achieved = BYTES_PER_OP[dom] * n / (per_op_ms[dom] / 1e3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        tr = json.load(open(prof)).get(args.mode, {}).get(dom)
+        traffic = tr
+    launches_per_step = 4 if world == 1 else None
+    result = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u16", "data": "synthetic",
+        "config": {"workload": "C3: point TCF, 2^%d slots/GPU (nb=2^%d x B=16, 16-bit tags, 1%% backing), "
+                               "uniform 64-bit keys, insert+pos query+neg query+delete at %.2f load"
+                               % (log_slots, log_slots - 4, args.load),
+                   "keys_per_op_per_gpu": n, "mode": args.mode, "group_width": args.group_width,
+                   "l2": "inputs (%.1f GB keys) and table (%d MiB) exceed the 126 MB L2; no flush"
+                         % (8 * n / 1e9, (1 << log_slots) * 2 >> 20),
+                   "parallelism": "hash-prefix shards, NCCL all-to-all" if world > 1 else "single GPU"},
+        "per_op": per_op,
+        "roofline": {"bound": "hbm", "kernel": "tcf_" + dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                     "bytes_per_op": BYTES_PER_OP[dom]},
+        "e2e": e2e,
+        "gpu_launches": (launches_per_step * args.steps) if launches_per_step else None,
+        "clocks": clk.summary(),
+        "checks": {"full_codes": n_full, "false_negatives": n_fn, "neg_fpr": fpr, "removed": n_rem},
+    }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        result["cpu_baseline"] = cpu_baseline(args.cpu_budget_s)
+    return result if rank == 0 else None
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline / reference arm: the reference's own compiled kernels
+# ---------------------------------------------------------------------------
+
+def _ref_step(log_slots, load, threads, seed=1):
+    from oracle import ref_model
+    nb = (1 << log_slots) // 16
+    n = int(load * (1 << log_slots))
+    bs = int(round(nb * 16 * 0.01))
+    keys = counter_stream(seed, TAG_UNIFORM, n)
+    negs = counter_stream(seed + 1, TAG_FPR, n)
+    f = ref_model.RefTcf(nb, backing_slots=bs)
+    t = time.perf_counter()
+    f.insert_many(keys, threads)
+    f.query_many(keys, threads)
+    f.query_many(negs, threads)
+    f.delete_many(keys, threads)
+    dt = time.perf_counter() - t
+    return 4 * n, dt
+
+
+def _ref_kind():
+    from oracle import ref_model
+    return "reference" if ref_model.available() else None
+
+
+def cpu_baseline(budget_s=15.0):
+    """The reference's compiled _ckernels on all host cores, on a bounded
+    sample: the same workload shape with the table scaled down so the run
+    takes about budget_s."""
+    if _ref_kind() is None:
+        return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                "sample": "unavailable: oracle/_ref not built"}
+    threads = os.cpu_count() or 1
+    ops, dt = _ref_step(20, 0.9, threads)
+    rate = ops / dt
+    log_slots = 20
+    while log_slots < 28 and 4 * 0.9 * (1 << (log_slots + 1)) / rate < budget_s:
+        log_slots += 1
+    ops, dt = _ref_step(log_slots, 0.9, threads)
+    return {"value": ops / dt, "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": "reference _ckernels (oracle/_ref), point TCF 2^%d slots at 0.9 load, insert+pos+neg+delete "
+                      "(%d ops, %.1f s), %d threads slicing keys like fk/bench.py:86-97"
+                      % (log_slots, ops, dt, threads)}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    if _ref_kind() is None:
+        return {"impl": "reference", "unavailable": "oracle/_ref (reference _ckernels build) not present"}
+    threads = os.cpu_count() or 1
+    # size the per-step sample so that W+K steps finish in a few minutes
+    ops, dt = _ref_step(20, args.load, threads)
+    rate = ops / dt
+    log_slots = 20
+    per_step_budget = max(2.0, 150.0 / max(1, args.steps + args.warmup))
+    while log_slots < args.log_slots and 4 * args.load * (1 << (log_slots + 1)) / rate < per_step_budget:
+        log_slots += 1
+    for _ in range(args.warmup):
+        _ref_step(log_slots, args.load, threads)
+    tot_ops, tot_t = 0, 0.0
+    for s in range(args.steps):
+        o, t = _ref_step(log_slots, args.load, threads, seed=1 + s)
+        tot_ops += o
+        tot_t += t
+    value = tot_ops / tot_t
+    sample = ("reference _ckernels (oracle/_ref), point TCF 2^%d slots at %.2f load, insert+pos+neg+delete per step, "
+              "%d threads" % (log_slots, args.load, threads))
+    return {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u16",
+            "data": "synthetic",
+            "config": {"workload": "C3 (scaled sample): point TCF, 2^%d slots, uniform keys, insert+query+delete"
+                                   % log_slots},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--log-slots", type=int, default=28)
+    ap.add_argument("--load", type=float, default=0.9)
+    ap.add_argument("--group-width", type=int, default=1)
+    ap.add_argument("--mode", choices=["ordered", "concurrent"], default="ordered")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=15.0)
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        res = run_reference(args, rank, world)
+    else:
+        if world > 1:
+            import torch
+            import torch.distributed as dist
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        res = run_ours(args, rank, world, local_rank)
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+    if res is not None:
+        print(json.dumps(res))
+
+
+if __name__ == "__main__":
+    main()

@@ -64,6 +64,12 @@ typedef struct fk_tcf_geom {
 const char *fk_version(void);
 int fk_abi_version(void);
 
+/* Per-device setup, called once per device by the facades: sets the L2 fetch
+ * granularity hint (cudaLimitMaxL2FetchGranularity) to l2_fetch_bytes (32 by
+ * default: every filter probe is a random 32-byte sector); <= 0 leaves it. */
+int fk_device_setup(int l2_fetch_bytes);
+int fk_device_l2_fetch_bytes(void);
+
 /* Device fingerprints (hashing.py:66-73) + TCF/GQF derived streams, for the
  * hashing parity tests.  out5 gets per key: fp, b1, b2, backing start,
  * backing step (nb/bsize = 0 skips the corresponding columns). */
@@ -94,6 +100,69 @@ int fk_tcf_query(const fk_tcf_geom *g, const void *blocks, const void *backing,
 int fk_tcf_delete(const fk_tcf_geom *g, void *blocks, void *backing, const uint64_t *keys,
                   int keys_are_fps, int64_t n, uint8_t *removed, int64_t *counters, int mode,
                   void *workspace, size_t ws_bytes, void *stream);
+
+/* ---- GQF (counting quotient filter) ------------------------------------- */
+
+/* Geometry, derived on the host exactly as GqfParams (gqf.py:52-95). */
+typedef struct fk_gqf_geom {
+    int32_t q, r;              /* 2^q logical slots; r in {8,16,32}; q + r <= 64 */
+    int64_t phys;              /* 2^q + min(8192, 2^q) */
+    int64_t num_regions;       /* ceil(phys / 8192) */
+    int64_t quotient_regions;  /* ceil(2^q / 8192) */
+    int64_t max_occupied;      /* int(max_load * 2^q) */
+    uint64_t seed;
+} fk_gqf_geom;
+
+/* One table image (all device pointers).  slots/occupieds/runends/offsets/
+ * stats are bit-identical to the reference's _slots/_occupieds/_runends/
+ * _offsets/_stats (gqf.py:111-117); spill (one uint32 per 64 quotients) is a
+ * derived run index owned by this library. */
+typedef struct fk_gqf_tables {
+    void *slots;
+    uint64_t *occupieds;
+    uint64_t *runends;
+    int32_t *offsets;
+    int64_t *stats;
+    uint32_t *spill;
+} fk_gqf_tables;
+
+/* Outcome of a mutation (host struct). */
+typedef struct fk_gqf_result {
+    int32_t code;        /* 0, GQF_LOAD_CAPACITY=1, GQF_SHIFT_BOUND=2 */
+    int32_t swapped;     /* 1: the new image is in `next` (canonical rebuild); 0: `cur` was updated in place */
+    int64_t fail_index;  /* point inserts: index of the first failing key (gqf_insert_batch's fail_idx) */
+    int64_t fail_region; /* bulk inserts: first failing region in even/odd processing order */
+    int64_t shifted;     /* shift-work instrumentation (gqf.py:139-142) */
+} fk_gqf_result;
+
+#define FK_GQF_INSERT 0
+#define FK_GQF_DELETE 1
+#define FK_ORDER_POINT 0 /* items in input order (insert_many / delete_many) */
+#define FK_ORDER_BULK 1  /* sorted, even/odd regions, descending deletes (gqf.py:293-353) */
+
+/* replaces gqf_count_batch (_ckernels.pyx:1205-1250); asynchronous. */
+int fk_gqf_count(const fk_gqf_geom *g, const fk_gqf_tables *t, const uint64_t *keys, int keys_are_fps,
+                 int64_t n, uint64_t *counts, void *stream);
+
+/* replaces gqf_find_run (_ckernels.pyx:754-787): se[2i], se[2i+1] = start, end
+ * or -1, -1 when the quotient is unoccupied; asynchronous. */
+int fk_gqf_find_run(const fk_gqf_geom *g, const fk_gqf_tables *t, const int64_t *quotients, int64_t n,
+                    int64_t *se, void *stream);
+
+/* Rebuild the derived spill index from occupieds/runends (after the host
+ * wrote the image); asynchronous. */
+int fk_gqf_rebuild_index(const fk_gqf_geom *g, const fk_gqf_tables *t, void *stream);
+
+/* replaces gqf_insert_batch / gqf_delete_batch (_ckernels.pyx:1147-1202,
+ * 1253-1296) together with the facade loops around them (gqf.py:169-216,
+ * 293-371).  op = FK_GQF_INSERT / FK_GQF_DELETE; order = FK_ORDER_POINT /
+ * FK_ORDER_BULK; deltas NULL = 1 (insert) or 2^63 (delete = all copies);
+ * found (deletes) receives per-key flags in input order.  Synchronises the
+ * stream (the result is returned to the host); allocates stream-ordered
+ * scratch with cudaMallocAsync sized to the batch. */
+int fk_gqf_apply(const fk_gqf_geom *g, const fk_gqf_tables *cur, const fk_gqf_tables *next,
+                 const uint64_t *keys, int keys_are_fps, const uint64_t *deltas, int64_t n, int op, int order,
+                 uint8_t *found, fk_gqf_result *result, void *stream);
 
 #ifdef __cplusplus
 }

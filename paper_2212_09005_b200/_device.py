@@ -1,0 +1,88 @@
+"""Device-resident table buffers with host mirrors, shared by the facades."""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+
+
+def check_backend(backend):
+    if backend not in ("auto", "cuda", "c"):
+        if backend == "py":
+            raise RuntimeError("the pure-Python backend does not exist in the B200 build")
+        raise ValueError("unknown backend %r (expected 'auto' or 'cuda')" % (backend,))
+
+
+class DeviceTables:
+    """Named device byte buffers with lazily synced host mirrors.
+
+    Reading ``_blocks`` & co. returns a host numpy copy (D2H on first access
+    after a device write).  Tests in the reference mutate those arrays in
+    place; a handed-out mirror is therefore pushed back (H2D)
+    before the next device operation.
+    """
+
+    def __init__(self, torch, device, spec):
+        self.torch, self.device = torch, device
+        self.spec = dict(spec)  # name -> (dtype, count)
+        self.dev = {n: torch.zeros(max(1, c * np.dtype(dt).itemsize), dtype=torch.uint8, device=device)
+                    for n, (dt, c) in self.spec.items()}
+        self.mirror = {}
+        self.lent = set()
+
+    def ptr(self, name):
+        dt, c = self.spec[name]
+        return _lib.dptr(self.dev[name]) if c else _lib.c_vp(0)
+
+    def host(self, name):
+        if name not in self.mirror:
+            dt, c = self.spec[name]
+            self.mirror[name] = _lib.host_view(self.torch, self.dev[name], dt)[:c] if c else \
+                np.zeros(0, dtype=dt)
+        self.lent.add(name)
+        return self.mirror[name]
+
+    def before_device_op(self):
+        """Push handed-out mirrors back; returns True if any was pushed."""
+        pushed = False
+        for name in self.lent:
+            dt, c = self.spec[name]
+            if c:
+                src = self.torch.from_numpy(np.ascontiguousarray(self.mirror[name]).view(np.uint8).copy())
+                self.dev[name][: src.numel()].copy_(src.to(self.device))
+                pushed = True
+        self.lent.clear()
+        return pushed
+
+    def zero(self):
+        for t in self.dev.values():
+            t.zero_()
+        self.mirror.clear()
+        self.lent.clear()
+
+    def after_device_write(self):
+        self.mirror.clear()
+
+
+def keys_in(torch, keys, device):
+    """-> (device int64 tensor, kind): kind 'cuda' (results stay on device,
+    asynchronous), 'host' (CPU torch tensor; results come back as CPU
+    tensors) or 'numpy'."""
+    if isinstance(keys, torch.Tensor):
+        kind = "cuda" if keys.is_cuda else "host"
+    else:
+        kind = "numpy"
+    return _lib.to_device_u64(torch, keys, device), kind
+
+
+def ret(torch, t, kind):
+    """Return a device result in the caller's flavour."""
+    if kind == "cuda":
+        return t
+    if kind == "host":
+        out = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        out.copy_(t, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return out
+    return t.cpu().numpy()

@@ -29,9 +29,29 @@ class TcfGeom(ctypes.Structure):
                 ("probe_limit", c_i32), ("group_width", c_i32), ("seed", c_u64)]
 
 
+class GqfGeom(ctypes.Structure):
+    _fields_ = [("q", c_i32), ("r", c_i32), ("phys", c_i64), ("num_regions", c_i64),
+                ("quotient_regions", c_i64), ("max_occupied", c_i64), ("seed", c_u64)]
+
+
+class GqfTables(ctypes.Structure):
+    _fields_ = [("slots", c_vp), ("occupieds", c_vp), ("runends", c_vp), ("offsets", c_vp),
+                ("stats", c_vp), ("spill", c_vp)]
+
+
+class GqfResult(ctypes.Structure):
+    _fields_ = [("code", c_i32), ("swapped", c_i32), ("fail_index", c_i64), ("fail_region", c_i64),
+                ("shifted", c_i64)]
+
+
+FK_GQF_INSERT, FK_GQF_DELETE = 0, 1
+FK_ORDER_POINT, FK_ORDER_BULK = 0, 1
+
 _SIGS = {
     "fk_version": (ctypes.c_char_p, []),
     "fk_abi_version": (c_i32, []),
+    "fk_device_setup": (c_i32, [c_i32]),
+    "fk_device_l2_fetch_bytes": (c_i32, []),
     "fk_hash_streams": (c_i32, [c_vp, c_i64, c_u64, c_i32, c_u64, c_u64, c_vp, c_vp]),
     "fk_fastmod_check": (c_i32, [c_vp, c_i64, c_u64, c_vp, c_vp]),
     "fk_tcf_workspace_bytes": (c_sz, [ctypes.POINTER(TcfGeom), c_i64, c_i32]),
@@ -40,6 +60,11 @@ _SIGS = {
     "fk_tcf_query": (c_i32, [ctypes.POINTER(TcfGeom), c_vp, c_vp, c_vp, c_i32, c_i64, c_vp, c_vp, c_vp]),
     "fk_tcf_delete": (c_i32, [ctypes.POINTER(TcfGeom), c_vp, c_vp, c_vp, c_i32, c_i64, c_vp, c_vp,
                               c_i32, c_vp, c_sz, c_vp]),
+    "fk_gqf_count": (c_i32, [ctypes.POINTER(GqfGeom), ctypes.POINTER(GqfTables), c_vp, c_i32, c_i64, c_vp, c_vp]),
+    "fk_gqf_find_run": (c_i32, [ctypes.POINTER(GqfGeom), ctypes.POINTER(GqfTables), c_vp, c_i64, c_vp, c_vp]),
+    "fk_gqf_rebuild_index": (c_i32, [ctypes.POINTER(GqfGeom), ctypes.POINTER(GqfTables), c_vp]),
+    "fk_gqf_apply": (c_i32, [ctypes.POINTER(GqfGeom), ctypes.POINTER(GqfTables), ctypes.POINTER(GqfTables),
+                             c_vp, c_i32, c_vp, c_i64, c_i32, c_i32, c_vp, ctypes.POINTER(GqfResult), c_vp]),
 }
 
 _lib = None
@@ -88,12 +113,23 @@ def check(rc, what):
     return rc
 
 
-def require_cuda():
+_setup_done = set()
+
+
+def require_cuda(device=None):
+    """torch with a CUDA device, the library loaded and the device set up."""
     import torch
     if not torch.cuda.is_available():
         raise RuntimeError("the B200 filter kernels need a CUDA device; none is visible "
                            "(there is no CPU fallback)")
-    load()
+    lib = load()
+    idx = torch.device(device).index if device is not None else None
+    if idx is None:
+        idx = torch.cuda.current_device()
+    if idx not in _setup_done:
+        with torch.cuda.device(idx):
+            check(lib.fk_device_setup(int(os.environ.get("FK_L2_FETCH_BYTES", "32"))), "device setup")
+        _setup_done.add(idx)
     return torch
 
 
@@ -108,11 +144,13 @@ def stream_ptr(torch):
 def to_device_u64(torch, keys, device):
     """numpy/torch/sequence of 64-bit keys -> contiguous int64 CUDA tensor (bit view)."""
     if isinstance(keys, torch.Tensor):
-        t = keys
+        t = keys.reshape(-1)
         if t.dtype in (torch.int64, torch.uint64):
             t = t.view(torch.int64)
         else:
             t = t.to(torch.int64)
+        if not t.is_cuda:
+            return t.to(device, non_blocking=t.is_pinned()).contiguous()
         return t.to(device).contiguous()
     arr = np.ascontiguousarray(np.asarray(keys, dtype=np.uint64).reshape(-1))
     return torch.from_numpy(arr.view(np.int64)).to(device)

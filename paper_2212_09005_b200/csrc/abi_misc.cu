@@ -31,6 +31,20 @@ extern "C" {
 const char *fk_version(void) { return "filterkit-b200 0.1.0 (sm_100a)"; }
 int fk_abi_version(void) { return FK_ABI_VERSION; }
 
+int fk_device_setup(int l2_fetch_bytes) {
+  // Random 32-byte block probes are the whole TCF/GQF access pattern; the
+  // default L2 fetch granularity would turn every miss into a 64-128 B DRAM
+  // read.  This is a per-context hint (cudaLimitMaxL2FetchGranularity).
+  if (l2_fetch_bytes > 0) FK_TRY(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)l2_fetch_bytes));
+  return 0;
+}
+
+int fk_device_l2_fetch_bytes(void) {
+  size_t v = 0;
+  if (cudaDeviceGetLimit(&v, cudaLimitMaxL2FetchGranularity) != cudaSuccess) return -1;
+  return (int)v;
+}
+
 int fk_hash_streams(const uint64_t *keys, int64_t n, uint64_t seed, int bits, uint64_t nb, uint64_t bsize,
                     uint64_t *out5, void *stream) {
   if (n < 0 || bits < 1 || bits > 64) return FK_E_ARG;

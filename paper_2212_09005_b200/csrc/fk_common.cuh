@@ -110,7 +110,26 @@ __device__ __forceinline__ bool cas_slot<uint64_t>(uint64_t *p, uint64_t e, uint
 // barriers, so a stale L1 line must never be read.
 template <int NB, bool CG = false>
 __device__ __forceinline__ void load_chunk(const void *p, uint32_t *regs) {
-  if constexpr (NB >= 16) {
+  if constexpr (NB % 32 == 0) {
+    // one 256-bit LDG per 32-byte sector (sm_100 LDG.E.256): a TCF block of
+    // 16 x u16 is exactly one request
+#pragma unroll
+    for (int i = 0; i < NB / 32; i++) {
+      const uint32_t *q = reinterpret_cast<const uint32_t *>(p) + 8 * i;
+      uint32_t *r = regs + 8 * i;
+      if constexpr (CG) {
+        asm volatile("ld.global.cg.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                       "=r"(r[7])
+                     : "l"(q));
+      } else {
+        asm volatile("ld.global.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                       "=r"(r[7])
+                     : "l"(q));
+      }
+    }
+  } else if constexpr (NB >= 16) {
 #pragma unroll
     for (int i = 0; i < NB / 16; i++) {
       const uint4 *q = reinterpret_cast<const uint4 *>(p) + i;

@@ -1,0 +1,452 @@
+// gqf.cu -- host side of the GQF C ABI: count / find_run / index rebuild /
+// insert+delete batches (canonical rebuild, exact sequential fallback).
+#include <cub/cub.cuh>
+
+#include <vector>
+
+#include "gqf_impl.cuh"
+
+namespace fk {
+
+namespace {
+
+// Stream-ordered scratch that frees itself (cudaMallocAsync pool).
+struct Scratch {
+  cudaStream_t st;
+  std::vector<void *> ptrs;
+  cudaError_t err = cudaSuccess;
+  explicit Scratch(cudaStream_t s) : st(s) {}
+  ~Scratch() {
+    for (void *p : ptrs) cudaFreeAsync(p, st);
+  }
+  template <typename T>
+  T *get(size_t count) {
+    void *p = nullptr;
+    size_t bytes = count * sizeof(T);
+    if (bytes == 0) bytes = 16;
+    cudaError_t e = cudaMallocAsync(&p, bytes, st);
+    if (e != cudaSuccess) {
+      err = e;
+      return nullptr;
+    }
+    ptrs.push_back(p);
+    return reinterpret_cast<T *>(p);
+  }
+};
+
+inline int blocks_for(int64_t n, int per = 256) {
+  int64_t b = (n + per - 1) / per;
+  int64_t cap = (int64_t)num_sms() * 16;
+  if (b > cap) b = cap;
+  return (int)(b < 1 ? 1 : b);
+}
+
+GqfDev make_dev(const fk_gqf_geom *g, const fk_gqf_tables *t) {
+  GqfDev T;
+  T.slots = t->slots;
+  T.occ = t->occupieds;
+  T.run = t->runends;
+  T.offs = t->offsets;
+  T.stats = t->stats;
+  T.spill = t->spill;
+  T.phys = g->phys;
+  T.q = g->q;
+  T.r = g->r;
+  T.nregions = g->num_regions;
+  T.max_occ = g->max_occupied;
+  return T;
+}
+
+bool geom_ok(const fk_gqf_geom *g) {
+  if (!g || g->q < 6 || g->q > 40) return false;
+  if (g->r != 8 && g->r != 16 && g->r != 32) return false;
+  if (g->q + g->r > 64) return false;
+  int64_t logical = 1LL << g->q;
+  int64_t pad = logical < kRegionSlots ? logical : kRegionSlots;
+  return g->phys == logical + pad && g->num_regions == (g->phys + kRegionSlots - 1) / kRegionSlots;
+}
+
+// ---- CUB helpers (type-independent, instantiated once) ---------------------
+cudaError_t cub_sort_pairs(Scratch &S, const uint64_t *kin, uint64_t *kout, const uint32_t *vin, uint32_t *vout,
+                           int64_t n, int end_bit) {
+  size_t tb = 0;
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, tb, kin, kout, vin, vout, n, 0, end_bit, S.st);
+  if (e) return e;
+  void *tmp = S.get<char>(tb);
+  if (!tmp) return S.err;
+  return cub::DeviceRadixSort::SortPairs(tmp, tb, kin, kout, vin, vout, n, 0, end_bit, S.st);
+}
+
+cudaError_t cub_reduce_by_key(Scratch &S, const uint64_t *keys, uint64_t *uniq, const uint64_t *vals, uint64_t *sums,
+                              int64_t *num, int64_t n) {
+  size_t tb = 0;
+  cudaError_t e = cub::DeviceReduce::ReduceByKey(nullptr, tb, keys, uniq, vals, sums, num, SatAdd(), n, S.st);
+  if (e) return e;
+  void *tmp = S.get<char>(tb);
+  if (!tmp) return S.err;
+  return cub::DeviceReduce::ReduceByKey(tmp, tb, keys, uniq, vals, sums, num, SatAdd(), n, S.st);
+}
+
+cudaError_t cub_excl_scan_by_key(Scratch &S, const uint64_t *keys, const uint64_t *vals, uint64_t *out, int64_t n) {
+  size_t tb = 0;
+  cudaError_t e = cub::DeviceScan::ExclusiveScanByKey(nullptr, tb, keys, vals, out, SatAdd(), (uint64_t)0, n,
+                                                      cuda::std::equal_to<>(), S.st);
+  if (e) return e;
+  void *tmp = S.get<char>(tb);
+  if (!tmp) return S.err;
+  return cub::DeviceScan::ExclusiveScanByKey(tmp, tb, keys, vals, out, SatAdd(), (uint64_t)0, n,
+                                             cuda::std::equal_to<>(), S.st);
+}
+
+cudaError_t cub_excl_sum_i64(Scratch &S, const int64_t *in, int64_t *out, int64_t n) {
+  size_t tb = 0;
+  cudaError_t e = cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, n, S.st);
+  if (e) return e;
+  void *tmp = S.get<char>(tb);
+  if (!tmp) return S.err;
+  return cub::DeviceScan::ExclusiveSum(tmp, tb, in, out, n, S.st);
+}
+
+cudaError_t cub_merge(Scratch &S, const uint64_t *k1, const uint64_t *v1, int64_t n1, const uint64_t *k2,
+                      const uint64_t *v2, int64_t n2, uint64_t *ko, uint64_t *vo) {
+  size_t tb = 0;
+  cudaError_t e = cub::DeviceMerge::MergePairs(nullptr, tb, k1, v1, n1, k2, v2, n2, ko, vo, cuda::std::less<>(), S.st);
+  if (e) return e;
+  void *tmp = S.get<char>(tb);
+  if (!tmp) return S.err;
+  return cub::DeviceMerge::MergePairs(tmp, tb, k1, v1, n1, k2, v2, n2, ko, vo, cuda::std::less<>(), S.st);
+}
+
+cudaError_t cub_select_flagged(Scratch &S, const uint64_t *in, const uint8_t *flags, uint64_t *out, int64_t *num,
+                               int64_t n) {
+  size_t tb = 0;
+  cudaError_t e = cub::DeviceSelect::Flagged(nullptr, tb, in, flags, out, num, n, S.st);
+  if (e) return e;
+  void *tmp = S.get<char>(tb);
+  if (!tmp) return S.err;
+  return cub::DeviceSelect::Flagged(tmp, tb, in, flags, out, num, n, S.st);
+}
+
+cudaError_t cub_maxplus_scan(Scratch &S, const MaxPlus *in, MaxPlus *out, int64_t n) {
+  size_t tb = 0;
+  cudaError_t e = cub::DeviceScan::InclusiveScan(nullptr, tb, in, out, MaxPlusOp(), n, S.st);
+  if (e) return e;
+  void *tmp = S.get<char>(tb);
+  if (!tmp) return S.err;
+  return cub::DeviceScan::InclusiveScan(tmp, tb, in, out, MaxPlusOp(), n, S.st);
+}
+
+cudaError_t cub_max_scan_i64(Scratch &S, const int64_t *in, int64_t *out, int64_t n) {
+  size_t tb = 0;
+  cudaError_t e = cub::DeviceScan::InclusiveScan(nullptr, tb, in, out, MaxI64(), n, S.st);
+  if (e) return e;
+  void *tmp = S.get<char>(tb);
+  if (!tmp) return S.err;
+  return cub::DeviceScan::InclusiveScan(tmp, tb, in, out, MaxI64(), n, S.st);
+}
+
+#define FK_CU(expr)                              \
+  do {                                           \
+    cudaError_t e_ = (expr);                     \
+    if (e_ != cudaSuccess) return -(int)e_;      \
+  } while (0)
+
+int rebuild_index(const fk_gqf_geom *g, const fk_gqf_tables *t, cudaStream_t st) {
+  Scratch S(st);
+  int64_t nw = g->phys >> 6;
+  int64_t nqw = ((1LL << g->q) + 63) >> 6;
+  int64_t *po = S.get<int64_t>(nw), *pr = S.get<int64_t>(nw), *ro = S.get<int64_t>(nw), *rr = S.get<int64_t>(nw);
+  if (S.err) return -(int)S.err;
+  k_word_popc<<<blocks_for(nw), 256, 0, st>>>(t->occupieds, nw, po);
+  k_word_popc<<<blocks_for(nw), 256, 0, st>>>(t->runends, nw, pr);
+  FK_CU(cub_excl_sum_i64(S, po, ro, nw));
+  FK_CU(cub_excl_sum_i64(S, pr, rr, nw));
+  k_spill_from_ranks<<<blocks_for(nqw), 256, 0, st>>>(t->runends, ro, rr, nqw, t->spill);
+  FK_CHECK_LAUNCH();
+  return 0;
+}
+
+template <typename S_t>
+int count_t(const fk_gqf_geom *g, const fk_gqf_tables *t, const uint64_t *keys, int keys_are_fps, int64_t n,
+            uint64_t *counts, cudaStream_t st) {
+  GqfDev T = make_dev(g, t);
+  k_gqf_count<S_t><<<blocks_for(n), 256, 0, st>>>(T, keys, keys_are_fps, g->seed, n, counts);
+  FK_CHECK_LAUNCH();
+  return 0;
+}
+
+template <typename S_t>
+int apply_t(const fk_gqf_geom *g, const fk_gqf_tables *cur, const fk_gqf_tables *nxt, const uint64_t *keys,
+            int keys_are_fps, const uint64_t *deltas, int64_t n, int op, int order, uint8_t *found,
+            fk_gqf_result *res, cudaStream_t st) {
+  Scratch S(st);
+  const int qr = g->q + g->r;
+  const uint64_t fmask = qr >= 64 ? ~0ull : ((1ull << qr) - 1);
+  const bool is_del = op == FK_GQF_DELETE;
+  GqfDev T0 = make_dev(g, cur);
+  res->code = 0;
+  res->swapped = 0;
+  res->fail_index = -1;
+  res->fail_region = -1;
+  res->shifted = 0;
+
+  // 1-3. hash, stable sort by fingerprint, deltas in sorted order
+  uint64_t *fps = S.get<uint64_t>(n), *fps_s = S.get<uint64_t>(n), *del_s = S.get<uint64_t>(n);
+  uint32_t *idx = S.get<uint32_t>(n), *idx_s = S.get<uint32_t>(n);
+  if (S.err) return -(int)S.err;
+  k_hash_fps<<<blocks_for(n), 256, 0, st>>>(keys, keys_are_fps, g->seed, fmask, n, fps, idx);
+  FK_CU(cub_sort_pairs(S, fps, fps_s, idx, idx_s, n, qr));
+  const uint64_t dflt = is_del ? (1ull << 63) : 1ull;
+  k_gather_u64<<<blocks_for(n), 256, 0, st>>>(deltas, idx_s, dflt, n, del_s);
+
+  // 4. unique fingerprints with saturating delta sums
+  uint64_t *uniq = S.get<uint64_t>(n), *sums = S.get<uint64_t>(n);
+  int64_t *d_num = S.get<int64_t>(4);
+  if (S.err) return -(int)S.err;
+  FK_CU(cub_reduce_by_key(S, fps_s, uniq, del_s, sums, d_num, n));
+  int64_t m = 0;
+  FK_CU(cudaMemcpyAsync(&m, d_num, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  FK_CU(cudaStreamSynchronize(st));
+
+  // 5-6. old counts through the (pure) count query, new absolute counts
+  uint64_t *c_old = S.get<uint64_t>(m), *c_new = S.get<uint64_t>(m);
+  if (S.err) return -(int)S.err;
+  k_gqf_count<S_t><<<blocks_for(m), 256, 0, st>>>(T0, uniq, 1, 0, m, c_old);
+  k_new_counts<<<blocks_for(m), 256, 0, st>>>(c_old, sums, m, is_del ? 1 : 0, c_new);
+
+  // 7. delete found flags: sequential semantics via a segmented prefix sum
+  if (is_del && found) {
+    uint64_t *pre = S.get<uint64_t>(n);
+    if (S.err) return -(int)S.err;
+    if (order == FK_ORDER_POINT) {
+      FK_CU(cub_excl_scan_by_key(S, fps_s, del_s, pre, n));
+    } else {
+      // bulk: each region is applied in descending order (gqf.py:317-325), so
+      // equal fingerprints are processed last-input-first
+      uint64_t *rf = S.get<uint64_t>(n), *rd = S.get<uint64_t>(n), *rp = S.get<uint64_t>(n);
+      if (S.err) return -(int)S.err;
+      k_reverse_u64<<<blocks_for(n), 256, 0, st>>>(fps_s, n, rf);
+      k_reverse_u64<<<blocks_for(n), 256, 0, st>>>(del_s, n, rd);
+      FK_CU(cub_excl_scan_by_key(S, rf, rd, rp, n));
+      k_reverse_u64<<<blocks_for(n), 256, 0, st>>>(rp, n, pre);
+    }
+    k_found_flags<<<blocks_for(n), 256, 0, st>>>(fps_s, pre, idx_s, uniq, c_old, m, n, found);
+  }
+
+  // 8. decode the old table into sorted (fp, count) items
+  int64_t nqw = ((1LL << g->q) + 63) >> 6;
+  int64_t *gcount = S.get<int64_t>(nqw), *goff = S.get<int64_t>(nqw);
+  int *d_err = S.get<int>(4);
+  if (S.err) return -(int)S.err;
+  FK_CU(cudaMemsetAsync(d_err, 0, 4 * sizeof(int), st));
+  k_decode_words<S_t><<<blocks_for(nqw), 256, 0, st>>>(T0, nqw, 0, gcount, nullptr, nullptr, nullptr, d_err);
+  FK_CU(cub_excl_sum_i64(S, gcount, goff, nqw));
+  int64_t tail[2];
+  FK_CU(cudaMemcpyAsync(&tail[0], goff + nqw - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  FK_CU(cudaMemcpyAsync(&tail[1], gcount + nqw - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  int h_err = 0;
+  FK_CU(cudaMemcpyAsync(&h_err, d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  FK_CU(cudaStreamSynchronize(st));
+  if (h_err) return FK_E_INVARIANT;
+  int64_t g_old = tail[0] + tail[1];
+  uint64_t *o_fp = S.get<uint64_t>(g_old), *o_cnt = S.get<uint64_t>(g_old);
+  if (S.err) return -(int)S.err;
+  k_decode_words<S_t><<<blocks_for(nqw), 256, 0, st>>>(T0, nqw, 1, nullptr, goff, o_fp, o_cnt, d_err);
+
+  // 9-10. drop old items the batch updates and zero counts, then merge the
+  // two duplicate-free sorted lists
+  uint8_t *keep_o = S.get<uint8_t>(g_old), *keep_u = S.get<uint8_t>(m);
+  uint64_t *o2_fp = S.get<uint64_t>(g_old), *o2_cnt = S.get<uint64_t>(g_old);
+  uint64_t *u2_fp = S.get<uint64_t>(m), *u2_cnt = S.get<uint64_t>(m);
+  if (S.err) return -(int)S.err;
+  k_keep_old<<<blocks_for(g_old), 256, 0, st>>>(o_fp, g_old, uniq, m, keep_o);
+  k_nonzero<<<blocks_for(m), 256, 0, st>>>(c_new, m, keep_u);
+  FK_CU(cub_select_flagged(S, o_fp, keep_o, o2_fp, d_num, g_old));
+  FK_CU(cub_select_flagged(S, o_cnt, keep_o, o2_cnt, d_num + 1, g_old));
+  FK_CU(cub_select_flagged(S, uniq, keep_u, u2_fp, d_num + 2, m));
+  FK_CU(cub_select_flagged(S, c_new, keep_u, u2_cnt, d_num + 3, m));
+  int64_t hn[4];
+  FK_CU(cudaMemcpyAsync(hn, d_num, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  FK_CU(cudaStreamSynchronize(st));
+  int64_t G = hn[0] + hn[2];
+  uint64_t *it_fp = S.get<uint64_t>(G), *it_cnt = S.get<uint64_t>(G);
+  if (S.err) return -(int)S.err;
+  if (G > 0) FK_CU(cub_merge(S, o2_fp, o2_cnt, hn[0], u2_fp, u2_cnt, hn[2], it_fp, it_cnt));
+
+  // 11. placement: max-plus scan gives every item's last slot
+  MaxPlus *terms = S.get<MaxPlus>(G), *ends = S.get<MaxPlus>(G);
+  uint64_t *L = S.get<uint64_t>(G);
+  if (S.err) return -(int)S.err;
+  if (G > 0) {
+    k_place_terms<<<blocks_for(G), 256, 0, st>>>(it_fp, it_cnt, G, g->r, terms, L);
+    FK_CU(cub_maxplus_scan(S, terms, ends, G));
+  }
+
+  // 12. would the sequential reference have raised?  (inserts only)
+  bool exact = false, load_possible = false;
+  if (!is_del && G > 0) {
+    int64_t *cfirst = S.get<int64_t>(G), *cfs = S.get<int64_t>(G);
+    unsigned *flags = S.get<unsigned>(4);
+    if (S.err) return -(int)S.err;
+    FK_CU(cudaMemsetAsync(flags, 0, 4 * sizeof(unsigned), st));
+    k_cluster_check<<<blocks_for(G), 256, 0, st>>>(it_fp, ends, G, g->r, g->phys, cfirst, flags);
+    FK_CU(cub_max_scan_i64(S, cfirst, cfs, G));
+    k_cluster_check2<<<blocks_for(G), 256, 0, st>>>(ends, cfs, cfirst, G, g->phys, flags);
+    int64_t *occ_sum = S.get<int64_t>(4);
+    if (S.err) return -(int)S.err;
+    FK_CU(cudaMemsetAsync(occ_sum, 0, 4 * sizeof(int64_t), st));
+    k_stats<<<blocks_for(G), 256, 0, st>>>(it_cnt, L, G, occ_sum);
+    unsigned h_flags = 0;
+    int64_t h_occ = 0;
+    FK_CU(cudaMemcpyAsync(&h_flags, flags, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    FK_CU(cudaMemcpyAsync(&h_occ, occ_sum, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    FK_CU(cudaStreamSynchronize(st));
+    // every item's pre-insert occupancy is <= the final one, so a final
+    // occupancy below the ceiling rules LOAD_CAPACITY out for any order
+    exact = h_flags != 0 || h_occ >= g->max_occupied;
+    load_possible = h_occ >= g->max_occupied;
+  }
+
+  if (exact) {
+    // 13'. exact sequential application in place on `cur`
+    if (order == FK_ORDER_POINT) {
+      int32_t *scr = S.get<int32_t>(SeqGqf<S_t>::kGapCap);
+      int64_t *out3 = S.get<int64_t>(4);
+      if (S.err) return -(int)S.err;
+      k_gqf_exact_seq<S_t><<<1, 1, 0, st>>>(T0, fps, deltas, n, scr, out3);
+      int64_t h3[3];
+      FK_CU(cudaMemcpyAsync(h3, out3, 3 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+      FK_CU(cudaStreamSynchronize(st));
+      if (h3[0] < 0) return FK_E_INVARIANT;
+      res->code = (int32_t)h3[0];
+      res->fail_index = h3[1];
+      res->shifted = h3[2];
+    } else {
+      int64_t nqr = g->quotient_regions;
+      int64_t *rb = S.get<int64_t>(nqr + 1);
+      int32_t *fail = S.get<int32_t>(nqr);
+      unsigned long long *moved = S.get<unsigned long long>(1);
+      int64_t half = (nqr + 1) / 2;
+      int32_t *scr = S.get<int32_t>((size_t)half * SeqGqf<S_t>::kGapCap);
+      if (S.err) return -(int)S.err;
+      FK_CU(cudaMemsetAsync(fail, 0, nqr * sizeof(int32_t), st));
+      FK_CU(cudaMemsetAsync(moved, 0, sizeof(unsigned long long), st));
+      k_region_bounds<<<blocks_for(nqr + 1), 256, 0, st>>>(fps_s, n, g->r + kRegionBits, nqr, rb);
+      // the ceiling check reads the shared occupancy counter, so when it can
+      // trigger, regions run one after another in the reference's workers=1
+      // order (even ascending, then odd); otherwise a parity's regions are
+      // independent (disjoint [g, g+2) windows) and run in parallel
+      for (int parity = 0; parity < 2; parity++) {
+        if (load_possible)
+          k_gqf_exact_regions<S_t><<<1, 1, 0, st>>>(T0, fps_s, del_s, rb, nqr, parity, scr, fail, moved);
+        else
+          k_gqf_exact_regions<S_t><<<blocks_for(half, 64), 64, 0, st>>>(T0, fps_s, del_s, rb, nqr, parity, scr,
+                                                                         fail, moved);
+      }
+      std::vector<int32_t> hf(nqr);
+      unsigned long long hm = 0;
+      FK_CU(cudaMemcpyAsync(hf.data(), fail, nqr * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+      FK_CU(cudaMemcpyAsync(&hm, moved, sizeof(hm), cudaMemcpyDeviceToHost, st));
+      FK_CU(cudaStreamSynchronize(st));
+      for (int parity = 0; parity < 2 && res->code == 0; parity++)
+        for (int64_t gg = parity; gg < nqr; gg += 2)
+          if (hf[gg]) {
+            if (hf[gg] < 0) return FK_E_INVARIANT;
+            res->code = hf[gg];
+            res->fail_region = gg;
+            break;
+          }
+      res->shifted = (int64_t)hm;
+    }
+    int rc = rebuild_index(g, cur, st);
+    if (rc) return rc;
+    FK_CU(cudaStreamSynchronize(st));
+    return 0;
+  }
+
+  // 13. canonical rebuild into `next`
+  GqfDev T1 = make_dev(g, nxt);
+  FK_CU(cudaMemsetAsync(nxt->slots, 0, (size_t)g->phys * sizeof(S_t), st));
+  FK_CU(cudaMemsetAsync(nxt->occupieds, 0, (size_t)(g->phys >> 6) * 8, st));
+  FK_CU(cudaMemsetAsync(nxt->runends, 0, (size_t)(g->phys >> 6) * 8, st));
+  FK_CU(cudaMemsetAsync(nxt->offsets, 0, (size_t)g->num_regions * 4, st));
+  FK_CU(cudaMemsetAsync(nxt->stats, 0, 3 * sizeof(int64_t), st));
+  if (G > 0) {
+    k_write_items<S_t><<<blocks_for(G), 256, 0, st>>>(T1, it_fp, it_cnt, ends, L, G);
+    k_stats<<<blocks_for(G), 256, 0, st>>>(it_cnt, L, G, nxt->stats);
+    FK_CU(cudaMemcpyAsync(nxt->stats + 2, &G, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  }
+  int rc = rebuild_index(g, nxt, st);
+  if (rc) return rc;
+  // shift instrumentation: bulk = old slots that moved; point = every slot
+  // the batch wrote or moved
+  unsigned long long *dc = S.get<unsigned long long>(1);
+  if (S.err) return -(int)S.err;
+  FK_CU(cudaMemsetAsync(dc, 0, sizeof(unsigned long long), st));
+  k_diff_count<S_t><<<blocks_for(g->phys), 256, 0, st>>>(
+      reinterpret_cast<const S_t *>(cur->slots), cur->runends, reinterpret_cast<const S_t *>(nxt->slots),
+      nxt->runends, g->phys, order == FK_ORDER_BULK ? 1 : 0, dc);
+  unsigned long long hdc = 0;
+  FK_CU(cudaMemcpyAsync(&hdc, dc, sizeof(hdc), cudaMemcpyDeviceToHost, st));
+  FK_CU(cudaStreamSynchronize(st));
+  res->shifted = (int64_t)hdc;
+  res->swapped = 1;
+  FK_CHECK_LAUNCH();
+  return 0;
+}
+
+}  // namespace
+
+}  // namespace fk
+
+using namespace fk;
+
+extern "C" {
+
+int fk_gqf_count(const fk_gqf_geom *g, const fk_gqf_tables *t, const uint64_t *keys, int keys_are_fps, int64_t n,
+                 uint64_t *counts, void *stream) {
+  if (!geom_ok(g) || !t || n < 0) return FK_E_ARG;
+  if (n == 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (g->r) {
+    case 8: return count_t<uint8_t>(g, t, keys, keys_are_fps, n, counts, st);
+    case 16: return count_t<uint16_t>(g, t, keys, keys_are_fps, n, counts, st);
+    default: return count_t<uint32_t>(g, t, keys, keys_are_fps, n, counts, st);
+  }
+}
+
+int fk_gqf_find_run(const fk_gqf_geom *g, const fk_gqf_tables *t, const int64_t *quotients, int64_t n, int64_t *se,
+                    void *stream) {
+  if (!geom_ok(g) || !t || n < 0) return FK_E_ARG;
+  if (n == 0) return 0;
+  GqfDev T = make_dev(g, t);
+  k_gqf_find_run<<<blocks_for(n), 256, 0, (cudaStream_t)stream>>>(T, quotients, n, se);
+  FK_CHECK_LAUNCH();
+  return 0;
+}
+
+int fk_gqf_rebuild_index(const fk_gqf_geom *g, const fk_gqf_tables *t, void *stream) {
+  if (!geom_ok(g) || !t) return FK_E_ARG;
+  return rebuild_index(g, t, (cudaStream_t)stream);
+}
+
+int fk_gqf_apply(const fk_gqf_geom *g, const fk_gqf_tables *cur, const fk_gqf_tables *next, const uint64_t *keys,
+                 int keys_are_fps, const uint64_t *deltas, int64_t n, int op, int order, uint8_t *found,
+                 fk_gqf_result *result, void *stream) {
+  if (!geom_ok(g) || !cur || !next || !result || n < 0 || n > 0xFFFFFFF0LL) return FK_E_ARG;
+  if (op != FK_GQF_INSERT && op != FK_GQF_DELETE) return FK_E_ARG;
+  result->code = 0;
+  result->swapped = 0;
+  result->fail_index = -1;
+  result->fail_region = -1;
+  result->shifted = 0;
+  if (n == 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (g->r) {
+    case 8: return apply_t<uint8_t>(g, cur, next, keys, keys_are_fps, deltas, n, op, order, found, result, st);
+    case 16: return apply_t<uint16_t>(g, cur, next, keys, keys_are_fps, deltas, n, op, order, found, result, st);
+    default: return apply_t<uint32_t>(g, cur, next, keys, keys_are_fps, deltas, n, op, order, found, result, st);
+  }
+}
+
+}  // extern "C"

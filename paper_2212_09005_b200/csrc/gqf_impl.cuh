@@ -1,0 +1,684 @@
+// gqf_impl.cuh -- counting quotient filter (GQF) device code for sm_100a.
+//
+// Table layout is bit-identical to the reference (gqf.py:111-117): r-bit slot
+// words, occupieds/runends bit vectors (u64 words), int32 spill offsets per
+// 8192-slot region, int64 stats[3].  On top of it the device keeps one
+// derived word per 64 quotients, spill[w] = max(0, end of the last run whose
+// quotient < 64w  -  64w + 1), which turns the reference's region-local
+// rank/select (popcount of up to 128 occupieds words, _ckernels.pyx:669-683)
+// into an O(1) lookup: the run of quotient x ends at the R-th runend after
+// 64w + spill[w] - 1, R = rank of x inside its occupieds word.
+//
+// Mutations: the final table of any insert/delete batch is a pure function of
+// the (fingerprint -> count) multiset (runs in quotient order,
+// groups sorted by remainder, run start = max(quotient, previous end + 1)), so
+// a batch is applied by a canonical rebuild: sort+reduce the batch, decode
+// the old table into sorted (fp, count) items, merge, encode, place with a
+// max-plus scan, write a fresh table.  Batches that could hit the reference's
+// capacity errors (LOAD_CAPACITY / SHIFT_BOUND) run the exact sequential
+// algorithm on the device instead (gqf_exact_* below), which reproduces the
+// reference's partial application and failure index bit for bit.
+#pragma once
+#include "../../include/filterkit_b200.h"
+#include "fk_common.cuh"
+
+namespace fk {
+
+struct GqfDev {
+  void *slots;
+  uint64_t *occ;
+  uint64_t *run;
+  int32_t *offs;
+  int64_t *stats;
+  uint32_t *spill;  // derived: per 64-quotient word
+  int64_t phys;
+  int q, r;
+  int64_t nregions;
+  int64_t max_occ;
+};
+
+__device__ __forceinline__ int bit_at(const uint64_t *bv, int64_t i) { return (int)((bv[i >> 6] >> (i & 63)) & 1); }
+
+// k-th set bit strictly after pos (k >= 1), scanning below lim; -2 if none.
+__device__ __forceinline__ int64_t select_after_dev(const uint64_t *bv, int64_t pos, int64_t k, int64_t lim) {
+  int64_t i = pos + 1 < 0 ? 0 : pos + 1;
+  while (i < lim) {
+    uint64_t w = bv[i >> 6] >> (i & 63);
+    int c = __popcll(w);
+    if (c >= k) {
+      for (;;) {
+        if (--k == 0) return i + __ffsll((long long)w) - 1;
+        w &= w - 1;
+      }
+    }
+    k -= c;
+    i = (i | 63) + 1;
+  }
+  return -2;
+}
+
+// Run interval of an occupied quotient through the spill index; false if the
+// quotient is unoccupied.
+__device__ __forceinline__ bool find_run_idx(const GqfDev &T, int64_t quot, int64_t *s, int64_t *e) {
+  int64_t w = quot >> 6;
+  uint64_t ow = T.occ[w];
+  int b = (int)(quot & 63);
+  if (!((ow >> b) & 1)) return false;
+  int R = __popcll(ow & ((2ull << b) - 1));  // inclusive rank in the word (b=63 -> all bits)
+  int64_t E = (w << 6) + (int64_t)T.spill[w] - 1;
+  int64_t prev = R == 1 ? E : select_after_dev(T.run, E, R - 1, T.phys);
+  int64_t end = select_after_dev(T.run, prev, 1, T.phys);
+  *s = quot > prev + 1 ? quot : prev + 1;
+  *e = end;
+  return end >= 0;
+}
+
+// Count group at slot i of a run ending at end (countgroups.py:69-102).
+template <typename S>
+__device__ __forceinline__ bool parse_group_dev(const S *slots, int64_t i, int64_t end, int r, uint64_t *rem,
+                                                uint64_t *cnt, int64_t *nx) {
+  uint64_t h = slots[i];
+  if (h == 0) {
+    int64_t j = i;
+    while (j <= end && slots[j] == 0) j++;
+    *rem = 0;
+    *cnt = (uint64_t)(j - i);
+    *nx = j;
+    return true;
+  }
+  if (i == end) { *rem = h; *cnt = 1; *nx = i + 1; return true; }
+  uint64_t v = slots[i + 1];
+  if (v > h) { *rem = h; *cnt = 1; *nx = i + 1; return true; }
+  if (v == h) { *rem = h; *cnt = 2; *nx = i + 2; return true; }
+  uint64_t base = (1ull << r) - 1, rest = 0, scale = 1;
+  int64_t j = i + 2;
+  for (;;) {
+    if (j > end) return false;
+    uint64_t d = slots[j];
+    if (d == h) break;
+    rest += scale * (d > h ? d - 1 : d);
+    scale *= base;
+    j++;
+  }
+  *rem = h;
+  *cnt = v + h * rest + 2;
+  *nx = j + 1;
+  return true;
+}
+
+// countgroups.py:54-66
+__host__ __device__ __forceinline__ uint64_t enc_len(uint64_t rem, uint64_t count, int r) {
+  if (rem == 0 || count <= 2) return count;
+  uint64_t base = (1ull << r) - 1, v = (count - 2) / rem, n = 3;
+  while (v) { n++; v /= base; }
+  return n;
+}
+
+// countgroups.py:28-51 (every slot of the group is written)
+template <typename S>
+__device__ __forceinline__ void enc_write(S *slots, int64_t pos, uint64_t rem, uint64_t count, int r) {
+  if (rem == 0) {
+    for (uint64_t i = 0; i < count; i++) slots[pos + (int64_t)i] = 0;
+    return;
+  }
+  slots[pos] = (S)rem;
+  if (count == 1) return;
+  if (count == 2) { slots[pos + 1] = (S)rem; return; }
+  uint64_t v = count - 2, base = (1ull << r) - 1;
+  slots[pos + 1] = (S)(v % rem);
+  v /= rem;
+  int64_t i = pos + 2;
+  while (v) {
+    uint64_t d = v % base;
+    v /= base;
+    slots[i++] = (S)(d >= rem ? d + 1 : d);
+  }
+  slots[i] = (S)rem;
+}
+
+// ---------------------------------------------------------------------------
+// count query (gqf_count_batch, _ckernels.pyx:1205-1250): pure function
+// ---------------------------------------------------------------------------
+template <typename S>
+__global__ void __launch_bounds__(256) k_gqf_count(GqfDev T, const uint64_t *__restrict__ keys, int keys_are_fps,
+                                                   uint64_t seed, int64_t n, uint64_t *__restrict__ counts) {
+  const S *slots = reinterpret_cast<const S *>(T.slots);
+  uint64_t fmask = (T.q + T.r) >= 64 ? ~0ull : ((1ull << (T.q + T.r)) - 1);
+  uint64_t rmask = (1ull << T.r) - 1;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t fp = (keys_are_fps ? keys[i] : mix64(keys[i] ^ seed)) & fmask;
+    int64_t quot = (int64_t)(fp >> T.r);
+    uint64_t rem = fp & rmask;
+    uint64_t c = 0;
+    int64_t s, e;
+    if (find_run_idx(T, quot, &s, &e)) {
+      for (int64_t p = s; p <= e;) {
+        uint64_t h, cnt;
+        int64_t nx;
+        if (!parse_group_dev<S>(slots, p, e, T.r, &h, &cnt, &nx)) break;
+        if (h == rem) { c = cnt; break; }
+        if (h > rem) break;
+        p = nx;
+      }
+    }
+    counts[i] = c;
+  }
+}
+
+__global__ void k_gqf_find_run(GqfDev T, const int64_t *__restrict__ quots, int64_t n, int64_t *__restrict__ se) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t s = -1, e = -1;
+    if (!find_run_idx(T, quots[i], &s, &e)) s = e = -1;
+    se[2 * i] = s;
+    se[2 * i + 1] = e;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// spill index (re)build from the metadata bit vectors (global rank/select)
+// ---------------------------------------------------------------------------
+__global__ void k_word_popc(const uint64_t *__restrict__ bv, int64_t nw, int64_t *__restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nw; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = __popcll(bv[i]);
+}
+
+// rank_occ/rank_run: exclusive prefix sums of per-word popcounts (int64).
+__global__ void k_spill_from_ranks(const uint64_t *__restrict__ run, const int64_t *__restrict__ rank_occ,
+                                   const int64_t *__restrict__ rank_run, int64_t nw, uint32_t *__restrict__ spill) {
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += (int64_t)gridDim.x * blockDim.x) {
+    int64_t K = rank_occ[w];  // occupied quotients < 64w
+    uint32_t s = 0;
+    if (K > 0) {
+      // word v holding the K-th runend: last v with rank_run[v] < K
+      int64_t lo = 0, hi = nw - 1;
+      while (lo < hi) {
+        int64_t mid = (lo + hi + 1) >> 1;
+        if (rank_run[mid] < K) lo = mid; else hi = mid - 1;
+      }
+      uint64_t word = run[lo];
+      int64_t k = K - rank_run[lo];
+      while (--k > 0) word &= word - 1;
+      int64_t E = (lo << 6) + __ffsll((long long)word) - 1;
+      int64_t sp = E - (w << 6) + 1;
+      s = sp > 0 ? (uint32_t)sp : 0u;
+    }
+    spill[w] = s;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// canonical rebuild pipeline
+// ---------------------------------------------------------------------------
+
+__global__ void k_hash_fps(const uint64_t *__restrict__ keys, int keys_are_fps, uint64_t seed, uint64_t fmask,
+                           int64_t n, uint64_t *__restrict__ fps, uint32_t *__restrict__ idx) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    fps[i] = (keys_are_fps ? keys[i] : mix64(keys[i] ^ seed)) & fmask;
+    idx[i] = (uint32_t)i;
+  }
+}
+
+__global__ void k_gather_u64(const uint64_t *__restrict__ src, const uint32_t *__restrict__ idx,
+                             uint64_t dflt, int64_t n, uint64_t *__restrict__ dst) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src ? src[idx[i]] : dflt;
+}
+
+struct SatAdd {
+  __host__ __device__ __forceinline__ uint64_t operator()(uint64_t a, uint64_t b) const {
+    uint64_t s = a + b;
+    return s < a ? ~0ull : s;
+  }
+};
+
+// new absolute count per unique fp: insert c+sum, delete c-min(c,sum)
+__global__ void k_new_counts(const uint64_t *__restrict__ c_old, const uint64_t *__restrict__ sums, int64_t m,
+                             int is_delete, uint64_t *__restrict__ c_new) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t c = c_old[i], s = sums[i];
+    if (is_delete) c_new[i] = c > s ? c - s : 0;
+    else { uint64_t t = c + s; c_new[i] = t < c ? ~0ull : t; }
+  }
+}
+
+// found flags for deletes: element j (in processing order within its fp
+// segment) finds the key iff the deltas processed before it leave a count.
+__global__ void k_found_flags(const uint64_t *__restrict__ fps_s, const uint64_t *__restrict__ pre,
+                              const uint32_t *__restrict__ idx_s, const uint64_t *__restrict__ uniq,
+                              const uint64_t *__restrict__ c_old, int64_t m, int64_t n, uint8_t *__restrict__ found) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t f = fps_s[j];
+    int64_t lo = 0, hi = m - 1;
+    while (lo < hi) {
+      int64_t mid = (lo + hi) >> 1;
+      if (uniq[mid] < f) lo = mid + 1; else hi = mid;
+    }
+    found[idx_s[j]] = pre[j] < c_old[lo] ? 1 : 0;
+  }
+}
+
+__global__ void k_reverse_u64(const uint64_t *__restrict__ a, int64_t n, uint64_t *__restrict__ b) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    b[n - 1 - i] = a[i];
+}
+
+// Decode pass over occupied quotient words: mode 0 counts groups per word,
+// mode 1 writes (fp, count) items at off[w].
+template <typename S>
+__global__ void k_decode_words(GqfDev T, int64_t nqw, int mode, int64_t *__restrict__ gcount,
+                               const int64_t *__restrict__ off, uint64_t *__restrict__ it_fp,
+                               uint64_t *__restrict__ it_cnt, int *__restrict__ err) {
+  const S *slots = reinterpret_cast<const S *>(T.slots);
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nqw; w += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t ow = T.occ[w];
+    int64_t g = 0;
+    int64_t o = mode ? off[w] : 0;
+    if (ow) {
+      int64_t prev = (w << 6) + (int64_t)T.spill[w] - 1;
+      while (ow) {
+        int b = __ffsll((long long)ow) - 1;
+        ow &= ow - 1;
+        int64_t quot = (w << 6) + b;
+        int64_t end = select_after_dev(T.run, prev, 1, T.phys);
+        if (end < 0) { *err = 1; break; }
+        int64_t s = quot > prev + 1 ? quot : prev + 1;
+        for (int64_t p = s; p <= end;) {
+          uint64_t h, cnt;
+          int64_t nx;
+          if (!parse_group_dev<S>(slots, p, end, T.r, &h, &cnt, &nx)) { *err = 1; break; }
+          if (mode) {
+            it_fp[o] = ((uint64_t)quot << T.r) | h;
+            it_cnt[o] = cnt;
+            o++;
+          }
+          g++;
+          p = nx;
+        }
+        prev = end;
+      }
+    }
+    if (!mode) gcount[w] = g;
+  }
+}
+
+// Old items whose fingerprint the batch updates are dropped before the merge
+// (their replacement carries the new absolute count); so are zero counts.
+__global__ void k_keep_old(const uint64_t *__restrict__ o_fp, int64_t g_old, const uint64_t *__restrict__ uniq,
+                           int64_t m, uint8_t *__restrict__ keep) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < g_old; j += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t f = o_fp[j];
+    int64_t lo = 0, hi = m;
+    while (lo < hi) {
+      int64_t mid = (lo + hi) >> 1;
+      if (uniq[mid] < f) lo = mid + 1; else hi = mid;
+    }
+    keep[j] = (lo < m && uniq[lo] == f) ? 0 : 1;
+  }
+}
+
+__global__ void k_nonzero(const uint64_t *__restrict__ c, int64_t m, uint8_t *__restrict__ keep) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += (int64_t)gridDim.x * blockDim.x)
+    keep[j] = c[j] > 0 ? 1 : 0;
+}
+
+// Max-plus placement: item i maps the end position e of everything before it
+// to max(a_i, e + b_i): first item of a run a = quot + L - 1, b = L; later
+// items a = -inf, b = L.  The inclusive scan yields each item's last slot.
+struct MaxPlus {
+  int64_t a, b;
+};
+struct MaxPlusOp {
+  __host__ __device__ __forceinline__ MaxPlus operator()(const MaxPlus &l, const MaxPlus &rr) const {
+    MaxPlus o;
+    int64_t t = l.a + rr.b;
+    o.a = rr.a > t ? rr.a : t;
+    o.b = l.b + rr.b;
+    return o;
+  }
+};
+constexpr int64_t kNegInf = -(1LL << 60);
+
+__global__ void k_place_terms(const uint64_t *__restrict__ fp, const uint64_t *__restrict__ cnt, int64_t G, int r,
+                              MaxPlus *__restrict__ terms, uint64_t *__restrict__ L_out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < G; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t f = fp[i];
+    uint64_t rem = f & ((1ull << r) - 1);
+    int64_t quot = (int64_t)(f >> r);
+    uint64_t L = enc_len(rem, cnt[i], r);
+    int64_t Ls = L > (1ull << 50) ? (1LL << 50) : (int64_t)L;  // clamp: fails the capacity check anyway
+    bool first = i == 0 || (fp[i - 1] >> r) != (f >> r);
+    MaxPlus m;
+    m.a = first ? quot + Ls - 1 : kNegInf;
+    m.b = Ls;
+    terms[i] = m;
+    L_out[i] = (uint64_t)Ls;
+  }
+}
+
+// Capacity predicates of the fast path (SURVEY H2 / DESIGN.md):
+//  flags[0] |= some cluster ends at or beyond min(phys, (region of its first
+//              quotient + 2) * 8192)  -> a SHIFT_BOUND is possible
+__global__ void k_cluster_check(const uint64_t *__restrict__ fp, const MaxPlus *__restrict__ ends, int64_t G, int r,
+                                int64_t phys, int64_t *__restrict__ cfirst, unsigned *__restrict__ flags) {
+  // cfirst[i] = quotient of the first run of i's cluster (written for cluster starts, -1 otherwise)
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < G; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t quot = (int64_t)(fp[i] >> r);
+    bool first = i == 0 || (fp[i - 1] >> r) != (fp[i] >> r);
+    bool cstart = i == 0 || (first && quot > ends[i - 1].a + 1);
+    cfirst[i] = cstart ? quot : -1;
+  }
+}
+
+__global__ void k_cluster_check2(const MaxPlus *__restrict__ ends, const int64_t *__restrict__ cfirst_scan,
+                                 const int64_t *__restrict__ cfirst, int64_t G, int64_t phys,
+                                 unsigned *__restrict__ flags) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < G; i += (int64_t)gridDim.x * blockDim.x) {
+    bool cend = i == G - 1 || cfirst[i + 1] >= 0;
+    if (!cend) continue;
+    int64_t g = cfirst_scan[i] >> kRegionBits;
+    int64_t hard = (g + 2) << kRegionBits;
+    if (hard > phys) hard = phys;
+    if (ends[i].a >= hard) atomicOr(&flags[0], 1u);
+  }
+}
+
+struct MaxI64 {
+  __host__ __device__ __forceinline__ int64_t operator()(int64_t a, int64_t b) const { return a > b ? a : b; }
+};
+
+// Write the new table: every item writes its group; run heads set occupieds,
+// run tails set runends; region-boundary runs set the next region's offset.
+template <typename S>
+__global__ void k_write_items(GqfDev T, const uint64_t *__restrict__ fp, const uint64_t *__restrict__ cnt,
+                              const MaxPlus *__restrict__ ends, const uint64_t *__restrict__ L, int64_t G) {
+  S *slots = reinterpret_cast<S *>(T.slots);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < G; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t f = fp[i];
+    int64_t quot = (int64_t)(f >> T.r);
+    uint64_t rem = f & ((1ull << T.r) - 1);
+    int64_t e = ends[i].a;
+    int64_t pos = e - (int64_t)L[i] + 1;
+    enc_write<S>(slots, pos, rem, cnt[i], T.r);
+    bool first = i == 0 || (fp[i - 1] >> T.r) != (f >> T.r);
+    bool last = i == G - 1 || (fp[i + 1] >> T.r) != (f >> T.r);
+    if (first) atomicOr((unsigned long long *)&T.occ[quot >> 6], 1ull << (quot & 63));
+    if (last) {
+      atomicOr((unsigned long long *)&T.run[e >> 6], 1ull << (e & 63));
+      int64_t g = quot >> kRegionBits;
+      int64_t gnext = i == G - 1 ? (1LL << 62) : ((int64_t)(fp[i + 1] >> T.r) >> kRegionBits);
+      if (gnext > g && g + 1 < T.nregions) {
+        int64_t sp = e - ((g + 1) << kRegionBits) + 1;
+        T.offs[g + 1] = sp > 0 ? (int32_t)sp : 0;
+      }
+    }
+  }
+}
+
+__global__ void k_stats(const uint64_t *__restrict__ cnt, const uint64_t *__restrict__ L, int64_t G,
+                        int64_t *__restrict__ stats) {
+  long long a = 0, b = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < G; i += (int64_t)gridDim.x * blockDim.x) {
+    a += (long long)L[i];
+    b += (long long)cnt[i];
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xFFFFFFFFu, a, o);
+    b += __shfl_xor_sync(0xFFFFFFFFu, b, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (a) atomicAdd((unsigned long long *)&stats[0], (unsigned long long)a);
+    if (b) atomicAdd((unsigned long long *)&stats[1], (unsigned long long)b);
+  }
+}
+
+// shift instrumentation: slots whose (word, runend bit) changed, optionally
+// restricted to positions the old table used
+template <typename S>
+__global__ void k_diff_count(const S *__restrict__ a, const uint64_t *__restrict__ ra, const S *__restrict__ b,
+                             const uint64_t *__restrict__ rb, int64_t phys, int old_only,
+                             unsigned long long *__restrict__ out) {
+  unsigned long long c = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < phys; i += (int64_t)gridDim.x * blockDim.x) {
+    int ba = bit_at(ra, i), bb = bit_at(rb, i);
+    bool used_old = a[i] != 0 || ba;
+    if ((a[i] != b[i] || ba != bb) && (!old_only || used_old)) c++;
+  }
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
+// ---------------------------------------------------------------------------
+// exact sequential path (reference algorithm, _pykernels.py:485-656), used
+// only when a batch may hit a capacity error
+// ---------------------------------------------------------------------------
+template <typename S>
+struct SeqGqf {
+  S *slots;
+  uint64_t *occ, *run;
+  int32_t *offs;
+  int64_t *stats;
+  int64_t phys;
+  int r;
+  int32_t *scratch;  // GAP_CAP entries for this thread
+
+  static constexpr int64_t kGapCap = 2 * kRegionSlots;
+
+  __device__ int64_t rank_range(const uint64_t *bv, int64_t a, int64_t b) const {
+    int64_t n = 0;
+    for (int64_t i = a; i < b;) {
+      int64_t lo = i & 63, span = 64 - lo;
+      if (span > b - i) span = b - i;
+      uint64_t w = bv[i >> 6] >> lo;
+      if (span < 64) w &= (1ull << span) - 1;
+      n += __popcll(w);
+      i += span;
+    }
+    return n;
+  }
+  __device__ int64_t run_end_local(int64_t x, int64_t hard) const {  // pk:469-482
+    int64_t h = x >> kRegionBits, s_h = h << kRegionBits;
+    int64_t k = rank_range(occ, s_h, x + 1);
+    int64_t base = s_h + offs[h] - 1;
+    return k == 0 ? base : select_after_dev(run, base, k, hard);
+  }
+  __device__ int64_t first_unused(int64_t pos, int64_t hard) const {  // pk:485-495
+    for (int64_t x = pos; x < hard;) {
+      int64_t e = run_end_local(x, hard);
+      if (e == -2) return -2;
+      if (e < x) return x;
+      x = e + 1;
+    }
+    return -2;
+  }
+  __device__ void setb(uint64_t *bv, int64_t i, int v) const {
+    uint64_t m = 1ull << (i & 63);
+    if (v) bv[i >> 6] |= m; else bv[i >> 6] &= ~m;
+  }
+  __device__ void move_up(int64_t a, int64_t b, int64_t L) const {  // pk:498-505
+    for (int64_t i = b - 1; i >= a; i--) slots[i + L] = slots[i];
+    for (int64_t i = b - 1; i >= a; i--) setb(run, i + L, bit_at(run, i));
+    int64_t stop = a + L < b + L ? a + L : b + L;
+    for (int64_t i = a; i < stop; i++) setb(run, i, 0);
+  }
+  __device__ int64_t make_room(int64_t pos, int64_t L, int64_t hard, int64_t *far) const {  // pk:508-533
+    if (L > kGapCap) return -1;
+    int64_t x = pos;
+    for (int64_t t = 0; t < L; t++) {
+      int64_t e = first_unused(x, hard);
+      if (e < 0) return -1;
+      scratch[t] = (int32_t)e;
+      x = e + 1;
+    }
+    int64_t moved = 0;
+    for (int64_t k = L; k >= 1; k--) {
+      int64_t a = (k >= 2 ? (int64_t)scratch[k - 2] : pos - 1) + 1, b = scratch[k - 1];
+      if (b > a) { move_up(a, b, L - k + 1); moved += b - a; }
+    }
+    *far = scratch[L - 1];
+    return moved;
+  }
+  __device__ bool run_interval(int64_t quot, int64_t *s, int64_t *e) const {  // pk:536-549
+    int64_t h = quot >> kRegionBits;
+    int64_t hard = (h + 2) << kRegionBits;
+    if (hard > phys) hard = phys;
+    int64_t s_h = h << kRegionBits;
+    int64_t k = rank_range(occ, s_h, quot + 1);
+    int64_t base = s_h + offs[h] - 1;
+    int64_t prev = k == 1 ? base : select_after_dev(run, base, k - 1, hard);
+    int64_t end = select_after_dev(run, base, k, hard);
+    if (prev == -2 || end == -2) return false;
+    *s = quot > prev + 1 ? quot : prev + 1;
+    *e = end;
+    return true;
+  }
+  __device__ bool find_group(int64_t st, int64_t en, uint64_t rem, int64_t *gs, int64_t *ge, uint64_t *c,
+                             int64_t *sp) const {  // pk:552-566
+    *gs = *ge = *sp = -1;
+    *c = 0;
+    for (int64_t i = st; i <= en;) {
+      uint64_t h, cnt;
+      int64_t nx;
+      if (!parse_group_dev<S>(slots, i, en, r, &h, &cnt, &nx)) return false;
+      if (h == rem) { *gs = i; *ge = nx - 1; *c = cnt; return true; }
+      if (h > rem) { *sp = i; return true; }
+      i = nx;
+    }
+    *sp = en + 1;
+    return true;
+  }
+  __device__ bool refresh_offset(int64_t h) const {  // pk:569-576
+    int64_t b = h << kRegionBits;
+    int64_t hard = (h + 1) << kRegionBits;
+    if (hard > phys) hard = phys;
+    int64_t e = run_end_local(b - 1, hard);
+    if (e == -2) return false;
+    offs[h] = (int32_t)(e - b + 1 > 0 ? e - b + 1 : 0);
+    return true;
+  }
+  __device__ void add_stats(int64_t a, int64_t b, int64_t c) const {  // fk_atomic_add64 (ck:36)
+    if (a) atomicAdd((unsigned long long *)&stats[0], (unsigned long long)a);
+    if (b) atomicAdd((unsigned long long *)&stats[1], (unsigned long long)b);
+    if (c) atomicAdd((unsigned long long *)&stats[2], (unsigned long long)c);
+  }
+  // pk:584-656 -> 0 ok, 1 LOAD_CAPACITY, 2 SHIFT_BOUND, -9 invariant
+  __device__ int insert_one(int64_t max_occ, uint64_t fp, uint64_t delta, int64_t *moved_out) {
+    int64_t quot = (int64_t)(fp >> r);
+    uint64_t rem = fp & ((1ull << r) - 1);
+    int64_t g = quot >> kRegionBits;
+    int64_t hard = (g + 2) << kRegionBits;
+    if (hard > phys) hard = phys;
+    int64_t moved = 0, far = 0, touched = 0;
+    *moved_out = 0;
+    if (*(volatile int64_t *)&stats[0] >= max_occ) return 1;
+    if (!bit_at(occ, quot)) {
+      int64_t e = run_end_local(quot, hard);
+      if (e == -2) return 2;
+      int64_t pos = quot > e + 1 ? quot : e + 1;
+      int64_t L = (int64_t)enc_len(rem, delta, r);
+      moved = make_room(pos, L, hard, &far);
+      if (moved < 0) return 2;
+      enc_write<S>(slots, pos, rem, delta, r);
+      setb(occ, quot, 1);
+      setb(run, pos + L - 1, 1);
+      touched = far + 1;
+      add_stats(L, (int64_t)delta, 1);
+    } else {
+      int64_t s, e, gs, ge, sp;
+      uint64_t c;
+      if (!run_interval(quot, &s, &e)) return -9;
+      if (!find_group(s, e, rem, &gs, &ge, &c, &sp)) return -9;
+      if (gs >= 0) {
+        int64_t L = (int64_t)enc_len(rem, c + delta, r);
+        int64_t diff = L - (ge - gs + 1);
+        if (diff > 0) {
+          moved = make_room(ge + 1, diff, hard, &far);
+          if (moved < 0) return 2;
+          if (ge == e) { setb(run, e, 0); setb(run, e + diff, 1); }
+          touched = far + 1;
+        }
+        enc_write<S>(slots, gs, rem, c + delta, r);
+        add_stats(diff, (int64_t)delta, 0);
+      } else {
+        int64_t L = (int64_t)enc_len(rem, delta, r);
+        moved = make_room(sp, L, hard, &far);
+        if (moved < 0) return 2;
+        enc_write<S>(slots, sp, rem, delta, r);
+        if (sp == e + 1) { setb(run, e, 0); setb(run, e + L, 1); }
+        touched = far + 1;
+        add_stats(L, (int64_t)delta, 1);
+      }
+    }
+    int64_t boundary = (g + 1) << kRegionBits;
+    if (boundary < phys && touched > boundary)
+      if (!refresh_offset(g + 1)) return -9;
+    *moved_out = moved;
+    return 0;
+  }
+};
+
+// insert_many semantics: one thread, input order, stop at the first failure
+template <typename S>
+__global__ void k_gqf_exact_seq(GqfDev T, const uint64_t *__restrict__ fps, const uint64_t *__restrict__ deltas,
+                                int64_t n, int32_t *scratch, int64_t *__restrict__ result) {
+  if (blockIdx.x || threadIdx.x) return;
+  SeqGqf<S> G{reinterpret_cast<S *>(T.slots), T.occ, T.run, T.offs, T.stats, T.phys, T.r, scratch};
+  int64_t moved_total = 0;
+  result[0] = 0;
+  result[1] = -1;
+  for (int64_t k = 0; k < n; k++) {
+    int64_t mv;
+    int code = G.insert_one(T.max_occ, fps[k], deltas ? deltas[k] : 1, &mv);
+    if (code) {
+      result[0] = code;
+      result[1] = k;
+      break;
+    }
+    moved_total += mv;
+  }
+  result[2] = moved_total;
+}
+
+// bulk_insert semantics: one thread per region of one parity, each applying
+// its sorted items in order; a failure stops that region only (gqf.py:293-353)
+template <typename S>
+__global__ void k_gqf_exact_regions(GqfDev T, const uint64_t *__restrict__ fps_s, const uint64_t *__restrict__ deltas_s,
+                                    const int64_t *__restrict__ rb, int64_t nqr, int parity, int32_t *scratch,
+                                    int32_t *__restrict__ fail_code, unsigned long long *__restrict__ moved) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t g = parity + 2 * t;
+    if (g >= nqr) break;
+    int64_t lo = rb[g], hi = rb[g + 1];
+    if (lo >= hi) continue;
+    int64_t slot = gridDim.x * blockDim.x == 1 ? 0 : t;  // one scratch area per concurrent thread
+    SeqGqf<S> G{reinterpret_cast<S *>(T.slots), T.occ, T.run, T.offs, T.stats, T.phys, T.r,
+                scratch + (size_t)slot * SeqGqf<S>::kGapCap};
+    unsigned long long mv_total = 0;
+    for (int64_t k = lo; k < hi; k++) {
+      int64_t mv;
+      // stats[0] is shared by concurrent regions: the reference's workers race
+      // on it the same way (gqf.py:309-315); reads here are atomic snapshots
+      int code = G.insert_one(T.max_occ, fps_s[k], deltas_s[k], &mv);
+      if (code) {
+        fail_code[g] = code;
+        break;
+      }
+      mv_total += (unsigned long long)mv;
+    }
+    if (mv_total) atomicAdd(moved, mv_total);
+  }
+}
+
+__global__ void k_region_bounds(const uint64_t *__restrict__ fps_s, int64_t n, int shift, int64_t nqr,
+                                int64_t *__restrict__ rb) {
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g <= nqr; g += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t mark = (uint64_t)g << shift;
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+      int64_t mid = (lo + hi) >> 1;
+      if (fps_s[mid] < mark) lo = mid + 1; else hi = mid;
+    }
+    rb[g] = lo;
+  }
+}
+
+}  // namespace fk

@@ -1,5 +1,7 @@
 // tcf_point.cu -- C-ABI entry points of the point two-choice filter.
 // Kernels: tcf_point_impl.cuh (instantiated per slot width in tcf_point_s*.cu).
+#include <stdlib.h>
+
 #include "tcf_point_impl.cuh"
 
 namespace fk {
@@ -48,18 +50,28 @@ static int run(const fk_tcf_geom *g, int op, const TcfDev &P, const TcfCall &c, 
   }
 }
 
+static int64_t ord_window(int64_t n) {
+  int64_t w = 1 << 20;  // keys introduced per round (tunable: FK_ORD_WINDOW)
+  if (const char *e = getenv("FK_ORD_WINDOW")) {
+    long long v = atoll(e);
+    if (v > 0) w = v;
+  }
+  return w < n ? w : (n < 1 ? 1 : n);
+}
+
 static size_t ord_ws_layout(const fk_tcf_geom *g, int64_t n, size_t *off) {
-  // off[]: res, bres, defer_idx, defer_fp, defer_word, defer_pend, ctl
+  // off[]: res, bres, defer_idx, defer_pend, ctl, carry0, carry1
   size_t a = 0;
   auto take = [&](size_t bytes) { size_t o = a; a += (bytes + 255) & ~(size_t)255; return o; };
   int64_t cap = n < 1 ? 1 : n;
+  int64_t w = ord_window(n);
   off[0] = take((size_t)g->num_blocks * 4);
   off[1] = take((size_t)(g->backing_slots ? g->backing_slots : 1) * 4);
-  off[2] = take((size_t)cap * 8);
-  off[3] = take((size_t)cap * 8);
-  off[4] = take((size_t)cap * 8);
-  off[5] = take((size_t)cap);
-  off[6] = take(64);
+  off[2] = take((size_t)cap * 4);
+  off[3] = take((size_t)cap);
+  off[4] = take(64);
+  off[5] = take((size_t)w * 4);
+  off[6] = take((size_t)w * 4);
   return a;
 }
 
@@ -71,12 +83,13 @@ static int prep_ordered(const fk_tcf_geom *g, int64_t n, void *ws, size_t ws_byt
   char *b = (char *)ws;
   X->res = (uint32_t *)(b + off[0]);
   X->bres = (uint32_t *)(b + off[1]);
-  X->defer_idx = (int64_t *)(b + off[2]);
-  X->defer_fp = (uint64_t *)(b + off[3]);
-  X->defer_word = (uint64_t *)(b + off[4]);
-  X->defer_pend = (uint8_t *)(b + off[5]);
-  X->ctl = (unsigned int *)(b + off[6]);
+  X->defer_idx = (uint32_t *)(b + off[2]);
+  X->defer_pend = (uint8_t *)(b + off[3]);
+  X->ctl = (unsigned int *)(b + off[4]);
+  X->carry[0] = (uint32_t *)(b + off[5]);
+  X->carry[1] = (uint32_t *)(b + off[6]);
   X->defer_cap = n < 1 ? 1 : n;
+  X->window = ord_window(n);
   FK_TRY(cudaMemsetAsync(X->res, 0xFF, (size_t)g->num_blocks * 4, st));
   FK_TRY(cudaMemsetAsync(X->bres, 0xFF, (size_t)(g->backing_slots ? g->backing_slots : 1) * 4, st));
   FK_TRY(cudaMemsetAsync(X->ctl, 0, 64, st));

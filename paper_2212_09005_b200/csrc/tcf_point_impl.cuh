@@ -332,19 +332,12 @@ __global__ void __launch_bounds__(256)
 struct OrdScratch {
   uint32_t *res;        // per-block reservation word (min pending input index)
   uint32_t *bres;       // per-backing-slot reservation word
-  int64_t *defer_idx;   // keys deferred to the backing phase (unordered list)
-  uint64_t *defer_fp;
-  uint64_t *defer_word;
+  uint32_t *carry[2];   // keys carried to the next round (double-buffered)
+  uint32_t *defer_idx;  // input indices deferred to the backing phase (unordered)
   uint8_t *defer_pend;
-  unsigned int *ctl;    // [0..1] round counters, [2] defer count
+  unsigned int *ctl;    // [0..1] carry counts, [2] defer count, [3..4] backing-phase round flags
   int64_t defer_cap;
-};
-
-template <int OP>  // 0 insert, 1 delete
-struct OrdKey {
-  uint32_t b1, b2;
-  uint64_t word;  // insert: packed slot word; delete: remapped tag
-  bool pend;
+  int64_t window;       // keys introduced per round
 };
 
 // CTA-wide OR of a predicate (all threads of the CTA must call).
@@ -364,11 +357,9 @@ __device__ __forceinline__ int tile_first_free(const Tile<G> &t, const Chunk<S, 
 // Returns the placement code, or 4 = "both blocks full, defer to backing".
 template <typename S, int G, int BF>
 __device__ __forceinline__ uint8_t commit_insert(const TcfDev &P, const Tile<G> &t, uint32_t b1, uint32_t b2,
-                                                 uint64_t word) {
+                                                 uint64_t word, const Chunk<S, G, BF> &c1) {
   S *blocks = reinterpret_cast<S *>(P.blocks);
   S *blk1 = blocks + (uint64_t)b1 * P.B, *blk2 = blocks + (uint64_t)b2 * P.B;
-  Chunk<S, G, BF> c1;
-  c1.template load<true>(blk1, P.B, t.lane);
   int u1 = t.sum(c1.used());
   int slot;
   if (u1 < P.cut) {
@@ -395,13 +386,14 @@ __device__ __forceinline__ uint8_t commit_insert(const TcfDev &P, const Tile<G> 
 // tombstone the first live match of b1, else of b2.  1 = done, 0 = defer.
 template <typename S, int G, int BF>
 __device__ __forceinline__ int commit_delete(const TcfDev &P, const Tile<G> &t, uint32_t b1, uint32_t b2,
-                                             uint64_t tag) {
+                                             uint64_t tag, const Chunk<S, G, BF> &c1) {
   S *blocks = reinterpret_cast<S *>(P.blocks);
 #pragma unroll 1
   for (int which = 0; which < 2; which++) {
     S *blk = blocks + (uint64_t)(which ? b2 : b1) * P.B;
     Chunk<S, G, BF> c;
-    c.template load<true>(blk, P.B, t.lane);
+    if (which) c.template load<true>(blk, P.B, t.lane);
+    else c = c1;
     int j = c.first_match(0, tag, P.fmask);
     unsigned bal = t.ballot(j >= 0);
     if (bal) {
@@ -413,105 +405,164 @@ __device__ __forceinline__ int commit_delete(const TcfDev &P, const Tile<G> &t, 
   return 0;
 }
 
-template <typename S, int G, int BF, int K, int OP>
-__global__ void __launch_bounds__(256)
+// Recompute a deferred key's fingerprint and slot word / tag from the inputs.
+template <int OP>
+__device__ __forceinline__ void deferred_key(const TcfDev &P, const uint64_t *keys, const uint64_t *values,
+                                             uint32_t i, uint64_t *fp, uint64_t *word) {
+  uint64_t key = keys[i];
+  *fp = P.keys_are_fps ? key : mix64(key ^ P.seed);
+  uint64_t tag = remap_tag(*fp, P.fmask);
+  *word = OP == 0 ? ((P.f >= 64 ? 0 : ((values ? values[i] : 0) << P.f)) | tag) : tag;
+}
+
+template <typename S, int G, int BF, int KB, int OP>
+__global__ void __launch_bounds__(256, 4)
     k_tcf_ordered(TcfDev P, const uint64_t *__restrict__ keys, const uint64_t *__restrict__ values, int64_t n,
                   uint8_t *__restrict__ out, int64_t *__restrict__ counters, OrdScratch X) {
+  // Sliding-window deterministic reservations.  Every round introduces the
+  // next input indices [F, F+room) (all keys below the frontier F are thus
+  // introduced) plus the keys carried over from the previous round; each
+  // bids its input index on both blocks (atomicMin), and after a grid
+  // barrier a key that holds both commits -- every earlier key that could
+  // change those blocks has committed already -- while the others are
+  // carried.  The minimum pending index always commits, so the carry is
+  // bounded by the window; no round is spent draining a window tail.
   cg::grid_group grid = cg::this_grid();
   Tile<G> t;
   const int64_t tiles = (int64_t)gridDim.x * (blockDim.x / G);
   const int64_t tid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
-  const int64_t W = tiles * K;
+  const int64_t Wn = X.window;
   long long n_a = 0;  // insert: placed in a block; delete: removed
+  int64_t F = 0;
+  int64_t nc = 0;
+  int cur = 0;
   unsigned round = 0;
 
-  for (int64_t w0 = 0; w0 < n; w0 += W) {
-    OrdKey<OP> ks[K];
+  for (;;) {
+    int64_t room = Wn - nc;
+    if (room < 0) room = 0;
+    int64_t Fend = F + room < n ? F + room : n;
+    int64_t total = (Fend - F) + nc;
+    const uint32_t *cin = X.carry[cur];
+    uint32_t *cout = X.carry[cur ^ 1];
+
+    // ---- reserve --------------------------------------------------------
+    for (int64_t base = tid; base < total; base += tiles * KB) {
+      uint32_t idx[KB], b1[KB], b2[KB];
+      bool ok[KB];
 #pragma unroll
-    for (int k = 0; k < K; k++) {
-      int64_t i = w0 + tid + (int64_t)k * tiles;
-      ks[k].pend = i < n;
-      if (ks[k].pend) {
-        KeyInfo ki = key_info(P, keys[i]);
-        ks[k].b1 = (uint32_t)ki.b1;
-        ks[k].b2 = (uint32_t)ki.b2;
-        ks[k].word = OP == 0 ? ((P.f >= 64 ? 0 : ((values ? values[i] : 0) << P.f)) | ki.tag) : ki.tag;
+      for (int j = 0; j < KB; j++) {
+        int64_t e = base + (int64_t)j * tiles;
+        ok[j] = e < total;
+        idx[j] = ok[j] ? (e < nc ? __ldcg(cin + e) : (uint32_t)(F + e - nc)) : 0u;
       }
-    }
-    for (;;) {
-      // reserve: every pending key bids its input index on both blocks
+#pragma unroll
+      for (int j = 0; j < KB; j++) {
+        if (!ok[j]) continue;
+        KeyInfo ki = key_info(P, keys[idx[j]]);
+        b1[j] = (uint32_t)ki.b1;
+        b2[j] = (uint32_t)ki.b2;
+      }
       if (t.lane == 0) {
 #pragma unroll
-        for (int k = 0; k < K; k++) {
-          if (!ks[k].pend) continue;
-          uint32_t idx = (uint32_t)(w0 + tid + (int64_t)k * tiles - w0);
-          atomicMin(&X.res[ks[k].b1], idx);
-          if (ks[k].b2 != ks[k].b1) atomicMin(&X.res[ks[k].b2], idx);
+        for (int j = 0; j < KB; j++) {
+          if (!ok[j]) continue;
+          atomicMin(&X.res[b1[j]], idx[j]);
+          if (b2[j] != b1[j]) atomicMin(&X.res[b2[j]], idx[j]);
         }
       }
-      grid.sync();
-      bool left = false;
+    }
+    grid.sync();
+
+    // ---- commit ---------------------------------------------------------
+    if (blockIdx.x == 0 && threadIdx.x == 0) X.ctl[cur] = 0;  // list `cur` is consumed this round
+    for (int64_t base = tid;; base += tiles * KB) {
+      // warp-uniform trip count: lanes past the end still join the shuffles
+      if (!__any_sync(0xFFFFFFFFu, base < total)) break;
+      uint32_t idx[KB], b1[KB], b2[KB];
+      uint64_t word[KB];
+      bool ok[KB], hold[KB];
 #pragma unroll
-      for (int k = 0; k < K; k++) {
-        if (!ks[k].pend) continue;
-        int64_t i = w0 + tid + (int64_t)k * tiles;
-        uint32_t idx = (uint32_t)(i - w0);
-        int mine = 0;
-        if (t.lane == 0) mine = __ldcg(&X.res[ks[k].b1]) == idx && __ldcg(&X.res[ks[k].b2]) == idx;
-        mine = t.bcast(mine, 0);
-        if (!mine) {
-          left = true;
-          continue;
+      for (int j = 0; j < KB; j++) {
+        int64_t e = base + (int64_t)j * tiles;
+        ok[j] = e < total;
+        idx[j] = ok[j] ? (e < nc ? __ldcg(cin + e) : (uint32_t)(F + e - nc)) : 0u;
+      }
+#pragma unroll
+      for (int j = 0; j < KB; j++) {
+        if (!ok[j]) continue;
+        KeyInfo ki = key_info(P, keys[idx[j]]);
+        b1[j] = (uint32_t)ki.b1;
+        b2[j] = (uint32_t)ki.b2;
+        word[j] = OP == 0 ? ((P.f >= 64 ? 0 : ((values ? values[idx[j]] : 0) << P.f)) | ki.tag) : ki.tag;
+      }
+#pragma unroll
+      for (int j = 0; j < KB; j++)
+        hold[j] = ok[j] && __ldcg(&X.res[b1[j]]) == idx[j] && __ldcg(&X.res[b2[j]]) == idx[j];
+      Chunk<S, G, BF> c1[KB];
+      S *blocks = reinterpret_cast<S *>(P.blocks);
+#pragma unroll
+      for (int j = 0; j < KB; j++)
+        if (hold[j]) c1[j].template load<true>(blocks + (uint64_t)b1[j] * P.B, P.B, t.lane);
+      // carry the losers: one warp-aggregated atomicAdd per pass
+      {
+        unsigned mine = 0;
+#pragma unroll
+        for (int j = 0; j < KB; j++) mine += (ok[j] && !hold[j] && t.lane == 0) ? 1u : 0u;
+        unsigned lane = threadIdx.x & 31;
+        unsigned incl = mine;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          unsigned v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+          if ((int)lane >= o) incl += v;
         }
+        unsigned total_w = __shfl_sync(0xFFFFFFFFu, incl, 31);
+        unsigned basepos = 0;
+        if (lane == 31 && total_w) basepos = atomicAdd(&X.ctl[cur ^ 1], total_w);
+        basepos = __shfl_sync(0xFFFFFFFFu, basepos, 31);
+        unsigned pos = basepos + incl - mine;
+#pragma unroll
+        for (int j = 0; j < KB; j++)
+          if (ok[j] && !hold[j] && t.lane == 0) cout[pos++] = idx[j];
+      }
+#pragma unroll
+      for (int j = 0; j < KB; j++) {
+        if (!ok[j] || !hold[j]) continue;
+        bool defer;
         if (OP == 0) {
-          uint8_t code = commit_insert<S, G, BF>(P, t, ks[k].b1, ks[k].b2, ks[k].word);
-          if (t.lane == 0) {
-            if (code == 4) {
-              int64_t slot = atomicAdd(&X.ctl[2], 1u);
-              if (slot < X.defer_cap) {
-                X.defer_idx[slot] = i;
-                X.defer_fp[slot] = P.keys_are_fps ? keys[i] : mix64(keys[i] ^ P.seed);
-                X.defer_word[slot] = ks[k].word;
-                X.defer_pend[slot] = 1;
-              }
-            } else {
-              out[i] = code;
-              n_a++;
-            }
+          uint8_t code = commit_insert<S, G, BF>(P, t, b1[j], b2[j], word[j], c1[j]);
+          defer = code == 4;
+          if (!defer && t.lane == 0) {
+            out[idx[j]] = code;
+            n_a++;
           }
         } else {
-          int ok = commit_delete<S, G, BF>(P, t, ks[k].b1, ks[k].b2, ks[k].word);
-          if (t.lane == 0) {
-            if (!ok && P.bsize) {
-              int64_t slot = atomicAdd(&X.ctl[2], 1u);
-              if (slot < X.defer_cap) {
-                X.defer_idx[slot] = i;
-                X.defer_fp[slot] = P.keys_are_fps ? keys[i] : mix64(keys[i] ^ P.seed);
-                X.defer_word[slot] = ks[k].word;
-                X.defer_pend[slot] = 1;
-              }
-            } else {
-              out[i] = ok ? 1 : 0;
-              n_a += ok;
-            }
+          int done = commit_delete<S, G, BF>(P, t, b1[j], b2[j], word[j], c1[j]);
+          defer = !done && P.bsize;
+          if (!defer && t.lane == 0) {
+            out[idx[j]] = done ? 1 : 0;
+            n_a += done;
           }
         }
-        if (t.lane == 0) {  // release both reservations (only the holder writes them now)
-          X.res[ks[k].b1] = kNoRes;
-          X.res[ks[k].b2] = kNoRes;
+        if (t.lane == 0) {
+          if (defer) {
+            unsigned slot = atomicAdd(&X.ctl[2], 1u);
+            if (slot < X.defer_cap) {
+              X.defer_idx[slot] = idx[j];
+              X.defer_pend[slot] = 1;
+            }
+          }
+          X.res[b1[j]] = kNoRes;  // only the holder writes these words now
+          X.res[b2[j]] = kNoRes;
         }
-        ks[k].pend = false;
       }
-      bool any = cta_any(left);
-      if (threadIdx.x == 0) {
-        if (any) atomicAdd(&X.ctl[round & 1], 1u);
-        if (blockIdx.x == 0) X.ctl[(round + 1) & 1] = 0;
-      }
-      grid.sync();
-      unsigned cnt = __ldcg(&X.ctl[round & 1]);
-      round++;
-      if (cnt == 0) break;
     }
+    grid.sync();
+    nc = (int64_t)__ldcg(&X.ctl[cur ^ 1]);
+    cur ^= 1;
+    F = Fend;
+    round++;
+    if (F >= n && nc == 0) break;
   }
 
   // ---- backing phase: deferred keys in input-index order -------------------
@@ -526,9 +577,10 @@ __global__ void __launch_bounds__(256)
       // free probe positions, for deletes all live matches before the chain
       // ends (pk:104-117, pk:223-233)
       for (int64_t e = tid; e < nd; e += tiles) {
-        if (t.lane != 0 || !X.defer_pend[e]) continue;
-        uint32_t idx = (uint32_t)X.defer_idx[e];
-        uint64_t fp = X.defer_fp[e], word = X.defer_word[e];
+        if (t.lane != 0 || !__ldcg(&X.defer_pend[e])) continue;
+        uint32_t idx = __ldcg(&X.defer_idx[e]);
+        uint64_t fp, word;
+        deferred_key<OP>(P, keys, values, idx, &fp, &word);
         if (!P.bsize) continue;
         uint64_t p = fmod64(mix64(fp ^ kBackStart), P.bsm);
         uint64_t step = fmod64(mix64(fp ^ kBackStep) | 1, P.bsm);
@@ -547,10 +599,11 @@ __global__ void __launch_bounds__(256)
       grid.sync();
       bool left = false;
       for (int64_t e = tid; e < nd; e += tiles) {
-        if (t.lane != 0 || !X.defer_pend[e]) continue;
-        int64_t i = X.defer_idx[e];
-        uint32_t idx = (uint32_t)i;
-        uint64_t fp = X.defer_fp[e], word = X.defer_word[e];
+        if (t.lane != 0 || !__ldcg(&X.defer_pend[e])) continue;
+        uint32_t idx = __ldcg(&X.defer_idx[e]);
+        int64_t i = idx;
+        uint64_t fp, word;
+        deferred_key<OP>(P, keys, values, idx, &fp, &word);
         int64_t target = -1;
         if (P.bsize) {
           uint64_t p = fmod64(mix64(fp ^ kBackStart), P.bsm);
@@ -592,11 +645,11 @@ __global__ void __launch_bounds__(256)
       }
       bool any = cta_any(left);
       if (threadIdx.x == 0) {
-        if (any) atomicAdd(&X.ctl[round & 1], 1u);
-        if (blockIdx.x == 0) X.ctl[(round + 1) & 1] = 0;
+        if (any) atomicAdd(&X.ctl[3 + (round & 1)], 1u);
+        if (blockIdx.x == 0) X.ctl[3 + ((round + 1) & 1)] = 0;
       }
       grid.sync();
-      unsigned cnt = __ldcg(&X.ctl[round & 1]);
+      unsigned cnt = __ldcg(&X.ctl[3 + (round & 1)]);
       round++;
       if (cnt == 0) break;
     }
@@ -614,12 +667,12 @@ __global__ void __launch_bounds__(256)
 // Dispatch over (G, compile-time B) for one slot type -------------------------
 // BF=16 is the vectorised fast path for the default/benchmarked geometry
 // (B=16); BF=32 the CG-32 sweep point (B=32, u16); everything else BF=0.
-constexpr int kOrdK = 4;
+constexpr int kOrdKB = 4;  // items per thread per pass in the ordered kernel
 
 template <typename S, int G, int BF, int OP>
 static int launch_ordered(const TcfDev &P, const uint64_t *keys, const uint64_t *values, int64_t n, uint8_t *out,
                           int64_t *counters, OrdScratch X, cudaStream_t st) {
-  auto kern = k_tcf_ordered<S, G, BF, kOrdK, OP>;
+  auto kern = k_tcf_ordered<S, G, BF, kOrdKB, OP>;
   int per_sm = 0;
   FK_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
   if (per_sm < 1) return FK_E_ARG;

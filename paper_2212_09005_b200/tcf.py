@@ -32,6 +32,7 @@ from enum import IntEnum
 import numpy as np
 
 from . import _lib
+from ._device import DeviceTables as _DeviceTables, check_backend as _check_backend
 from .errors import FilterFullError, ValidationError
 from .hashing import EMPTY, TOMBSTONE
 
@@ -114,54 +115,6 @@ class TcfParams:
 _MODES = {"ordered": _lib.FK_ORDERED, "concurrent": _lib.FK_CONCURRENT}
 
 
-def _check_backend(backend):
-    if backend not in ("auto", "cuda", "c"):
-        if backend == "py":
-            raise RuntimeError("the pure-Python backend does not exist in the B200 build")
-        raise ValueError("unknown backend %r (expected 'auto' or 'cuda')" % (backend,))
-
-
-class _DeviceTables:
-    """Named device byte buffers with lazily synced host mirrors.
-
-    Reading ``_blocks`` & co. returns a host numpy copy (D2H on first access
-    after a device write).  Tests in the reference mutate those arrays in
-    place; a handed-out mirror is therefore pushed back (H2D)
-    before the next device operation.
-    """
-
-    def __init__(self, torch, device, spec):
-        self.torch, self.device = torch, device
-        self.spec = dict(spec)  # name -> (dtype, count)
-        self.dev = {n: torch.zeros(max(1, c * np.dtype(dt).itemsize), dtype=torch.uint8, device=device)
-                    for n, (dt, c) in self.spec.items()}
-        self.mirror = {}
-        self.lent = set()
-
-    def ptr(self, name):
-        dt, c = self.spec[name]
-        return _lib.dptr(self.dev[name]) if c else _lib.c_vp(0)
-
-    def host(self, name):
-        if name not in self.mirror:
-            dt, c = self.spec[name]
-            self.mirror[name] = _lib.host_view(self.torch, self.dev[name], dt)[:c] if c else \
-                np.zeros(0, dtype=dt)
-        self.lent.add(name)
-        return self.mirror[name]
-
-    def before_device_op(self):
-        for name in self.lent:
-            dt, c = self.spec[name]
-            if c:
-                src = self.torch.from_numpy(np.ascontiguousarray(self.mirror[name]).view(np.uint8).copy())
-                self.dev[name][: src.numel()].copy_(src.to(self.device))
-        self.lent.clear()
-
-    def after_device_write(self):
-        self.mirror.clear()
-
-
 class Tcf:
     """Two-choice filter with point (per-key) operations on the B200."""
 
@@ -175,7 +128,7 @@ class Tcf:
             raise ValueError("mode must be 'ordered' or 'concurrent'")
         self.params = params
         self.mode = mode
-        torch = _lib.require_cuda()
+        torch = _lib.require_cuda(device)
         self._torch = torch
         self._device = torch.device(device) if device is not None else \
             torch.device("cuda", torch.cuda.current_device())
@@ -206,9 +159,34 @@ class Tcf:
 
     # -- plumbing -------------------------------------------------------------
     def _keys_in(self, keys):
+        """-> (device int64 tensor, kind); kind is 'cuda' (results stay on the
+        device, asynchronous), 'host' (a CPU torch tensor, e.g. pinned: results
+        come back as CPU tensors) or 'numpy'."""
         torch = self._torch
-        on_dev = isinstance(keys, torch.Tensor) and keys.is_cuda
-        return _lib.to_device_u64(torch, keys, self._device), on_dev
+        if isinstance(keys, torch.Tensor):
+            kind = "cuda" if keys.is_cuda else "host"
+        else:
+            kind = "numpy"
+        return _lib.to_device_u64(torch, keys, self._device), kind
+
+    def _ret(self, t, kind):
+        if kind == "cuda":
+            return t
+        if kind == "host":
+            out = self._torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+            out.copy_(t, non_blocking=True)
+            self._torch.cuda.current_stream().synchronize()
+            return out
+        return t.cpu().numpy()
+
+    def _reset(self):
+        """Zero every table and counter (benchmark helper; not in the reference API)."""
+        with self._op_lock:
+            for t in self._t.dev.values():
+                t.zero_()
+            self._counters_dev.zero_()
+            self._t.mirror.clear()
+            self._t.lent.clear()
 
     def _check_values(self, values, n, on_dev):
         torch = self._torch
@@ -237,12 +215,6 @@ class Tcf:
             return None, 0
         return self._torch.empty(nbytes, dtype=self._torch.uint8, device=self._device), nbytes
 
-    def _out(self, t, on_dev, dtype=None):
-        if on_dev:
-            return t
-        a = t.cpu().numpy()
-        return a if dtype is None else a.view(dtype)
-
     # -- point operations -------------------------------------------------------
     def insert(self, key, value=0):
         code = int(self.insert_many([key], [value])[0])
@@ -268,7 +240,7 @@ class Tcf:
                     mode, _lib.dptr(ws), wsb, _lib.stream_ptr(torch))
                 _lib.check(rc, "tcf insert")
                 self._t.after_device_write()
-        return self._out(codes, on_dev)
+        return self._ret(codes, on_dev)
 
     def query(self, key):
         return bool(self.query_many([key])[0])
@@ -278,14 +250,17 @@ class Tcf:
         return bool(found[0]), int(values[0])
 
     def query_many(self, keys):
-        return self.query_values_many(keys)[0]
+        return self._query(keys, False)[0]
 
     def query_values_many(self, keys):
+        return self._query(keys, True)
+
+    def _query(self, keys, want_values):
         torch = self._torch
         k, on_dev = self._keys_in(keys)
         n = k.numel()
         found = torch.empty(n, dtype=torch.uint8, device=self._device)
-        vals = torch.empty(n, dtype=torch.int64, device=self._device)
+        vals = torch.empty(n if want_values else 0, dtype=torch.int64, device=self._device)
         if n:
             with self._op_lock:
                 self._t.before_device_op()
@@ -293,9 +268,11 @@ class Tcf:
                     ctypes_byref(self._geom), self._t.ptr("blocks"), self._t.ptr("backing"),
                     _lib.dptr(k), 0, n, _lib.dptr(found), _lib.dptr(vals), _lib.stream_ptr(torch))
                 _lib.check(rc, "tcf query")
-        if on_dev:
-            return found.bool(), vals
-        return found.cpu().numpy().astype(bool), vals.cpu().numpy().view(np.uint64)
+        if on_dev == "cuda":
+            return found.bool(), (vals if want_values else None)
+        if on_dev == "host":
+            return self._ret(found, "host").bool(), (self._ret(vals, "host") if want_values else None)
+        return found.cpu().numpy().astype(bool), (vals.cpu().numpy().view(np.uint64) if want_values else None)
 
     def delete(self, key):
         return bool(self.delete_many([key])[0])
@@ -316,8 +293,10 @@ class Tcf:
                     _lib.dptr(ws), wsb, _lib.stream_ptr(torch))
                 _lib.check(rc, "tcf delete")
                 self._t.after_device_write()
-        if on_dev:
+        if on_dev == "cuda":
             return removed.bool()
+        if on_dev == "host":
+            return self._ret(removed, "host").bool()
         return removed.cpu().numpy().astype(bool)
 
     # -- inspection (quiescent; host mirrors) ------------------------------------

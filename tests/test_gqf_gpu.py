@@ -1,0 +1,270 @@
+"""GQF parity on the B200: the CUDA path vs the CPU oracle / reference goldens.
+
+Bit-exact: table image (_slots/_occupieds/_runends/_offsets/_stats), counts,
+delete found flags, capacity errors (code, failure point, partial image).
+"""
+
+import numpy as np
+import pytest
+
+from conftest import counter_keys
+
+pytestmark = pytest.mark.gpu
+
+IMG = ("slots", "occupieds", "runends", "offsets", "stats")
+_INV1 = pow(0xBF58476D1CE4E5B9, -1, 2 ** 64)
+_INV2 = pow(0x94D049BB133111EB, -1, 2 ** 64)
+M64 = 2 ** 64 - 1
+
+
+def _unshift(x, s):
+    y = x
+    for _ in range(64 // s + 1):
+        y = x ^ (y >> s)
+    return y
+
+
+def unmix64(x):
+    x = _unshift(x, 31)
+    x = (x * _INV2) & M64
+    x = _unshift(x, 27)
+    x = (x * _INV1) & M64
+    return _unshift(x, 30)
+
+
+def craft(g, pairs):
+    p = g.params
+    return np.array([unmix64((qt << p.r) | rem) ^ p.seed for qt, rem in pairs], dtype=np.uint64)
+
+
+def _oracle(g, oracle):
+    p = g.params
+    return oracle.OracleGqf(p.q, p.r, p.seed, p.max_occupied)
+
+
+def same_image(g, o):
+    img = o.image()
+    for nm in IMG:
+        assert np.array_equal(getattr(g, "_" + nm), img[nm]), nm
+
+
+def golden_image(g, t, pre):
+    for nm in IMG:
+        assert np.array_equal(getattr(g, "_" + nm), t[pre + nm]), (pre, nm)
+
+
+@pytest.mark.parametrize("r", [8, 16])
+def test_golden_sequence(golden, r):
+    from paper_2212_09005_b200 import Gqf
+    t = golden("gqf")
+    pre = "r%d_" % r
+    g = Gqf(q=14, r=r)
+    g.insert_many(t[pre + "k"], t[pre + "c"])
+    golden_image(g, t, pre + "ins_")
+    assert np.array_equal(g.count_many(t[pre + "k"]), t[pre + "count"])
+    assert np.array_equal(g.delete_many(t[pre + "dk"], t[pre + "dc"]).astype(np.uint8), t[pre + "dfound"])
+    golden_image(g, t, pre + "del_")
+    g.bulk_insert(t[pre + "k2"])
+    golden_image(g, t, pre + "bulk_")
+    assert np.array_equal(g.bulk_delete(t[pre + "kk"]).astype(np.uint8), t[pre + "bfound"])
+    golden_image(g, t, pre + "bdel_")
+    g.validate()
+
+
+def test_golden_duplicates_and_mapreduce(golden):
+    from paper_2212_09005_b200 import Gqf
+    t = golden("gqf")
+    g = Gqf(q=16, r=8)
+    g.bulk_insert(t["ur_keys"])
+    golden_image(g, t, "ur_")
+    uq, uc = np.unique(t["ur_keys"], return_counts=True)
+    assert np.array_equal(g.count_many(uq), t["ur_count"])
+    g2 = Gqf(q=16, r=8)
+    g2.bulk_insert(uq, uc.astype(np.uint64))
+    golden_image(g2, t, "ur_")
+
+
+def test_golden_capacity_partial_image(golden):
+    from paper_2212_09005_b200 import CapacityError, Gqf
+    t = golden("gqf")
+    g = Gqf(q=10, r=8)
+    with pytest.raises(CapacityError):
+        g.insert_many(t["cap_k"])
+    golden_image(g, t, "cap_")
+    g.validate()
+
+
+def test_crafted_layouts():
+    from paper_2212_09005_b200 import Gqf
+    g = Gqf(q=8, r=8, seed=1)
+    g.insert_many(craft(g, [(50, 9), (50, 3), (50, 200)]))
+    assert g.find_run(50) == (50, 52)
+    assert g._slots[50:53].tolist() == [3, 9, 200]
+    g = Gqf(q=8, r=8, seed=2)
+    g.insert_many(craft(g, [(5, 10), (5, 20), (6, 30), (7, 40)]))
+    assert [g.find_run(x) for x in (5, 6, 7)] == [(5, 6), (7, 7), (8, 8)]
+    assert g.find_run(99) == (-1, -1)
+    g = Gqf(q=8, r=8, seed=6)
+    key = int(craft(g, [(10, 7)])[0])
+    for add in (1, 1, 298):
+        g.insert(key, count=add)
+    assert g.count(key) == 300
+    assert g._slots[10:14].tolist() == [7, 4, 43, 7]
+    assert g.delete(key, count=250) and g.count(key) == 50
+    assert g.delete(key, count=50) and g.count(key) == 0 and not g.query(key)
+    g.validate()
+
+
+@pytest.mark.parametrize("q,r,n,seed", [(12, 8, 3000, 1), (16, 16, 50_000, 2), (18, 8, 230_000, 3)])
+def test_point_ops_vs_oracle(oracle, q, r, n, seed):
+    from paper_2212_09005_b200 import Gqf
+    rng = np.random.default_rng(seed)
+    g = Gqf(q=q, r=r, seed=seed)
+    o = _oracle(g, oracle)
+    keys = rng.integers(0, 2 ** 63, n, dtype=np.uint64)
+    counts = rng.integers(1, 4, n, dtype=np.uint64)
+    code, _ = o.insert_many(keys, counts)
+    assert code == 0
+    g.insert_many(keys, counts)
+    same_image(g, o)
+    probe = np.concatenate([keys[: n // 2], rng.integers(0, 2 ** 63, n // 2, dtype=np.uint64)])
+    assert np.array_equal(g.count_many(probe), o.count_many(probe))
+    for qt in rng.integers(0, 1 << q, 200).tolist():
+        assert g.find_run(qt) == o.find_run(qt)
+    d = np.concatenate([keys[::3], keys[:100], probe[-100:]])
+    dc = rng.integers(1, 3, len(d), dtype=np.uint64)
+    assert np.array_equal(g.delete_many(d, dc), o.delete_many(d, dc))
+    same_image(g, o)
+    g.validate()
+
+
+@pytest.mark.parametrize("dist", ["uniform", "ur_count", "zipf"])
+def test_bulk_ops_vs_oracle(oracle, dist):
+    from paper_2212_09005_b200 import Gqf
+    from paper_2212_09005_b200.workloads import WorkloadSpec, gen_keys
+    q = 18
+    spec = {"uniform": WorkloadSpec("uniform", n=int(0.85 * 2 ** q), seed=4),
+            "ur_count": WorkloadSpec("ur_count", n=int(0.9 * 2 ** q) // 8, seed=4),
+            "zipf": WorkloadSpec("zipf", n=200_000, seed=4, universe=100_000)}[dist]
+    keys = gen_keys(spec)
+    g = Gqf(q=q, r=8)
+    o = _oracle(g, oracle)
+    assert o.bulk_insert(keys) == []
+    g.bulk_insert(keys)
+    same_image(g, o)
+    g.validate()
+    dk = np.concatenate([keys[::4], keys[:1000]])
+    assert np.array_equal(g.bulk_delete(dk), o.bulk_delete(dk))
+    same_image(g, o)
+    dc = np.full(5000, 3, np.uint64)
+    assert np.array_equal(g.bulk_delete(keys[-5000:], dc), o.bulk_delete(keys[-5000:], dc))
+    same_image(g, o)
+    g.validate()
+
+
+def test_bulk_equals_point_equals_mapreduce(oracle):
+    from paper_2212_09005_b200 import Gqf
+    rng = np.random.default_rng(9)
+    keys = rng.integers(0, 2 ** 40, 40_000, dtype=np.uint64)
+    keys = np.concatenate([keys, keys[:5000], keys[:100]])
+    a, b, c = Gqf(q=16, r=8), Gqf(q=16, r=8), Gqf(q=16, r=8)
+    a.bulk_insert(keys)
+    b.insert_many(rng.permutation(keys))
+    u, cnt = np.unique(keys, return_counts=True)
+    c.bulk_insert(u, cnt.astype(np.uint64))
+    for nm in IMG:
+        assert np.array_equal(getattr(a, "_" + nm), getattr(b, "_" + nm))
+        assert np.array_equal(getattr(a, "_" + nm), getattr(c, "_" + nm))
+
+
+def test_load_capacity_point_and_bulk(oracle):
+    from paper_2212_09005_b200 import CapacityError, Gqf
+    rng = np.random.default_rng(11)
+    for trial in range(3):
+        keys = rng.integers(0, 2 ** 50, 1100 + 50 * trial, dtype=np.uint64)
+        g = Gqf(q=10, r=8)
+        o = _oracle(g, oracle)
+        code, idx = o.insert_many(keys)
+        assert code != 0
+        with pytest.raises(CapacityError):
+            g.insert_many(keys)
+        same_image(g, o)
+        g = Gqf(q=10, r=8)
+        o = _oracle(g, oracle)
+        assert o.bulk_insert(keys) != []
+        with pytest.raises(CapacityError):
+            g.bulk_insert(keys)
+        same_image(g, o)
+
+
+def test_shift_bound_rem0_unary(oracle):
+    """A remainder-0 group spends one slot per copy (countgroups.py:14-16):
+    a large count crosses the region hard bound -> SHIFT_BOUND, table intact."""
+    from paper_2212_09005_b200 import CapacityError, Gqf
+    g = Gqf(q=15, r=8, seed=3)
+    o = _oracle(g, oracle)
+    k = craft(g, [(100, 0), (8000, 5), (8100, 0)])
+    cnt = np.array([20_000, 1, 9000], dtype=np.uint64)
+    code, idx = o.insert_many(k, cnt)
+    assert code == 2
+    with pytest.raises(CapacityError, match="hard bound"):
+        g.insert_many(k, cnt)
+    same_image(g, o)
+    g.validate()
+
+
+def test_validate_detects_corruption():
+    from paper_2212_09005_b200 import Gqf, ValidationError
+    g = Gqf(q=12, r=8)
+    g.insert_many(np.random.default_rng(3).integers(0, 2 ** 40, 2000, dtype=np.uint64))
+    g.validate()
+    s = g._slots
+    i = int(np.flatnonzero(s == 0)[-1])
+    s[i] = 7
+    with pytest.raises(ValidationError):
+        g.validate()
+    s[i] = 0
+    g.validate()
+    g._offsets[1] += 1
+    with pytest.raises(ValidationError):
+        g.validate()
+
+
+def test_mirror_edits_reach_device():
+    from paper_2212_09005_b200 import Gqf
+    g = Gqf(q=10, r=8, seed=2)
+    key = int(craft(g, [(7, 9)])[0])
+    g.insert(key, 5)
+    assert g.count(key) == 5
+    s = g._slots
+    pos = g.find_run(7)[0]
+    assert s[pos:pos + 4].tolist() == [9, 3, 0, 9] or g.count(key) == 5
+    # rewrite the count group by hand: [9, 9] = count 2
+    s[pos:pos + 4] = [9, 9, 0, 0]
+    rb = g._runends
+    rb[(pos + 3) >> 6] &= ~np.uint64(1 << ((pos + 3) & 63))
+    rb[(pos + 1) >> 6] |= np.uint64(1 << ((pos + 1) & 63))
+    assert g.count(key) == 2  # the device saw the edited image and re-derived its index
+
+
+def test_empty_and_stats():
+    from paper_2212_09005_b200 import Gqf
+    g = Gqf(q=8)
+    g.bulk_insert(np.zeros(0, np.uint64))
+    assert len(g.bulk_delete(np.zeros(0, np.uint64))) == 0
+    assert g.occupied_slots == 0 and g.total_items == 0 and g.distinct_items == 0
+    g.insert_many([1, 2, 3], [1, 1, 5])
+    assert g.total_items == 7 and g.distinct_items == 3
+    assert g.size_bits() == (g.params.physical_slots * 8 + 2 * (g.params.physical_slots // 64) * 64
+                             + g.params.num_regions * 32) + g.params.num_regions * 512
+
+
+def test_shift_instrumentation():
+    from paper_2212_09005_b200 import Gqf
+    g = Gqf(q=13, r=8, seed=28)
+    keys = np.unique(np.random.default_rng(12).integers(0, 2 ** 50, 3000, dtype=np.uint64))
+    g.bulk_insert(keys, workers=2)
+    assert g.shifted_slots == 0
+    g = Gqf(q=13, r=8, seed=28)
+    g.insert_many(np.random.default_rng(12).integers(0, 2 ** 50, 3000, dtype=np.uint64))
+    assert g.shifted_slots > 0
