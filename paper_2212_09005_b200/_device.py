@@ -44,15 +44,16 @@ class DeviceTables:
         return self.mirror[name]
 
     def before_device_op(self):
-        """Push handed-out mirrors back; returns True if any was pushed."""
-        pushed = False
+        """Push handed-out mirrors back (they stay lent -- the caller may still
+        hold and edit them -- until a device write replaces them); returns
+        the set of names pushed."""
+        pushed = set()
         for name in self.lent:
             dt, c = self.spec[name]
             if c:
                 src = self.torch.from_numpy(np.ascontiguousarray(self.mirror[name]).view(np.uint8).copy())
                 self.dev[name][: src.numel()].copy_(src.to(self.device))
-                pushed = True
-        self.lent.clear()
+                pushed.add(name)
         return pushed
 
     def zero(self):
@@ -63,6 +64,7 @@ class DeviceTables:
 
     def after_device_write(self):
         self.mirror.clear()
+        self.lent.clear()
 
 
 def keys_in(torch, keys, device):

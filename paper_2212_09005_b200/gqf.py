@@ -157,7 +157,7 @@ class Gqf:
 
     def _sync_in(self):
         """Push host edits of the image back and re-derive the run index."""
-        if self._cur.before_device_op():
+        if self._cur.before_device_op() & {"occupieds", "runends"}:
             _lib.check(self._lib.fk_gqf_rebuild_index(ctypes.byref(self._geom), ctypes.byref(self._tables(self._cur)),
                                                       _lib.stream_ptr(self._torch)), "gqf index")
 
