@@ -101,6 +101,57 @@ int fk_tcf_delete(const fk_tcf_geom *g, void *blocks, void *backing, const uint6
                   int keys_are_fps, int64_t n, uint8_t *removed, int64_t *counters, int mode,
                   void *workspace, size_t ws_bytes, void *stream);
 
+/* ---- bulk TCF (sorted, front-packed blocks) ----------------------------- */
+
+/* Geometry, derived on the host exactly as BulkTcfParams (tcf_bulk.py:43-77).
+ * slot_bytes is the smallest of {1,2,4} holding tag_bits (tcf_bulk.py:80-84);
+ * block_slots <= 8192 (one block is staged in shared memory). */
+typedef struct fk_btcf_geom {
+    int64_t num_blocks;
+    int64_t backing_slots;
+    int32_t block_slots;
+    int32_t tag_bits;
+    int32_t slot_bytes;
+    int32_t cut_slots;
+    int32_t probe_limit;
+    int32_t reserved;
+    uint64_t seed;
+} fk_btcf_geom;
+
+/* replaces BulkTcf.insert_batch's kernel sequence (tcf_bulk.py:179-257):
+ * _partition_fps + btcf_merge_lists (shortcut) + btcf_route + btcf_merge_lists
+ * (dest-grouped) + backing_insert_batch.  `fill` is the device u32[nb] fill
+ * array.  failed_keys (device u64[n]) receives the keys the backing table
+ * could not take, in the reference's order; *n_failed (device int64) their
+ * count.  counters (device int64[3]) += inserts_ok, inserts_backing.
+ * status (device u32, caller sets 0xFFFFFFFF) receives 1 + the lowest block a
+ * merge would overfill (the reference's AssertionError).  Synchronises the
+ * stream twice (batch-dependent sizes); scratch is stream-ordered
+ * cudaMallocAsync memory released before return. */
+int fk_btcf_insert(const fk_btcf_geom *g, void *blocks, uint32_t *fill, void *backing, const uint64_t *keys,
+                   int keys_are_fps, int64_t n, uint64_t *failed_keys, int64_t *n_failed, int64_t *counters,
+                   uint32_t *status, void *stream);
+
+/* replaces btcf_query_batch (_ckernels.pyx:552-599); asynchronous. */
+int fk_btcf_query(const fk_btcf_geom *g, const void *blocks, const uint32_t *fill, const void *backing,
+                  const uint64_t *keys, int keys_are_fps, int64_t n, uint8_t *found, void *stream);
+
+/* replaces BulkTcf.delete_batch (tcf_bulk.py:283-325): btcf_delete_blocklocal
+ * over primary then secondary blocks, then backing_delete_batch.  removed
+ * (device u8[n]) per input key; counters[2] += removed. */
+int fk_btcf_delete(const fk_btcf_geom *g, void *blocks, uint32_t *fill, void *backing, const uint64_t *keys,
+                   int keys_are_fps, int64_t n, uint8_t *removed, int64_t *counters, void *stream);
+
+/* replaces _partition_fps (tcf_bulk.py:133-143): sorted_keys[i] =
+ * (b1 << tag_bits) | word in stable order, order[i] = input position. */
+int fk_btcf_partition(const fk_btcf_geom *g, const uint64_t *keys, int keys_are_fps, int64_t n,
+                      uint64_t *sorted_keys, uint32_t *order, void *stream);
+
+/* replaces btcf_merge_lists (_ckernels.pyx:379-405) over all blocks: block b
+ * merges words (sorted_keys[i] & tag mask) for i in [seg_lo[b], seg_hi[b]). */
+int fk_btcf_merge_lists(const fk_btcf_geom *g, void *blocks, uint32_t *fill, const uint64_t *sorted_keys,
+                        const uint32_t *seg_lo, const uint32_t *seg_hi, uint32_t *status, void *stream);
+
 /* ---- GQF (counting quotient filter) ------------------------------------- */
 
 /* Geometry, derived on the host exactly as GqfParams (gqf.py:52-95). */

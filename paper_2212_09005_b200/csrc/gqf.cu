@@ -4,35 +4,12 @@
 
 #include <vector>
 
+#include "fk_scratch.cuh"
 #include "gqf_impl.cuh"
 
 namespace fk {
 
 namespace {
-
-// Stream-ordered scratch that frees itself (cudaMallocAsync pool).
-struct Scratch {
-  cudaStream_t st;
-  std::vector<void *> ptrs;
-  cudaError_t err = cudaSuccess;
-  explicit Scratch(cudaStream_t s) : st(s) {}
-  ~Scratch() {
-    for (void *p : ptrs) cudaFreeAsync(p, st);
-  }
-  template <typename T>
-  T *get(size_t count) {
-    void *p = nullptr;
-    size_t bytes = count * sizeof(T);
-    if (bytes == 0) bytes = 16;
-    cudaError_t e = cudaMallocAsync(&p, bytes, st);
-    if (e != cudaSuccess) {
-      err = e;
-      return nullptr;
-    }
-    ptrs.push_back(p);
-    return reinterpret_cast<T *>(p);
-  }
-};
 
 inline int blocks_for(int64_t n, int per = 256) {
   int64_t b = (n + per - 1) / per;

@@ -1,0 +1,953 @@
+// tcf_bulk.cu -- bulk two-choice filter on sm_100a.
+//
+// Replaces the bulk half of the reference kernel contract together with the
+// numpy orchestration around it (fk/tcf_bulk.py:133-325):
+//   partition            _partition_fps            tcf_bulk.py:133-143
+//   phase-1 shortcut     btcf_merge_lists          tcf_bulk.py:191-208, ck:379-405
+//   two-choice routing   btcf_route                tcf_bulk.py:210-223, ck:408-444
+//   dest-grouped merge   btcf_merge_lists          tcf_bulk.py:225-245
+//   backing overflow     backing_insert_batch      tcf_bulk.py:247-255, ck:447-466
+//   query                btcf_query_batch          ck:552-599
+//   3-pass delete        btcf_delete_blocklocal +  tcf_bulk.py:283-325, ck:482-549
+//                        backing_delete_batch
+//
+// Blocks hold B tag words sorted and front-packed (fill[b] live words, the
+// tail EMPTY).  Partitioning is a stable CUB radix sort of (block << f | word)
+// over exactly the significant bits, so equal keys keep input order as numpy's
+// stable argsort does.  Per-block merges/deletes run one warp per block with
+// the block staged in shared memory; output positions come from merge-path
+// ranks (lower/upper bounds), so a merge is one pass with no serial loop.
+// The reference's routing is a sequential greedy pass over the leftovers; it
+// is reproduced exactly by windowed deterministic reservations (a leftover
+// commits once it holds the minimum pending index on both of its blocks),
+// and the ordered backing inserts/deletes likewise by reservations on probe
+// positions.  Every result -- table image, fill, failed keys and their order,
+// removed flags, counters -- is bit-identical to the reference.
+#include <cub/cub.cuh>
+
+#include "../../include/filterkit_b200.h"
+#include "fk_common.cuh"
+#include "fk_scratch.cuh"
+
+namespace fk {
+
+namespace {
+
+constexpr uint32_t kNone = 0xFFFFFFFFu;
+
+struct BDev {
+  void *blocks;
+  uint32_t *fill;
+  void *backing;
+  uint64_t nb;
+  FastMod nbm;
+  uint64_t bsize;
+  FastMod bsm;
+  int B, f, cut, probe_limit;
+  uint64_t fmask;
+  uint64_t seed;
+  int keys_are_fps;
+};
+
+inline int grid_for(int64_t n, int per = 256) {
+  int64_t b = (n + per - 1) / per;
+  int64_t cap = (int64_t)num_sms() * 16;
+  if (b > cap) b = cap;
+  return (int)(b < 1 ? 1 : b);
+}
+
+__device__ __forceinline__ uint64_t key_fp(const BDev &P, uint64_t key) {
+  return P.keys_are_fps ? key : mix64(key ^ P.seed);  // tcf_bulk.py:115-117
+}
+
+// ---------------------------------------------------------------------------
+// partition keys: sort key = (block << f) | word, value = position
+// ---------------------------------------------------------------------------
+// which: 0 = primary block, 1 = secondary block.  idx == nullptr: items are
+// keys[0..n); else items are keys[idx[0..n)] (delete passes over pending keys).
+__global__ void k_part_keys(BDev P, const uint64_t *__restrict__ keys, const uint32_t *__restrict__ idx, int64_t n,
+                            int which, uint64_t *__restrict__ skey, uint32_t *__restrict__ sval) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t src = idx ? idx[i] : (uint32_t)i;
+    uint64_t fp = key_fp(P, keys[src]);
+    uint64_t word = remap_tag(fp, P.fmask);
+    uint64_t b = fmod64(mix64(fp ^ (which ? kBlock2 : kBlock1)), P.nbm);
+    skey[i] = (b << P.f) | word;
+    sval[i] = src;
+  }
+}
+
+// seg_lo/seg_hi[s] = [first, last+1) sorted position of segment s = skey >> f
+// (arrays pre-zeroed: absent segments stay empty).
+__global__ void k_seg_bounds(const uint64_t *__restrict__ skey, int64_t n, int f, uint32_t *__restrict__ seg_lo,
+                             uint32_t *__restrict__ seg_hi) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t s = skey[p] >> f;
+    if (p == 0 || (skey[p - 1] >> f) != s) seg_lo[s] = (uint32_t)p;
+    if (p == n - 1 || (skey[p + 1] >> f) != s) seg_hi[s] = (uint32_t)(p + 1);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// per-block merge (btcf_merge_lists, ck:363-405): one warp per block
+// ---------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ int lower_bound_s(const T *a, int n, uint32_t v) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if ((uint32_t)a[mid] < v) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+template <typename T>
+__device__ __forceinline__ int upper_bound_s(const T *a, int n, uint32_t v) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if ((uint32_t)a[mid] <= v) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+__device__ __forceinline__ int64_t lower_bound_g(const uint64_t *a, int64_t lo, int64_t hi, uint64_t v) {
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (a[mid] < v) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+__device__ __forceinline__ int64_t upper_bound_g(const uint64_t *a, int64_t lo, int64_t hi, uint64_t v) {
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (a[mid] <= v) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// phase1 = 1: take = min(len, max(0, cut - fill)) and flag the rest of the
+// segment as leftovers (tcf_bulk.py:191-213); phase1 = 0: merge everything.
+// Segment s of block b is s = b + seg_off (seg_off = 1 for the dest-grouped
+// pass, whose segment 0 is the backing list).  Overflow -> atomicMin(status,
+// 1 + b) and the block is left untouched (the reference asserts).
+template <typename S>
+__global__ void __launch_bounds__(256) k_btcf_merge(BDev P, const uint64_t *__restrict__ skey,
+                                                    const uint32_t *__restrict__ seg_lo,
+                                                    const uint32_t *__restrict__ seg_hi, int seg_off, int phase1,
+                                                    uint8_t *__restrict__ left, unsigned *__restrict__ status) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int B = P.B;
+  S *E = reinterpret_cast<S *>(smem_raw) + (size_t)wib * 2 * B;
+  S *I = E + B;
+  S *blocks = reinterpret_cast<S *>(P.blocks);
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t b = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib; b < (int64_t)P.nb; b += warps) {
+    uint32_t lo = seg_lo[b + seg_off], hi = seg_hi[b + seg_off];
+    if (hi <= lo) continue;
+    uint32_t span = hi - lo;
+    int len = span > 0x7FFFFFFFu ? 0x7FFFFFFF : (int)span;
+    int cur = (int)P.fill[b];
+    int take = len;
+    if (phase1) {
+      int room = P.cut - cur;
+      room = room < 0 ? 0 : room;
+      take = len < room ? len : room;
+      for (int64_t p = (int64_t)lo + take + lane; p < hi; p += 32) left[p] = 1;
+    }
+    if (take == 0) continue;
+    if (cur + (int64_t)take > B) {
+      if (lane == 0) atomicMin(status, (unsigned)(b + 1));
+      continue;
+    }
+    S *blk = blocks + (uint64_t)b * B;
+    for (int i = lane; i < cur; i += 32) E[i] = blk[i];
+    for (int j = lane; j < take; j += 32) I[j] = (S)(skey[lo + j] & P.fmask);
+    __syncwarp();
+    // stable merge of [existing, incoming]: existing first on ties
+    for (int i = lane; i < cur; i += 32) blk[i + lower_bound_s(I, take, (uint32_t)E[i])] = E[i];
+    for (int j = lane; j < take; j += 32) blk[j + upper_bound_s(E, cur, (uint32_t)I[j])] = I[j];
+    if (lane == 0) P.fill[b] = (uint32_t)(cur + take);
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// per-block delete (btcf_delete_blocklocal, ck:482-512): one warp per block
+// ---------------------------------------------------------------------------
+// Sequential semantics per block: each sorted item removes one stored copy
+// of its word if one is left.  For a word w requested q_w times and stored
+// c_w times, the first min(q_w, c_w) requests (in sorted order) hit and
+// min(q_w, c_w) copies go; the block is then re-packed.
+template <typename S>
+__global__ void __launch_bounds__(256) k_btcf_delete(BDev P, const uint64_t *__restrict__ skey,
+                                                     const uint32_t *__restrict__ sval,
+                                                     const uint32_t *__restrict__ seg_lo,
+                                                     const uint32_t *__restrict__ seg_hi, uint8_t *__restrict__ hit,
+                                                     uint8_t *__restrict__ removed) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int B = P.B;
+  S *E = reinterpret_cast<S *>(smem_raw) + (size_t)wib * B;
+  S *blocks = reinterpret_cast<S *>(P.blocks);
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t b = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib; b < (int64_t)P.nb; b += warps) {
+    int64_t lo = seg_lo[b], hi = seg_hi[b];
+    if (hi <= lo) continue;
+    int cur = (int)P.fill[b];
+    if (cur > B) cur = B;
+    S *blk = blocks + (uint64_t)b * B;
+    for (int i = lane; i < cur; i += 32) E[i] = blk[i];
+    __syncwarp();
+    const uint64_t bkey = (uint64_t)b << P.f;
+    // requests
+    for (int64_t k = lo + lane; k < hi; k += 32) {
+      uint32_t w = (uint32_t)(skey[k] & P.fmask);
+      int64_t r = k - lower_bound_g(skey, lo, k, bkey | w);
+      int c = upper_bound_s(E, cur, w) - lower_bound_s(E, cur, w);
+      uint8_t h = r < c ? 1 : 0;
+      hit[k] = h;
+      if (h) removed[sval[k]] = 1;
+    }
+    // stored copies: drop the first min(q_w, c_w) of each word, re-pack
+    int base = 0;
+    for (int i0 = 0; i0 < cur; i0 += 32) {
+      int i = i0 + lane;
+      bool keep = false;
+      S w = 0;
+      if (i < cur) {
+        w = E[i];
+        int j = i - lower_bound_s(E, cur, (uint32_t)w);
+        int64_t q = upper_bound_g(skey, lo, hi, bkey | (uint32_t)w) - lower_bound_g(skey, lo, hi, bkey | (uint32_t)w);
+        keep = (int64_t)j >= q;
+      }
+      unsigned bal = __ballot_sync(0xFFFFFFFFu, keep);
+      if (keep) blk[base + __popc(bal & ((1u << lane) - 1u))] = w;
+      base += __popc(bal);
+    }
+    __syncwarp();
+    for (int i = base + lane; i < cur; i += 32) blk[i] = (S)0;
+    if (lane == 0) P.fill[b] = (uint32_t)base;
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// query (btcf_query_batch, ck:552-599): 8 lanes per key, one 32-byte sector
+// per lane per round.  The block's sorted prefix is followed by EMPTY (0)
+// slots and words are >= 2, so "bisect hit in the prefix" == "some slot of
+// the block equals the word".
+// ---------------------------------------------------------------------------
+template <typename S>
+__device__ __forceinline__ bool sector_has(const uint32_t (&r)[8], uint32_t word) {
+  if constexpr (sizeof(S) == 2) {
+    uint32_t pat = word | (word << 16);
+    unsigned m = 0;
+#pragma unroll
+    for (int i = 0; i < 8; i++) m |= __vcmpeq2(r[i], pat);
+    return m != 0;
+  } else if constexpr (sizeof(S) == 1) {
+    uint32_t pat = word * 0x01010101u;
+    unsigned m = 0;
+#pragma unroll
+    for (int i = 0; i < 8; i++) m |= __vcmpeq4(r[i], pat);
+    return m != 0;
+  } else {
+    bool h = false;
+#pragma unroll
+    for (int i = 0; i < 8; i++) h |= r[i] == word;
+    return h;
+  }
+}
+
+template <typename S>
+__global__ void __launch_bounds__(256) k_btcf_query(BDev P, const uint64_t *__restrict__ keys, int64_t n,
+                                                    uint8_t *__restrict__ found) {
+  constexpr int G = 8;
+  const unsigned lane = threadIdx.x & 31, sub = lane % G, base = lane - sub;
+  const unsigned mask = 0xFFu << base;
+  const S *blocks = reinterpret_cast<const S *>(P.blocks);
+  const S *backing = reinterpret_cast<const S *>(P.backing);
+  const int64_t bytes = (int64_t)P.B * sizeof(S);
+  const bool vec = (bytes % 32) == 0;
+  const int sectors = (int)((bytes + 31) / 32);
+  const int64_t tiles = (int64_t)gridDim.x * (blockDim.x / G);
+  const int64_t first = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+  // warp-uniform trip count: every lane of the warp takes part in the ballots
+  const int64_t nround = (n + tiles - 1) / tiles;
+  for (int64_t it = 0; it < nround; it++) {
+    int64_t i = first + it * tiles;
+    bool valid = i < n;
+    uint64_t fp = valid ? key_fp(P, keys[i]) : 0;
+    uint32_t word = (uint32_t)remap_tag(fp, P.fmask);
+    bool hit = false;
+#pragma unroll 1
+    for (int which = 0; which < 2; which++) {
+      bool h = false;
+      if (valid && !hit) {
+        uint64_t b = fmod64(mix64(fp ^ (which ? kBlock2 : kBlock1)), P.nbm);
+        const S *blk = blocks + b * (uint64_t)P.B;
+        if (vec) {
+          for (int s = (int)sub; s < sectors; s += G) {
+            uint32_t r[8];
+            load_chunk<32, false>(reinterpret_cast<const char *>(blk) + 32 * s, r);
+            h |= sector_has<S>(r, word);
+          }
+        } else {
+          for (int j = (int)sub; j < P.B; j += G) h |= (uint32_t)blk[j] == word;
+        }
+      }
+      hit = hit || (__ballot_sync(0xFFFFFFFFu, h) & mask) != 0;
+    }
+    if (valid && !hit && P.bsize && sub == 0) {  // backing chain (ck:581-592)
+      uint64_t p = fmod64(mix64(fp ^ kBackStart), P.bsm);
+      uint64_t step = fmod64(mix64(fp ^ kBackStep) | 1, P.bsm);
+      for (int q = 0; q < P.probe_limit; q++) {
+        uint64_t w = backing[p];
+        if (w == 0) break;
+        if (w != 1 && (w & P.fmask) == word) {
+          hit = true;
+          break;
+        }
+        p += step;
+        p = p >= P.bsize ? p - P.bsize : p;
+      }
+    }
+    if (valid && sub == 0) found[i] = hit ? 1 : 0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// sequential two-choice routing (btcf_route, ck:408-444) by windowed
+// deterministic reservations.  Leftover k (in sorted order) may decide once
+// it holds the minimum pending index on both of its blocks: every earlier
+// leftover that could change those blocks' committed load has decided.
+// ---------------------------------------------------------------------------
+struct RouteScratch {
+  uint32_t *res;       // per block: min pending leftover index
+  uint32_t *carry[2];  // leftovers carried to the next round
+  unsigned *ctl;       // [0..1] carry counts
+  int64_t window;
+};
+
+__global__ void __launch_bounds__(256) k_btcf_route(const uint32_t *__restrict__ lb1, const uint32_t *__restrict__ lb2,
+                                                    int64_t m, uint32_t *__restrict__ load, uint32_t B,
+                                                    int32_t *__restrict__ dest, RouteScratch X) {
+  cg::grid_group grid = cg::this_grid();
+  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t F = 0, nc = 0;
+  int cur = 0;
+  for (;;) {
+    int64_t room = X.window - nc;
+    room = room < 0 ? 0 : room;
+    int64_t Fend = F + room < m ? F + room : m;
+    int64_t total = (Fend - F) + nc;
+    const uint32_t *cin = X.carry[cur];
+    uint32_t *cout = X.carry[cur ^ 1];
+    for (int64_t e = tid; e < total; e += nthreads) {
+      uint32_t k = e < nc ? __ldcg(cin + e) : (uint32_t)(F + e - nc);
+      uint32_t a = lb1[k], b = lb2[k];
+      atomicMin(&X.res[a], k);
+      if (b != a) atomicMin(&X.res[b], k);
+    }
+    grid.sync();
+    if (tid == 0) X.ctl[cur] = 0;
+    for (int64_t e0 = tid - (threadIdx.x & 31);; e0 += nthreads) {
+      if (e0 >= total) break;  // warp-uniform
+      int64_t e = e0 + (threadIdx.x & 31);
+      bool ok = e < total;
+      uint32_t k = 0, a = 0, b = 0;
+      bool hold = false;
+      if (ok) {
+        k = e < nc ? __ldcg(cin + e) : (uint32_t)(F + e - nc);
+        a = lb1[k];
+        b = lb2[k];
+        hold = __ldcg(&X.res[a]) == k && __ldcg(&X.res[b]) == k;
+      }
+      bool carry = ok && !hold;
+      unsigned bal = __ballot_sync(0xFFFFFFFFu, carry);
+      unsigned basepos = 0;
+      if ((threadIdx.x & 31) == 0 && bal) basepos = atomicAdd(&X.ctl[cur ^ 1], (unsigned)__popc(bal));
+      basepos = __shfl_sync(0xFFFFFFFFu, basepos, 0);
+      if (carry) cout[basepos + __popc(bal & ((1u << (threadIdx.x & 31)) - 1u))] = k;
+      if (hold) {
+        uint32_t l1 = __ldcg(&load[a]), l2 = __ldcg(&load[b]);
+        uint32_t pick = l1 <= l2 ? a : b;  // tie -> primary (ck:431)
+        uint32_t lp = pick == a ? l1 : l2;
+        int32_t d;
+        if (lp >= B) {
+          pick = pick == a ? b : a;
+          lp = pick == a ? l1 : l2;
+          d = lp >= B ? -1 : (int32_t)pick;
+        } else {
+          d = (int32_t)pick;
+        }
+        if (d >= 0) load[d] = lp + 1;
+        dest[k] = d;
+        X.res[a] = kNone;
+        X.res[b] = kNone;
+      }
+    }
+    grid.sync();
+    nc = (int64_t)__ldcg(&X.ctl[cur ^ 1]);
+    cur ^= 1;
+    F = Fend;
+    if (F >= m && nc == 0) break;
+  }
+}
+
+// leftover positions -> (b1, b2) of each leftover and the words
+__global__ void k_left_blocks(BDev P, const uint64_t *__restrict__ keys, const uint32_t *__restrict__ sval,
+                              const uint32_t *__restrict__ lpos, int64_t m, uint32_t *__restrict__ lb1,
+                              uint32_t *__restrict__ lb2) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < m; k += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t fp = key_fp(P, keys[sval[lpos[k]]]);
+    lb1[k] = (uint32_t)fmod64(mix64(fp ^ kBlock1), P.nbm);
+    lb2[k] = (uint32_t)fmod64(mix64(fp ^ kBlock2), P.nbm);
+  }
+}
+
+// second partition: key = ((dest + 1) << f) | word, value = original key index
+__global__ void k_dest_keys(BDev P, const uint64_t *__restrict__ skey, const uint32_t *__restrict__ sval,
+                            const uint32_t *__restrict__ lpos, const int32_t *__restrict__ dest, int64_t m,
+                            uint64_t *__restrict__ skey2, uint32_t *__restrict__ sval2) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < m; k += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t p = lpos[k];
+    skey2[k] = ((uint64_t)(dest[k] + 1) << P.f) | (skey[p] & P.fmask);
+    sval2[k] = sval[p];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// ordered backing inserts / deletes (backing_insert_batch ck:447-466,
+// backing_delete_batch ck:515-549) by reservations on probe positions.
+// Item e of `bidx` (priority e) targets, for inserts, its first free probe
+// position; for deletes, its first live match before the chain's first
+// EMPTY.  Candidates only shrink during a batch, so an item holding its
+// target's reservation takes exactly the slot the sequential loop gives it.
+// ---------------------------------------------------------------------------
+template <typename S, int OP>
+__global__ void __launch_bounds__(256) k_backing_ordered(BDev P, const uint64_t *__restrict__ keys,
+                                                         const uint32_t *__restrict__ bidx, int64_t m,
+                                                         uint32_t *__restrict__ bres, uint8_t *__restrict__ pend,
+                                                         uint8_t *__restrict__ out, unsigned *__restrict__ ctl) {
+  cg::grid_group grid = cg::this_grid();
+  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  S *bk = reinterpret_cast<S *>(P.backing);
+  unsigned round = 0;
+  for (;;) {
+    for (int64_t e = tid; e < m; e += nthreads) {
+      if (!__ldcg(&pend[e])) continue;
+      uint64_t fp = key_fp(P, keys[bidx[e]]);
+      uint64_t word = remap_tag(fp, P.fmask);
+      uint64_t p = fmod64(mix64(fp ^ kBackStart), P.bsm);
+      uint64_t step = fmod64(mix64(fp ^ kBackStep) | 1, P.bsm);
+      for (int q = 0; q < P.probe_limit; q++) {
+        uint64_t w = load_slot<S, true>(bk + p);
+        if (OP == 0) {
+          if (!live_word(w)) atomicMin(&bres[p], (uint32_t)e);
+        } else {
+          if (w == 0) break;
+          if (w != 1 && (w & P.fmask) == word) atomicMin(&bres[p], (uint32_t)e);
+        }
+        p += step;
+        p = p >= P.bsize ? p - P.bsize : p;
+      }
+    }
+    grid.sync();
+    bool left = false;
+    for (int64_t e = tid; e < m; e += nthreads) {
+      if (!__ldcg(&pend[e])) continue;
+      uint64_t fp = key_fp(P, keys[bidx[e]]);
+      uint64_t word = remap_tag(fp, P.fmask);
+      uint64_t p0 = fmod64(mix64(fp ^ kBackStart), P.bsm);
+      uint64_t step = fmod64(mix64(fp ^ kBackStep) | 1, P.bsm);
+      int64_t target = -1;
+      uint64_t p = p0;
+      for (int q = 0; q < P.probe_limit; q++) {
+        uint64_t w = load_slot<S, true>(bk + p);
+        if (OP == 0) {
+          if (!live_word(w)) { target = (int64_t)p; break; }
+        } else {
+          if (w == 0) break;
+          if (w != 1 && (w & P.fmask) == word) { target = (int64_t)p; break; }
+        }
+        p += step;
+        p = p >= P.bsize ? p - P.bsize : p;
+      }
+      if (target < 0) {  // nothing claimable now, nor later in this batch
+        out[e] = 0;
+        pend[e] = 0;
+        continue;
+      }
+      if (__ldcg(&bres[target]) != (uint32_t)e) {
+        left = true;
+        continue;
+      }
+      bk[target] = (S)(OP == 0 ? word : 1);
+      out[e] = 1;
+      pend[e] = 0;
+      p = p0;
+      for (int q = 0; q < P.probe_limit; q++) {
+        atomicCAS(&bres[p], (uint32_t)e, kNone);
+        p += step;
+        p = p >= P.bsize ? p - P.bsize : p;
+      }
+    }
+    bool any = __syncthreads_or(left ? 1 : 0) != 0;
+    if (threadIdx.x == 0) {
+      if (any) atomicAdd(&ctl[round & 1], 1u);
+      if (blockIdx.x == 0) ctl[(round + 1) & 1] = 0;
+    }
+    grid.sync();
+    unsigned cnt = __ldcg(&ctl[round & 1]);
+    round++;
+    if (cnt == 0) break;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// small helpers
+// ---------------------------------------------------------------------------
+__global__ void k_iota_u32(uint32_t *__restrict__ a, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    a[i] = (uint32_t)i;
+}
+
+__global__ void k_not_u8(const uint8_t *__restrict__ a, int64_t n, uint8_t *__restrict__ b) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    b[i] = a[i] ? 0 : 1;
+}
+
+__global__ void k_gather_keys(const uint64_t *__restrict__ keys, const uint32_t *__restrict__ idx, int64_t n,
+                              uint64_t *__restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = keys[idx[i]];
+}
+
+__global__ void k_scatter_ones(const uint32_t *__restrict__ idx, const uint8_t *__restrict__ flag, int64_t n,
+                               uint8_t *__restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (flag[i]) out[idx[i]] = 1;
+}
+
+// counters[0] += n - fails; counters[1] += n_back - fails (insert);
+// counters[2] += sum(removed) (delete)
+__global__ void k_count_insert(int64_t n, const int64_t *__restrict__ n_back, const int64_t *__restrict__ n_fail,
+                               int64_t *__restrict__ counters) {
+  counters[0] += n - *n_fail;
+  counters[1] += *n_back - *n_fail;
+}
+
+__global__ void k_count_removed(const uint8_t *__restrict__ removed, int64_t n, int64_t *__restrict__ counters) {
+  unsigned long long c = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    c += removed[i];
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd((unsigned long long *)&counters[2], c);
+}
+
+__global__ void k_flags_from_codes(const uint8_t *__restrict__ ok, int64_t n, uint8_t *__restrict__ failed,
+                                   int64_t *__restrict__ n_fail) {
+  unsigned long long c = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    failed[i] = ok[i] ? 0 : 1;
+    c += ok[i] ? 0 : 1;
+  }
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd((unsigned long long *)n_fail, c);
+}
+
+__global__ void k_seg0_len(const uint32_t *__restrict__ seg_lo, const uint32_t *__restrict__ seg_hi,
+                           int64_t *__restrict__ out) {
+  *out = (int64_t)seg_hi[0] - (int64_t)seg_lo[0];
+}
+
+// ---------------------------------------------------------------------------
+// host pipeline pieces
+// ---------------------------------------------------------------------------
+inline int bits_for(uint64_t v) {  // bits needed to represent v
+  int b = 0;
+  while (b < 64 && (v >> b)) b++;
+  return b;
+}
+
+cudaError_t sort_pairs(Scratch &S, const uint64_t *kin, uint64_t *kout, const uint32_t *vin, uint32_t *vout,
+                       int64_t n, int end_bit) {
+  size_t tb = 0;
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, tb, kin, kout, vin, vout, n, 0, end_bit, S.st);
+  if (e) return e;
+  void *tmp = S.get<char>(tb);
+  if (!tmp) return S.err;
+  return cub::DeviceRadixSort::SortPairs(tmp, tb, kin, kout, vin, vout, n, 0, end_bit, S.st);
+}
+
+template <typename It>
+cudaError_t select_flagged(Scratch &S, It in, const uint8_t *flags, uint32_t *out, int64_t *num, int64_t n) {
+  size_t tb = 0;
+  cudaError_t e = cub::DeviceSelect::Flagged(nullptr, tb, in, flags, out, num, n, S.st);
+  if (e) return e;
+  void *tmp = S.get<char>(tb);
+  if (!tmp) return S.err;
+  return cub::DeviceSelect::Flagged(tmp, tb, in, flags, out, num, n, S.st);
+}
+
+cudaError_t select_keys(Scratch &S, const uint64_t *in, const uint8_t *flags, uint64_t *out, int64_t *num,
+                        int64_t n) {
+  size_t tb = 0;
+  cudaError_t e = cub::DeviceSelect::Flagged(nullptr, tb, in, flags, out, num, n, S.st);
+  if (e) return e;
+  void *tmp = S.get<char>(tb);
+  if (!tmp) return S.err;
+  return cub::DeviceSelect::Flagged(tmp, tb, in, flags, out, num, n, S.st);
+}
+
+int64_t read_i64(const int64_t *d, cudaStream_t st, cudaError_t *err) {
+  int64_t h = 0;
+  *err = cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, st);
+  if (*err == cudaSuccess) *err = cudaStreamSynchronize(st);
+  return h;
+}
+
+#define FK_S(expr)                               \
+  do {                                           \
+    cudaError_t e_ = (expr);                     \
+    if (e_ != cudaSuccess) return -(int)e_;      \
+  } while (0)
+#define FK_P(ptr)                                \
+  do {                                           \
+    if (!(ptr)) return -(int)S.err;              \
+  } while (0)
+
+template <typename S_t>
+int per_block_launch_cfg(int B, int per_warp_slots, int *threads, size_t *smem) {
+  size_t per_warp = (size_t)per_warp_slots * B * sizeof(S_t);
+  int warps = 8;
+  while (warps > 1 && per_warp * warps > 48 * 1024) warps >>= 1;
+  *threads = 32 * warps;
+  *smem = per_warp * warps;
+  return *smem <= 200 * 1024 ? 0 : FK_E_ARG;
+}
+
+template <typename S_t>
+int merge_segments(const BDev &P, const uint64_t *skey, const uint32_t *seg_lo, const uint32_t *seg_hi,
+                   int seg_off, int phase1, uint8_t *left, unsigned *status, cudaStream_t st) {
+  int threads;
+  size_t smem;
+  if (per_block_launch_cfg<S_t>(P.B, 2, &threads, &smem)) return FK_E_ARG;
+  auto kern = k_btcf_merge<S_t>;
+  if (smem > 48 * 1024) FK_S(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int64_t ctas = ((int64_t)P.nb + threads / 32 - 1) / (threads / 32);
+  int64_t cap = (int64_t)num_sms() * 32;
+  kern<<<(int)(ctas < cap ? ctas : cap), threads, smem, st>>>(P, skey, seg_lo, seg_hi, seg_off, phase1, left,
+                                                               status);
+  FK_CHECK_LAUNCH();
+  return 0;
+}
+
+int coop_grid(const void *kern, int threads) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, 0) != cudaSuccess || per_sm < 1)
+    return 0;
+  return per_sm * num_sms();
+}
+
+template <typename S_t, int OP>
+int backing_ordered(const BDev &P, const uint64_t *keys, const uint32_t *bidx, int64_t m, uint8_t *ok, Scratch &S) {
+  cudaStream_t st = S.st;
+  uint32_t *bres = S.get<uint32_t>(P.bsize);
+  FK_P(bres);
+  uint8_t *pend = S.get<uint8_t>(m);
+  FK_P(pend);
+  unsigned *ctl = S.get<unsigned>(4);
+  FK_P(ctl);
+  FK_S(cudaMemsetAsync(bres, 0xFF, P.bsize * 4, st));
+  FK_S(cudaMemsetAsync(pend, 1, m, st));
+  FK_S(cudaMemsetAsync(ctl, 0, 16, st));
+  auto kern = k_backing_ordered<S_t, OP>;
+  int grid = coop_grid((const void *)kern, 256);
+  if (!grid) return FK_E_ARG;
+  int64_t need = (m + 255) / 256;
+  if (need < grid) grid = (int)(need < 1 ? 1 : need);
+  void *args[] = {(void *)&P, (void *)&keys, (void *)&bidx, (void *)&m, (void *)&bres, (void *)&pend, (void *)&ok,
+                  (void *)&ctl};
+  FK_S(cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(256), args, 0, st));
+  return 0;
+}
+
+// ---- insert_batch (tcf_bulk.py:179-257) ------------------------------------
+template <typename S_t>
+int btcf_insert(const BDev &P, const uint64_t *keys, int64_t n, uint64_t *failed_keys, int64_t *n_failed,
+                int64_t *counters, unsigned *status, cudaStream_t st) {
+  Scratch S(st);
+  const int end1 = P.f + bits_for(P.nb - 1);
+  uint64_t *k0 = S.get<uint64_t>(n), *skey = S.get<uint64_t>(n);
+  uint32_t *v0 = S.get<uint32_t>(n), *sval = S.get<uint32_t>(n);
+  uint32_t *seg_lo = S.get<uint32_t>(P.nb + 1), *seg_hi = S.get<uint32_t>(P.nb + 1);
+  uint8_t *left = S.get<uint8_t>(n);
+  int64_t *cnt = S.get<int64_t>(4);  // [0] leftovers, [1] backing items, [2] fails
+  FK_P(k0); FK_P(skey); FK_P(v0); FK_P(sval); FK_P(seg_lo); FK_P(seg_hi); FK_P(left); FK_P(cnt);
+  FK_S(cudaMemsetAsync(cnt, 0, 32, st));
+  FK_S(cudaMemsetAsync(n_failed, 0, 8, st));
+  // partition (tcf_bulk.py:133-143): stable sort by (b1, word)
+  k_part_keys<<<grid_for(n), 256, 0, st>>>(P, keys, nullptr, n, 0, k0, v0);
+  FK_CHECK_LAUNCH();
+  FK_S(sort_pairs(S, k0, skey, v0, sval, n, end1));
+  FK_S(cudaMemsetAsync(seg_lo, 0, (P.nb + 1) * 4, st));
+  FK_S(cudaMemsetAsync(seg_hi, 0, (P.nb + 1) * 4, st));
+  k_seg_bounds<<<grid_for(n), 256, 0, st>>>(skey, n, P.f, seg_lo, seg_hi);
+  FK_CHECK_LAUNCH();
+  // phase 1: shortcut merge up to the cut line, flag leftovers
+  FK_S(cudaMemsetAsync(left, 0, n, st));
+  int rc = merge_segments<S_t>(P, skey, seg_lo, seg_hi, 0, 1, left, status, st);
+  if (rc) return rc;
+  // leftovers, in sorted order (tcf_bulk.py:211-213)
+  uint32_t *lpos = S.get<uint32_t>(n);
+  FK_P(lpos);
+  FK_S(select_flagged(S, cub::CountingInputIterator<uint32_t>(0), left, lpos, cnt, n));
+  cudaError_t err;
+  int64_t m = read_i64(cnt, st, &err);
+  FK_S(err);
+  if (m > 0) {
+    uint32_t *lb1 = S.get<uint32_t>(m), *lb2 = S.get<uint32_t>(m), *load = S.get<uint32_t>(P.nb);
+    int32_t *dest = S.get<int32_t>(m);
+    RouteScratch X;
+    X.res = S.get<uint32_t>(P.nb);
+    int64_t window = 1 << 18;
+    if (const char *e = getenv("FK_ROUTE_WINDOW")) window = atoll(e) > 0 ? atoll(e) : window;
+    X.window = window < m ? window : m;
+    X.carry[0] = S.get<uint32_t>(X.window);
+    X.carry[1] = S.get<uint32_t>(X.window);
+    X.ctl = S.get<unsigned>(4);
+    FK_P(lb1); FK_P(lb2); FK_P(load); FK_P(dest); FK_P(X.res); FK_P(X.carry[0]); FK_P(X.carry[1]); FK_P(X.ctl);
+    k_left_blocks<<<grid_for(m), 256, 0, st>>>(P, keys, sval, lpos, m, lb1, lb2);
+    FK_CHECK_LAUNCH();
+    FK_S(cudaMemcpyAsync(load, P.fill, P.nb * 4, cudaMemcpyDeviceToDevice, st));
+    FK_S(cudaMemsetAsync(X.res, 0xFF, P.nb * 4, st));
+    FK_S(cudaMemsetAsync(X.ctl, 0, 16, st));
+    int grid = coop_grid((const void *)k_btcf_route, 256);
+    if (!grid) return FK_E_ARG;
+    int64_t need = (X.window + 255) / 256;
+    if (need < grid) grid = (int)(need < 1 ? 1 : need);
+    uint32_t Bu = (uint32_t)P.B;
+    void *args[] = {(void *)&lb1, (void *)&lb2, (void *)&m, (void *)&load, (void *)&Bu, (void *)&dest, (void *)&X};
+    FK_S(cudaLaunchCooperativeKernel((const void *)k_btcf_route, dim3(grid), dim3(256), args, 0, st));
+    // group by destination; segment 0 = backing (tcf_bulk.py:225-234)
+    uint64_t *k2 = S.get<uint64_t>(m), *skey2 = S.get<uint64_t>(m);
+    uint32_t *v2 = S.get<uint32_t>(m), *sval2 = S.get<uint32_t>(m);
+    FK_P(k2); FK_P(skey2); FK_P(v2); FK_P(sval2);
+    k_dest_keys<<<grid_for(m), 256, 0, st>>>(P, skey, sval, lpos, dest, m, k2, v2);
+    FK_CHECK_LAUNCH();
+    FK_S(sort_pairs(S, k2, skey2, v2, sval2, m, P.f + bits_for(P.nb)));
+    FK_S(cudaMemsetAsync(seg_lo, 0, (P.nb + 1) * 4, st));
+    FK_S(cudaMemsetAsync(seg_hi, 0, (P.nb + 1) * 4, st));
+    k_seg_bounds<<<grid_for(m), 256, 0, st>>>(skey2, m, P.f, seg_lo, seg_hi);
+    FK_CHECK_LAUNCH();
+    rc = merge_segments<S_t>(P, skey2, seg_lo, seg_hi, 1, 0, nullptr, status, st);
+    if (rc) return rc;
+    // backing overflow, in (word, routing) order (tcf_bulk.py:247-255)
+    k_seg0_len<<<1, 1, 0, st>>>(seg_lo, seg_hi, cnt + 1);
+    FK_CHECK_LAUNCH();
+    int64_t nback = read_i64(cnt + 1, st, &err);
+    FK_S(err);
+    if (nback > 0) {
+      uint8_t *ok = S.get<uint8_t>(nback), *failf = S.get<uint8_t>(nback);
+      uint64_t *bkeys = S.get<uint64_t>(nback);
+      FK_P(ok); FK_P(failf); FK_P(bkeys);
+      if (P.bsize) {
+        rc = backing_ordered<S_t, 0>(P, keys, sval2, nback, ok, S);
+        if (rc) return rc;
+      } else {
+        FK_S(cudaMemsetAsync(ok, 0, nback, st));
+      }
+      k_flags_from_codes<<<grid_for(nback), 256, 0, st>>>(ok, nback, failf, cnt + 2);
+      FK_CHECK_LAUNCH();
+      k_gather_keys<<<grid_for(nback), 256, 0, st>>>(keys, sval2, nback, bkeys);
+      FK_CHECK_LAUNCH();
+      FK_S(select_keys(S, bkeys, failf, failed_keys, n_failed, nback));
+    }
+  }
+  k_count_insert<<<1, 1, 0, st>>>(n, cnt + 1, cnt + 2, counters);
+  FK_CHECK_LAUNCH();
+  return 0;
+}
+
+// ---- delete_batch (tcf_bulk.py:283-325) -------------------------------------
+template <typename S_t>
+int btcf_delete(const BDev &P, const uint64_t *keys, int64_t n, uint8_t *removed, int64_t *counters,
+                cudaStream_t st) {
+  Scratch S(st);
+  const int end1 = P.f + bits_for(P.nb - 1);
+  uint32_t *pend = S.get<uint32_t>(n), *pend2 = S.get<uint32_t>(n);
+  uint64_t *k0 = S.get<uint64_t>(n), *skey = S.get<uint64_t>(n);
+  uint32_t *sval = S.get<uint32_t>(n);
+  uint32_t *seg_lo = S.get<uint32_t>(P.nb), *seg_hi = S.get<uint32_t>(P.nb);
+  uint8_t *hit = S.get<uint8_t>(n), *miss = S.get<uint8_t>(n);
+  int64_t *cnt = S.get<int64_t>(2);
+  FK_P(pend); FK_P(pend2); FK_P(k0); FK_P(skey); FK_P(sval); FK_P(seg_lo); FK_P(seg_hi); FK_P(hit); FK_P(miss);
+  FK_P(cnt);
+  FK_S(cudaMemsetAsync(removed, 0, n, st));
+  k_iota_u32<<<grid_for(n), 256, 0, st>>>(pend, n);
+  FK_CHECK_LAUNCH();
+  int threads;
+  size_t smem;
+  if (per_block_launch_cfg<S_t>(P.B, 1, &threads, &smem)) return FK_E_ARG;
+  auto dkern = k_btcf_delete<S_t>;
+  if (smem > 48 * 1024) FK_S(cudaFuncSetAttribute(dkern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int64_t ctas = ((int64_t)P.nb + threads / 32 - 1) / (threads / 32);
+  int64_t cap = (int64_t)num_sms() * 32;
+  int dgrid = (int)(ctas < cap ? ctas : cap);
+  int64_t m = n;
+  for (int which = 0; which < 2 && m > 0; which++) {
+    k_part_keys<<<grid_for(m), 256, 0, st>>>(P, keys, pend, m, which, k0, pend2);
+    FK_CHECK_LAUNCH();
+    FK_S(sort_pairs(S, k0, skey, pend2, sval, m, end1));
+    FK_S(cudaMemsetAsync(seg_lo, 0, P.nb * 4, st));
+    FK_S(cudaMemsetAsync(seg_hi, 0, P.nb * 4, st));
+    k_seg_bounds<<<grid_for(m), 256, 0, st>>>(skey, m, P.f, seg_lo, seg_hi);
+    FK_CHECK_LAUNCH();
+    dkern<<<dgrid, threads, smem, st>>>(P, skey, sval, seg_lo, seg_hi, hit, removed);
+    FK_CHECK_LAUNCH();
+    // misses, in this pass's sorted order (tcf_bulk.py:318)
+    k_not_u8<<<grid_for(m), 256, 0, st>>>(hit, m, miss);
+    FK_CHECK_LAUNCH();
+    FK_S(select_flagged(S, sval, miss, pend, cnt, m));
+    cudaError_t err;
+    m = read_i64(cnt, st, &err);
+    FK_S(err);
+  }
+  if (m > 0 && P.bsize) {
+    uint8_t *ok = S.get<uint8_t>(m);
+    FK_P(ok);
+    int rc = backing_ordered<S_t, 1>(P, keys, pend, m, ok, S);
+    if (rc) return rc;
+    k_scatter_ones<<<grid_for(m), 256, 0, st>>>(pend, ok, m, removed);
+    FK_CHECK_LAUNCH();
+  }
+  k_count_removed<<<grid_for(n), 256, 0, st>>>(removed, n, counters);
+  FK_CHECK_LAUNCH();
+  return 0;
+}
+
+template <typename S_t>
+int btcf_query(const BDev &P, const uint64_t *keys, int64_t n, uint8_t *found, cudaStream_t st) {
+  int64_t tiles_per_cta = 256 / 8;
+  int64_t need = (n + tiles_per_cta - 1) / tiles_per_cta;
+  int64_t cap = (int64_t)num_sms() * 8;
+  k_btcf_query<S_t><<<(int)(need < cap ? (need < 1 ? 1 : need) : cap), 256, 0, st>>>(P, keys, n, found);
+  FK_CHECK_LAUNCH();
+  return 0;
+}
+
+// ---- partition (BulkTcf.partition, tcf_bulk.py:123-143) ---------------------
+int btcf_partition(const BDev &P, const uint64_t *keys, int64_t n, uint64_t *sorted_keys, uint32_t *order,
+                   cudaStream_t st) {
+  Scratch S(st);
+  uint64_t *k0 = S.get<uint64_t>(n);
+  uint32_t *v0 = S.get<uint32_t>(n);
+  FK_P(k0); FK_P(v0);
+  k_part_keys<<<grid_for(n), 256, 0, st>>>(P, keys, nullptr, n, 0, k0, v0);
+  FK_CHECK_LAUNCH();
+  FK_S(sort_pairs(S, k0, sorted_keys, v0, order, n, P.f + bits_for(P.nb - 1)));
+  return 0;
+}
+
+bool geom_ok(const fk_btcf_geom *g) {
+  if (!g || g->num_blocks < 1 || g->num_blocks > 0x7FFFFFF0LL || g->backing_slots < 0) return false;
+  if (g->block_slots < 2 || g->block_slots > 8192) return false;
+  if (g->slot_bytes != 1 && g->slot_bytes != 2 && g->slot_bytes != 4) return false;
+  if (g->tag_bits <= 2 || g->tag_bits > 8 * g->slot_bytes) return false;
+  if (g->tag_bits + bits_for((uint64_t)g->num_blocks) > 64) return false;
+  return true;
+}
+
+BDev make_dev(const fk_btcf_geom *g, void *blocks, uint32_t *fill, void *backing, int keys_are_fps) {
+  BDev P;
+  P.blocks = blocks;
+  P.fill = fill;
+  P.backing = backing;
+  P.nb = (uint64_t)g->num_blocks;
+  P.nbm = make_fastmod(P.nb);
+  P.bsize = (uint64_t)g->backing_slots;
+  P.bsm = make_fastmod(P.bsize ? P.bsize : 1);
+  P.B = g->block_slots;
+  P.f = g->tag_bits;
+  P.cut = g->cut_slots;
+  P.probe_limit = g->probe_limit;
+  P.fmask = (1ULL << g->tag_bits) - 1;
+  P.seed = g->seed;
+  P.keys_are_fps = keys_are_fps;
+  return P;
+}
+
+}  // namespace
+
+}  // namespace fk
+
+using namespace fk;
+
+extern "C" {
+
+int fk_btcf_insert(const fk_btcf_geom *g, void *blocks, uint32_t *fill, void *backing, const uint64_t *keys,
+                   int keys_are_fps, int64_t n, uint64_t *failed_keys, int64_t *n_failed, int64_t *counters,
+                   uint32_t *status, void *stream) {
+  if (!geom_ok(g) || n < 0 || n > 0xFFFFFFF0LL || !counters || !status || !n_failed) return FK_E_ARG;
+  if (n == 0) return 0;
+  BDev P = make_dev(g, blocks, fill, backing, keys_are_fps);
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (g->slot_bytes) {
+    case 1: return btcf_insert<uint8_t>(P, keys, n, failed_keys, n_failed, counters, status, st);
+    case 4: return btcf_insert<uint32_t>(P, keys, n, failed_keys, n_failed, counters, status, st);
+    default: return btcf_insert<uint16_t>(P, keys, n, failed_keys, n_failed, counters, status, st);
+  }
+}
+
+int fk_btcf_query(const fk_btcf_geom *g, const void *blocks, const uint32_t *fill, const void *backing,
+                  const uint64_t *keys, int keys_are_fps, int64_t n, uint8_t *found, void *stream) {
+  if (!geom_ok(g) || n < 0) return FK_E_ARG;
+  if (n == 0) return 0;
+  BDev P = make_dev(g, const_cast<void *>(blocks), const_cast<uint32_t *>(fill), const_cast<void *>(backing),
+                    keys_are_fps);
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (g->slot_bytes) {
+    case 1: return btcf_query<uint8_t>(P, keys, n, found, st);
+    case 4: return btcf_query<uint32_t>(P, keys, n, found, st);
+    default: return btcf_query<uint16_t>(P, keys, n, found, st);
+  }
+}
+
+int fk_btcf_delete(const fk_btcf_geom *g, void *blocks, uint32_t *fill, void *backing, const uint64_t *keys,
+                   int keys_are_fps, int64_t n, uint8_t *removed, int64_t *counters, void *stream) {
+  if (!geom_ok(g) || n < 0 || n > 0xFFFFFFF0LL || !counters) return FK_E_ARG;
+  if (n == 0) return 0;
+  BDev P = make_dev(g, blocks, fill, backing, keys_are_fps);
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (g->slot_bytes) {
+    case 1: return btcf_delete<uint8_t>(P, keys, n, removed, counters, st);
+    case 4: return btcf_delete<uint32_t>(P, keys, n, removed, counters, st);
+    default: return btcf_delete<uint16_t>(P, keys, n, removed, counters, st);
+  }
+}
+
+int fk_btcf_partition(const fk_btcf_geom *g, const uint64_t *keys, int keys_are_fps, int64_t n,
+                      uint64_t *sorted_keys, uint32_t *order, void *stream) {
+  if (!geom_ok(g) || n < 0 || n > 0xFFFFFFF0LL) return FK_E_ARG;
+  if (n == 0) return 0;
+  BDev P = make_dev(g, nullptr, nullptr, nullptr, keys_are_fps);
+  return btcf_partition(P, keys, n, sorted_keys, order, (cudaStream_t)stream);
+}
+
+int fk_btcf_merge_lists(const fk_btcf_geom *g, void *blocks, uint32_t *fill, const uint64_t *sorted_keys,
+                        const uint32_t *seg_lo, const uint32_t *seg_hi, uint32_t *status, void *stream) {
+  if (!geom_ok(g) || !status) return FK_E_ARG;
+  BDev P = make_dev(g, blocks, fill, nullptr, 1);
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (g->slot_bytes) {
+    case 1: return merge_segments<uint8_t>(P, sorted_keys, seg_lo, seg_hi, 0, 0, nullptr, status, st);
+    case 4: return merge_segments<uint32_t>(P, sorted_keys, seg_lo, seg_hi, 0, 0, nullptr, status, st);
+    default: return merge_segments<uint16_t>(P, sorted_keys, seg_lo, seg_hi, 0, 0, nullptr, status, st);
+  }
+}
+
+}  // extern "C"
