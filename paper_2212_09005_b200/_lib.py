@@ -29,6 +29,12 @@ class TcfGeom(ctypes.Structure):
                 ("probe_limit", c_i32), ("group_width", c_i32), ("seed", c_u64)]
 
 
+class BtcfGeom(ctypes.Structure):
+    _fields_ = [("num_blocks", c_i64), ("backing_slots", c_i64), ("block_slots", c_i32),
+                ("tag_bits", c_i32), ("slot_bytes", c_i32), ("cut_slots", c_i32),
+                ("probe_limit", c_i32), ("reserved", c_i32), ("seed", c_u64)]
+
+
 class GqfGeom(ctypes.Structure):
     _fields_ = [("q", c_i32), ("r", c_i32), ("phys", c_i64), ("num_regions", c_i64),
                 ("quotient_regions", c_i64), ("max_occupied", c_i64), ("seed", c_u64)]
@@ -60,6 +66,13 @@ _SIGS = {
     "fk_tcf_query": (c_i32, [ctypes.POINTER(TcfGeom), c_vp, c_vp, c_vp, c_i32, c_i64, c_vp, c_vp, c_vp]),
     "fk_tcf_delete": (c_i32, [ctypes.POINTER(TcfGeom), c_vp, c_vp, c_vp, c_i32, c_i64, c_vp, c_vp,
                               c_i32, c_vp, c_sz, c_vp]),
+    "fk_btcf_insert": (c_i32, [ctypes.POINTER(BtcfGeom), c_vp, c_vp, c_vp, c_vp, c_i32, c_i64, c_vp, c_vp,
+                               c_vp, c_vp, c_vp]),
+    "fk_btcf_query": (c_i32, [ctypes.POINTER(BtcfGeom), c_vp, c_vp, c_vp, c_vp, c_i32, c_i64, c_vp, c_vp]),
+    "fk_btcf_delete": (c_i32, [ctypes.POINTER(BtcfGeom), c_vp, c_vp, c_vp, c_vp, c_i32, c_i64, c_vp, c_vp,
+                               c_vp]),
+    "fk_btcf_partition": (c_i32, [ctypes.POINTER(BtcfGeom), c_vp, c_i32, c_i64, c_vp, c_vp, c_vp]),
+    "fk_btcf_merge_lists": (c_i32, [ctypes.POINTER(BtcfGeom), c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "fk_gqf_count": (c_i32, [ctypes.POINTER(GqfGeom), ctypes.POINTER(GqfTables), c_vp, c_i32, c_i64, c_vp, c_vp]),
     "fk_gqf_find_run": (c_i32, [ctypes.POINTER(GqfGeom), ctypes.POINTER(GqfTables), c_vp, c_i64, c_vp, c_vp]),
     "fk_gqf_rebuild_index": (c_i32, [ctypes.POINTER(GqfGeom), ctypes.POINTER(GqfTables), c_vp]),
