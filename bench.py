@@ -25,6 +25,7 @@ on the host's cores for the same metric.
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import subprocess
@@ -51,6 +52,21 @@ BYTES_PER_OP = {
     "query_neg": 8 + 64 + 1,                        # 73
     "delete": 8 + 32 * (1 + 0.1437) + 32 + 1,       # 77.6
 }
+
+
+# Random 32-B sectors per op (table blocks; the 5 MiB backing table is
+# L2-resident): b2 read on 26.0% of inserts / 14.37% of positive queries and
+# deletes, both blocks on every negative query.
+SECTORS_PER_OP = {"insert": 1.260, "query_pos": 1.1437, "query_neg": 2.0, "delete": 1.1437}
+
+KERNEL_OF = {
+    ("ordered", "insert"): "k_tcf_ordered<u16,G=1,B=16,KB=4,OP=insert>",
+    ("ordered", "delete"): "k_tcf_ordered<u16,G=1,B=16,KB=4,OP=delete>",
+    ("concurrent", "insert"): "k_tcf_insert_cas<u16,G=1,B=16>",
+    ("concurrent", "delete"): "k_tcf_delete_cas<u16,G=1,B=16>",
+}
+for _m in ("ordered", "concurrent"):
+    KERNEL_OF[(_m, "query_pos")] = KERNEL_OF[(_m, "query_neg")] = "k_tcf_query<u16,G=1,B=16>"
 
 
 def peaks():
@@ -133,6 +149,99 @@ def device_keys(torch, seed, tag, n, device):
     return out
 
 
+def random_sector_ceiling(torch, filt, stream, reps=3):
+    """Random 32-byte sector loads over the filter's own block table, same
+    hash stream and load width as the kernels (fk_sector_gather), timed with
+    CUDA events on the launching stream: the achievable random-access rate
+    the per-op `frac_of_random_sector_ceiling` figures are against."""
+    from paper_2212_09005_b200 import _lib
+    lib = _lib.load()
+    tab = filt._t.dev["blocks"]
+    sink = torch.zeros(32, dtype=torch.int32, device=tab.device)
+    n = 1 << 28
+    sp = ctypes.c_void_p(stream.cuda_stream)
+    _lib.check(lib.fk_sector_gather(_lib.dptr(tab), tab.numel(), n, 1, _lib.dptr(sink), sp), "gather")
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for r in range(reps):
+        _lib.check(lib.fk_sector_gather(_lib.dptr(tab), tab.numel(), n, 2 + r, _lib.dptr(sink), sp), "gather")
+    b.record(stream)
+    b.synchronize()
+    ms = a.elapsed_time(b) / reps
+    sps = n / (ms / 1e3)
+    return {"sectors_per_s": sps, "useful_gbs": 32 * sps / 1e9, "table_bytes": tab.numel(),
+            "how": "fk_sector_gather: %d random 32-B sector loads (ld.global.v8) over the %d MiB block table, "
+                   "mean of %d, CUDA events" % (n, tab.numel() >> 20, reps)}
+
+
+def ncu_traffic(mode, op, n):
+    """DRAM bytes (read + write) per launch of the dominant kernel from the
+    committed ncu --set full summary (profiles/)."""
+    import glob
+    want = {"insert": "OP=insert", "delete": "OP=delete"}.get(op)
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*tcf_point_%s_full.json" % mode)), reverse=True):
+        d = json.load(open(path))
+        ks = d["kernels"]
+        idx = {"insert": 0, "query_pos": 1, "query_neg": 2, "delete": 3}.get(op)
+        if idx is None or idx >= len(ks):
+            continue
+        k = ks[idx]
+        rd = k["dram__bytes_read.sum"]["value"] * _unit(k["dram__bytes_read.sum"]["unit"])
+        wr = k["dram__bytes_write.sum"]["value"] * _unit(k["dram__bytes_write.sum"]["unit"])
+        return {"bytes_per_launch": rd + wr, "bytes_per_op": (rd + wr) / n,
+                "source": os.path.relpath(path, ROOT) + " :: " + k["kernel"][:60]}
+    return None
+
+
+def _unit(u):
+    return {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}.get(u, 1)
+
+
+def count_launches(torch, step):
+    """Kernels launched by one untimed step, counted with the CUDA profiler
+    (activity trace) -- ours are the fk:: kernels and the CUB algorithms
+    compiled into libfkb200.so."""
+    try:
+        from torch.profiler import ProfilerActivity, profile
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            step()
+            torch.cuda.synchronize()
+        names = [e.name for e in prof.events() if e.device_type.name == "CUDA"]
+        return sum(1 for nm in names if "fk::" in nm or "cub::" in nm or nm.startswith("k_"))
+    except Exception:  # profiler unavailable: report unknown rather than guess
+        return None
+
+
+def concurrent_mode(torch, nb, args, keys, negs, stream, steps=2):
+    """The paper's free-threaded CAS mode on the same workload (secondary
+    numbers; not bit-identical to the sequential reference)."""
+    from paper_2212_09005_b200 import Tcf
+    f = Tcf(num_blocks=nb, group_width=args.group_width, mode="concurrent")
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+    res = {}
+    n = keys.numel()
+    for s in range(steps + 1):
+        f._reset()
+        evs[0].record(stream)
+        f.insert_many(keys)
+        evs[1].record(stream)
+        f.query_many(keys)
+        evs[2].record(stream)
+        f.query_many(negs)
+        evs[3].record(stream)
+        f.delete_many(keys)
+        evs[4].record(stream)
+        torch.cuda.synchronize()
+        if s:
+            for i, op in enumerate(("insert", "query_pos", "query_neg", "delete")):
+                res.setdefault(op, []).append(evs[i].elapsed_time(evs[i + 1]))
+    out = {op: {"ops_per_s": n / (np.mean(v) / 1e3), "ms": float(np.mean(v))} for op, v in res.items()}
+    out["step_ops_per_s"] = 4 * n / (sum(np.mean(v) for v in res.values()) / 1e3)
+    del f
+    torch.cuda.empty_cache()
+    return out
+
+
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
@@ -155,7 +264,7 @@ def run_ours(args, rank, world, local_rank):
 
     if world > 1:
         from paper_2212_09005_b200.sharding import ShardedTcf
-        filt = ShardedTcf(num_blocks=nb, group_width=args.group_width, mode=args.mode)
+        filt = ShardedTcf(num_blocks=nb * world, group_width=args.group_width, mode=args.mode)
     else:
         filt = Tcf(num_blocks=nb, group_width=args.group_width, mode=args.mode)
 
@@ -248,18 +357,22 @@ def run_ours(args, rank, world, local_rank):
 
     peak, peak_kind = peaks()
     dom = max(per_op_ms, key=per_op_ms.get)
+    local = filt._local if world > 1 else filt
+    ceiling = random_sector_ceiling(torch, local, stream)
     per_op = {}
     for op in ops:
-        gbs = BYTES_PER_OP[op] * n / (per_op_ms[op] / 1e3) / 1e9
-        per_op[op] = {"ops_per_s": n / (per_op_ms[op] / 1e3), "ms": per_op_ms[op],
-                      "achieved_gbs": gbs, "frac_of_%s_hbm" % peak_kind: gbs / peak}
+        rate = n / (per_op_ms[op] / 1e3)
+        gbs = BYTES_PER_OP[op] * rate / 1e9
+        per_op[op] = {"ops_per_s": rate, "ms": per_op_ms[op], "achieved_gbs": gbs,
+                      "frac_of_%s_hbm" % peak_kind: gbs / peak,
+                      "random_sectors_per_op": SECTORS_PER_OP[op],
+                      "frac_of_random_sector_ceiling": SECTORS_PER_OP[op] * rate / ceiling["sectors_per_s"]}
     achieved = BYTES_PER_OP[dom] * n / (per_op_ms[dom] / 1e3) / 1e9
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(prof):
-        tr = json.load(open(prof)).get(args.mode, {}).get(dom)
-        traffic = tr
-    launches_per_step = 4 if world == 1 else None
+    traffic = ncu_traffic(args.mode, dom, n)
+    launches = count_launches(torch, step) if not args.no_launch_count else None
+    conc = None
+    if args.mode == "ordered" and not args.no_concurrent and world == 1:
+        conc = concurrent_mode(torch, nb, args, keys, negs, stream)
     result = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
@@ -270,16 +383,23 @@ def run_ours(args, rank, world, local_rank):
                    "keys_per_op_per_gpu": n, "mode": args.mode, "group_width": args.group_width,
                    "l2": "inputs (%.1f GB keys) and table (%d MiB) exceed the 126 MB L2; no flush"
                          % (8 * n / 1e9, (1 << log_slots) * 2 >> 20),
-                   "parallelism": "hash-prefix shards, NCCL all-to-all" if world > 1 else "single GPU"},
+                   "parallelism": ("hash-prefix shards x%d, NCCL all-to-all" % world) if world > 1
+                   else "single GPU"},
         "per_op": per_op,
-        "roofline": {"bound": "hbm", "kernel": "tcf_" + dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "bytes_per_op": BYTES_PER_OP[dom]},
+        "roofline": {"bound": "hbm", "kernel": KERNEL_OF[(args.mode, dom)], "op": dom, "achieved": achieved,
+                     "peak": peak, "unit": "GB/s", "frac": achieved / peak, "peak_kind": peak_kind,
+                     "bytes_per_op": BYTES_PER_OP[dom], "traffic": traffic["bytes_per_launch"] if traffic else None,
+                     "traffic_bytes_per_op": traffic["bytes_per_op"] if traffic else None,
+                     "traffic_source": traffic["source"] if traffic else None},
+        "random_access_roofline": ceiling,
         "e2e": e2e,
-        "gpu_launches": (launches_per_step * args.steps) if launches_per_step else None,
+        "gpu_launches": launches * args.steps if launches is not None else None,
+        "gpu_launches_per_step": launches,
         "clocks": clk.summary(),
         "checks": {"full_codes": n_full, "false_negatives": n_fn, "neg_fpr": fpr, "removed": n_rem},
     }
+    if conc:
+        result["concurrent_mode"] = conc
     if rank == 0 and world == 1 and not args.no_cpu:
         result["cpu_baseline"] = cpu_baseline(args.cpu_budget_s)
     return result if rank == 0 else None
@@ -377,6 +497,8 @@ def main():
     ap.add_argument("--mode", choices=["ordered", "concurrent"], default="ordered")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-concurrent", action="store_true")
+    ap.add_argument("--no-launch-count", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=15.0)
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)

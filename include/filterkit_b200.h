@@ -76,6 +76,12 @@ int fk_device_l2_fetch_bytes(void);
 int fk_hash_streams(const uint64_t *keys, int64_t n, uint64_t seed, int bits, uint64_t nb,
                     uint64_t bsize, uint64_t *out5, void *stream);
 
+/* Measurement kernel (not a reference function): n random 32-byte sector
+ * loads over [table, table + table_bytes) with the filters' hash stream; the
+ * bench times it on the filter's own table as the random-access ceiling. */
+int fk_sector_gather(const void *table, int64_t table_bytes, int64_t n, uint64_t salt, uint32_t *sink,
+                     void *stream);
+
 /* Exact x % d on device through the fast-mod path (tests only). */
 int fk_fastmod_check(const uint64_t *x, int64_t n, uint64_t d, uint64_t *out, void *stream);
 
@@ -214,6 +220,22 @@ int fk_gqf_rebuild_index(const fk_gqf_geom *g, const fk_gqf_tables *t, void *str
 int fk_gqf_apply(const fk_gqf_geom *g, const fk_gqf_tables *cur, const fk_gqf_tables *next,
                  const uint64_t *keys, int keys_are_fps, const uint64_t *deltas, int64_t n, int op, int order,
                  uint8_t *found, fk_gqf_result *result, void *stream);
+
+/* ---- hash-prefix sharding (new in this build) -------------- */
+
+/* Stable partition of a key batch by owner shard, owner = bits
+ * [shift, shift + log2_shards) of mix64(key ^ seed) (TCF: shift = 64 -
+ * log2_shards, the fingerprint's top bits; GQF: shift = q' + r, the top
+ * quotient bits).  keys_out/vals_out get the keys (and optional 64-bit values)
+ * grouped by owner in input order, perm[i] the input position of output i,
+ * counts (device int64[2^log2_shards]) the group sizes.  Asynchronous. */
+int fk_shard_partition(const uint64_t *keys, const uint64_t *vals, int64_t n, uint64_t seed, int shift,
+                       int log2_shards, uint64_t *keys_out, uint64_t *vals_out, uint32_t *perm, int64_t *counts,
+                       void *stream);
+
+/* dst[perm[i]] = src[i] for 1- or 8-byte elements: per-key results that came
+ * back from the owners, restored to input order.  Asynchronous. */
+int fk_shard_unpermute(const uint32_t *perm, const void *src, int64_t n, int elem_bytes, void *dst, void *stream);
 
 #ifdef __cplusplus
 }

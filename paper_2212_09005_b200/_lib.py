@@ -59,6 +59,7 @@ _SIGS = {
     "fk_device_setup": (c_i32, [c_i32]),
     "fk_device_l2_fetch_bytes": (c_i32, []),
     "fk_hash_streams": (c_i32, [c_vp, c_i64, c_u64, c_i32, c_u64, c_u64, c_vp, c_vp]),
+    "fk_sector_gather": (c_i32, [c_vp, c_i64, c_i64, c_u64, c_vp, c_vp]),
     "fk_fastmod_check": (c_i32, [c_vp, c_i64, c_u64, c_vp, c_vp]),
     "fk_tcf_workspace_bytes": (c_sz, [ctypes.POINTER(TcfGeom), c_i64, c_i32]),
     "fk_tcf_insert": (c_i32, [ctypes.POINTER(TcfGeom), c_vp, c_vp, c_vp, c_i32, c_vp, c_i64, c_vp,
@@ -73,6 +74,8 @@ _SIGS = {
                                c_vp]),
     "fk_btcf_partition": (c_i32, [ctypes.POINTER(BtcfGeom), c_vp, c_i32, c_i64, c_vp, c_vp, c_vp]),
     "fk_btcf_merge_lists": (c_i32, [ctypes.POINTER(BtcfGeom), c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "fk_shard_partition": (c_i32, [c_vp, c_vp, c_i64, c_u64, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "fk_shard_unpermute": (c_i32, [c_vp, c_vp, c_i64, c_i32, c_vp, c_vp]),
     "fk_gqf_count": (c_i32, [ctypes.POINTER(GqfGeom), ctypes.POINTER(GqfTables), c_vp, c_i32, c_i64, c_vp, c_vp]),
     "fk_gqf_find_run": (c_i32, [ctypes.POINTER(GqfGeom), ctypes.POINTER(GqfTables), c_vp, c_i64, c_vp, c_vp]),
     "fk_gqf_rebuild_index": (c_i32, [ctypes.POINTER(GqfGeom), ctypes.POINTER(GqfTables), c_vp]),

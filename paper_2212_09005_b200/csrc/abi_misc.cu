@@ -22,6 +22,22 @@ __global__ void k_fastmod(const uint64_t *__restrict__ x, int64_t n, FastMod m, 
     out[i] = fmod64(x[i], m);
 }
 
+// Random 32-byte sector gather over a table: the random-access ceiling the
+// filter kernels are measured against (same hash stream, same sector size,
+// same 256-bit loads, run on the filter's own table in the same process).
+__global__ void __launch_bounds__(256) k_sector_gather(const uint32_t *__restrict__ table, uint64_t nsec, FastMod m,
+                                                       int64_t n, uint64_t salt, uint32_t *__restrict__ sink) {
+  uint32_t acc = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t b = fmod64(mix64((uint64_t)i ^ salt), m);
+    uint32_t r[8];
+    load_chunk<32, false>(table + 8 * b, r);
+#pragma unroll
+    for (int j = 0; j < 8; j++) acc ^= r[j];
+  }
+  if (acc == 0x9E3779B9u) sink[blockIdx.x & 31] = acc;  // keeps the loads live
+}
+
 }  // namespace fk
 
 using namespace fk;
@@ -54,6 +70,18 @@ int fk_hash_streams(const uint64_t *keys, int64_t n, uint64_t seed, int bits, ui
   if (grid > num_sms() * 16) grid = num_sms() * 16;
   k_hash_streams<<<grid, 256, 0, (cudaStream_t)stream>>>(keys, n, seed, m, nb, make_fastmod(nb ? nb : 1), bsize,
                                                          make_fastmod(bsize ? bsize : 1), out5);
+  FK_CHECK_LAUNCH();
+  return 0;
+}
+
+int fk_sector_gather(const void *table, int64_t table_bytes, int64_t n, uint64_t salt, uint32_t *sink,
+                     void *stream) {
+  if (n < 0 || table_bytes < 32 || ((uintptr_t)table & 31)) return FK_E_ARG;
+  if (n == 0) return 0;
+  uint64_t nsec = (uint64_t)table_bytes / 32;
+  int grid = num_sms() * 8;
+  k_sector_gather<<<grid, 256, 0, (cudaStream_t)stream>>>((const uint32_t *)table, nsec, make_fastmod(nsec), n, salt,
+                                                          sink);
   FK_CHECK_LAUNCH();
   return 0;
 }

@@ -1,0 +1,121 @@
+// shard.cu -- hash-prefix sharding of key batches across GPUs.
+//
+// The reference is single-process; this is the new build's scale-out path.
+// A key's owner is a prefix of its fingerprint: for the TCF the top log2(G)
+// bits of mix64(key ^ seed) (b1, b2, tag and backing schedule all come from
+// other hash streams, so each shard is an independent Tcf(num_blocks / G));
+// for the GQF the top log2(G) quotient bits, i.e. bits [q' + r, q + r) with
+// q' = q - log2(G), so the shard's own Gqf(q', r) sees exactly the low
+// q' + r fingerprint bits and its counts equal a global Gqf(q, r)'s.
+//
+// fk_shard_partition stably groups a batch by owner (one-digit CUB radix
+// sort of the owner ids, then a gather of keys and optional 64-bit values)
+// and counts per owner; the caller exchanges the groups with one NCCL
+// all-to-all.  fk_shard_unpermute_* scatter the per-key results that come
+// back into input order.
+#include <cub/cub.cuh>
+
+#include "../../include/filterkit_b200.h"
+#include "fk_common.cuh"
+#include "fk_scratch.cuh"
+
+namespace fk {
+namespace {
+
+inline int grid_for(int64_t n) {
+  int64_t b = (n + 255) / 256;
+  int64_t cap = (int64_t)num_sms() * 16;
+  if (b > cap) b = cap;
+  return (int)(b < 1 ? 1 : b);
+}
+
+__global__ void k_owner(const uint64_t *__restrict__ keys, int64_t n, uint64_t seed, int shift, uint32_t gmask,
+                        uint8_t *__restrict__ owner, uint32_t *__restrict__ iota,
+                        unsigned long long *__restrict__ counts) {
+  __shared__ unsigned int hist[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t h = mix64(keys[i] ^ seed);
+    uint32_t o = shift >= 64 ? 0u : (uint32_t)(h >> shift) & gmask;
+    owner[i] = (uint8_t)o;
+    iota[i] = (uint32_t)i;
+    atomicAdd(&hist[o], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i <= (int)gmask; i += blockDim.x)
+    if (hist[i]) atomicAdd(&counts[i], (unsigned long long)hist[i]);
+}
+
+__global__ void k_gather2(const uint64_t *__restrict__ keys, const uint64_t *__restrict__ vals,
+                          const uint32_t *__restrict__ perm, int64_t n, uint64_t *__restrict__ keys_out,
+                          uint64_t *__restrict__ vals_out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t p = perm[i];
+    keys_out[i] = keys[p];
+    if (vals) vals_out[i] = vals[p];
+  }
+}
+
+template <typename T>
+__global__ void k_unpermute(const uint32_t *__restrict__ perm, const T *__restrict__ src, int64_t n,
+                            T *__restrict__ dst) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[perm[i]] = src[i];
+}
+
+}  // namespace
+}  // namespace fk
+
+using namespace fk;
+
+extern "C" {
+
+int fk_shard_partition(const uint64_t *keys, const uint64_t *vals, int64_t n, uint64_t seed, int shift, int log2_shards,
+                       uint64_t *keys_out, uint64_t *vals_out, uint32_t *perm, int64_t *counts, void *stream) {
+  if (n < 0 || n > 0xFFFFFFF0LL || log2_shards < 0 || log2_shards > 8 || shift < 0 || !counts) return FK_E_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  int G = 1 << log2_shards;
+  FK_TRY(cudaMemsetAsync(counts, 0, sizeof(int64_t) * G, st));
+  if (n == 0) return 0;
+  Scratch S(st);
+  uint8_t *owner = S.get<uint8_t>(n), *owner_s = S.get<uint8_t>(n);
+  uint32_t *iota = S.get<uint32_t>(n);
+  if (!owner || !owner_s || !iota) return -(int)S.err;
+  int sh = log2_shards == 0 ? 64 : shift;
+  k_owner<<<grid_for(n), 256, 0, st>>>(keys, n, seed, sh, (uint32_t)(G - 1), owner, iota,
+                                       reinterpret_cast<unsigned long long *>(counts));
+  FK_CHECK_LAUNCH();
+  if (log2_shards == 0) {
+    FK_TRY(cudaMemcpyAsync(perm, iota, 4 * (size_t)n, cudaMemcpyDeviceToDevice, st));
+  } else {
+    size_t tb = 0;
+    FK_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tb, owner, owner_s, iota, perm, n, 0, log2_shards, st));
+    void *tmp = S.get<char>(tb);
+    if (!tmp) return -(int)S.err;
+    FK_TRY(cub::DeviceRadixSort::SortPairs(tmp, tb, owner, owner_s, iota, perm, n, 0, log2_shards, st));
+  }
+  k_gather2<<<grid_for(n), 256, 0, st>>>(keys, vals, perm, n, keys_out, vals_out);
+  FK_CHECK_LAUNCH();
+  return 0;
+}
+
+int fk_shard_unpermute(const uint32_t *perm, const void *src, int64_t n, int elem_bytes, void *dst, void *stream) {
+  if (n < 0) return FK_E_ARG;
+  if (n == 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (elem_bytes) {
+    case 1:
+      k_unpermute<uint8_t><<<grid_for(n), 256, 0, st>>>(perm, (const uint8_t *)src, n, (uint8_t *)dst);
+      break;
+    case 8:
+      k_unpermute<uint64_t><<<grid_for(n), 256, 0, st>>>(perm, (const uint64_t *)src, n, (uint64_t *)dst);
+      break;
+    default:
+      return FK_E_ARG;
+  }
+  FK_CHECK_LAUNCH();
+  return 0;
+}
+
+}  // extern "C"
