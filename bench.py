@@ -406,6 +406,159 @@ def run_ours(args, rank, world, local_rank):
 
 
 # ---------------------------------------------------------------------------
+# secondary workloads: bulk TCF (configs[0] shape) and GQF (configs[1], C2)
+# ---------------------------------------------------------------------------
+
+def _workload_setup(args, rank, world, dev, torch):
+    """-> (filter, {op: (fn(dev_inputs), n_items)}, inputs, describe, cpu_fn)."""
+    seed = 1 + 1000 * rank
+    if args.workload == "bulk_tcf":
+        from paper_2212_09005_b200 import BulkTcf
+        from paper_2212_09005_b200.sharding import ShardedBulkTcf
+        log_slots = args.log_slots if args.log_slots_set else 20
+        nb = (1 << log_slots) // 128
+        n = int(args.load * (1 << log_slots))
+        filt = ShardedBulkTcf(num_blocks=nb * world) if world > 1 else BulkTcf(num_blocks=nb)
+        keys = device_keys(torch, seed, TAG_UNIFORM, n, dev)
+        negs = device_keys(torch, seed + 1, TAG_FPR, n, dev)
+        ops = [("insert", lambda x: filt.insert_batch(x["keys"]), n),
+               ("query_pos", lambda x: filt.query_batch(x["keys"]), n),
+               ("query_neg", lambda x: filt.query_batch(x["negs"]), n),
+               ("delete", lambda x: filt.delete_batch(x["keys"]), n)]
+        desc = ("configs[0] shape: bulk TCF, 2^%d slots/GPU (nb=2^%d x B=128, 16-bit tags, 1%% backing), uniform "
+                "64-bit keys, one insert_batch to %.2f load + pos/neg query_batch + delete_batch"
+                % (log_slots, log_slots - 7, args.load))
+        return filt, ops, {"keys": keys, "negs": negs}, desc, ("bulk_tcf", log_slots, args.load)
+    # GQF, C2: duplicate-heavy ur_count keys (counts U{1..100}), naive bulk insert
+    from paper_2212_09005_b200 import Gqf
+    from paper_2212_09005_b200.sharding import ShardedGqf
+    from paper_2212_09005_b200.workloads import WorkloadSpec, gen_keys
+    q = args.log_slots if args.log_slots_set else 22
+    occ = gen_keys(WorkloadSpec("ur_count", n=int(args.load * (1 << q)) // 4, seed=seed))
+    uniq = np.unique(occ)
+    filt = ShardedGqf(q=q + (world.bit_length() - 1)) if world > 1 else Gqf(q=q)
+    x = {"occ": torch.from_numpy(occ.view(np.int64)).to(dev), "uniq": torch.from_numpy(uniq.view(np.int64)).to(dev)}
+    ops = [("bulk_insert", lambda d: filt.bulk_insert(d["occ"]), len(occ)),
+           ("count", lambda d: filt.count_many(d["uniq"]), len(uniq)),
+           ("bulk_delete", lambda d: filt.bulk_delete(d["uniq"]), len(uniq))]
+    desc = ("C2: GQF q=%d r=8 per GPU, ur_count keys (%d distinct x U{1..100} = %d occurrences), naive bulk_insert "
+            "of every occurrence + count_many(distinct) + bulk_delete(distinct, all copies)" % (q, len(uniq), len(occ)))
+    return filt, ops, x, desc, ("gqf", q, args.load)
+
+
+def run_workload(args, rank, world, local_rank):
+    import torch
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+    filt, ops, x, desc, cpu_key = _workload_setup(args, rank, world, dev, torch)
+    stream = torch.cuda.current_stream()
+
+    def step(ev=None, inp=x):
+        filt._reset()
+        out = []
+        for i, (_, fn, _) in enumerate(ops):
+            if ev:
+                ev[i].record(stream)
+            out.append(fn(inp))
+        if ev:
+            ev[len(ops)].record(stream)
+        return out
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(len(ops) + 1)] for _ in range(args.steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        t0.record(stream)
+        for s in range(args.steps):
+            step(evs[s])
+        t1.record(stream)
+        torch.cuda.synchronize()
+    ms_total = t0.elapsed_time(t1)
+    if dist:
+        t = torch.tensor([ms_total], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    items = sum(n for _, _, n in ops)
+    per_op = {}
+    for i, (name, _, n) in enumerate(ops):
+        ms = float(np.mean([evs[s][i].elapsed_time(evs[s][i + 1]) for s in range(args.steps)]))
+        per_op[name] = {"ops_per_s": n / (ms / 1e3), "ms": ms, "items": n}
+    e2e = None
+    if not args.no_e2e:
+        hx = {k: v.cpu().pin_memory() for k, v in x.items()}
+        step(inp=hx)
+        torch.cuda.synchronize()
+        tsum = time.perf_counter()
+        for _ in range(max(1, min(args.steps, 3))):
+            step(inp=hx)
+        torch.cuda.synchronize()
+        te = (time.perf_counter() - tsum) / max(1, min(args.steps, 3))
+        if dist:
+            t = torch.tensor([te], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            te = float(t.item())
+        e2e = {"value": items * world / te, "unit": UNIT, "ms_per_step": te * 1e3,
+               "h2d_bytes_per_step": 8 * items, "d2h_bytes_per_step": None}
+    launches = count_launches(torch, step) if not args.no_launch_count else None
+    res = {"metric": METRIC, "value": items * world / (ms_step / 1e3), "unit": UNIT, "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "u16" if args.workload == "bulk_tcf" else "u8",
+           "data": "synthetic", "config": {"workload": desc, "l2": "no flush: inputs + tables rewritten per step"},
+           "per_op": per_op, "e2e": e2e, "gpu_launches": launches * args.steps if launches is not None else None,
+           "gpu_launches_per_step": launches, "clocks": clk.summary()}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        res["cpu_baseline"] = cpu_baseline_workload(cpu_key)
+    return res if rank == 0 else None
+
+
+def cpu_baseline_workload(key):
+    """The reference's compiled kernels + restated facade glue (oracle/
+    ref_model.py) on all host cores, on the same workload."""
+    from oracle import ref_model
+    if not ref_model.available():
+        return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": "oracle/_ref not built"}
+    threads = os.cpu_count() or 1
+    kind, log_slots, load = key
+    if kind == "bulk_tcf":
+        nb = (1 << log_slots) // 128
+        n = int(load * (1 << log_slots))
+        keys = counter_stream(1, TAG_UNIFORM, n)
+        negs = counter_stream(2, TAG_FPR, n)
+        f = ref_model.RefBulkTcf(nb, backing_slots=int(round(nb * 128 * 0.01)))
+        t = time.perf_counter()
+        f.insert_batch(keys, threads)
+        f.query_batch(keys, threads)
+        f.query_batch(negs, threads)
+        f.delete_batch(keys, threads)
+        dt = time.perf_counter() - t
+        ops = 4 * n
+        what = "bulk TCF 2^%d, insert_batch+2x query_batch+delete_batch, workers=%d" % (log_slots, threads)
+    else:
+        from paper_2212_09005_b200.workloads import WorkloadSpec, gen_keys
+        occ = gen_keys(WorkloadSpec("ur_count", n=int(load * (1 << log_slots)) // 4, seed=1))
+        uniq = np.unique(occ)
+        f = ref_model.RefGqf(log_slots)
+        t = time.perf_counter()
+        f.bulk_insert(occ, workers=threads)
+        f.count_many(uniq, threads)
+        f.bulk_delete(uniq, workers=threads)
+        dt = time.perf_counter() - t
+        ops = len(occ) + 2 * len(uniq)
+        what = "GQF q=%d ur_count naive bulk_insert + count_many + bulk_delete, workers=%d" % (log_slots, threads)
+    return {"value": ops / dt, "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": "reference _ckernels (oracle/_ref) + facade glue: %s (%d ops, %.1f s)" % (what, ops, dt)}
+
+
+# ---------------------------------------------------------------------------
 # CPU baseline / reference arm: the reference's own compiled kernels
 # ---------------------------------------------------------------------------
 
@@ -491,7 +644,8 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--log-slots", type=int, default=28)
+    ap.add_argument("--workload", choices=["tcf", "bulk_tcf", "gqf"], default="tcf")
+    ap.add_argument("--log-slots", type=int, default=None)
     ap.add_argument("--load", type=float, default=0.9)
     ap.add_argument("--group-width", type=int, default=1)
     ap.add_argument("--mode", choices=["ordered", "concurrent"], default="ordered")
@@ -502,6 +656,9 @@ def main():
     ap.add_argument("--cpu-budget-s", type=float, default=15.0)
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    args.log_slots_set = args.log_slots is not None
+    if args.log_slots is None:
+        args.log_slots = 28
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -514,7 +671,7 @@ def main():
             import torch.distributed as dist
             torch.cuda.set_device(local_rank)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-        res = run_ours(args, rank, world, local_rank)
+        res = (run_ours if args.workload == "tcf" else run_workload)(args, rank, world, local_rank)
         if world > 1:
             import torch.distributed as dist
             dist.destroy_process_group()

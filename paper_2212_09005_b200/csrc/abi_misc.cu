@@ -52,6 +52,16 @@ int fk_device_setup(int l2_fetch_bytes) {
   // default L2 fetch granularity would turn every miss into a 64-128 B DRAM
   // read.  This is a per-context hint (cudaLimitMaxL2FetchGranularity).
   if (l2_fetch_bytes > 0) FK_TRY(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)l2_fetch_bytes));
+  // Batch pipelines take their scratch from the device's default memory pool
+  // (cudaMallocAsync).  With the default release threshold of 0 the pool
+  // hands memory back to the driver at every stream synchronisation and the
+  // next batch pays for re-mapping it; keep it cached instead.
+  int dev = 0;
+  FK_TRY(cudaGetDevice(&dev));
+  cudaMemPool_t pool;
+  FK_TRY(cudaDeviceGetDefaultMemPool(&pool, dev));
+  uint64_t keep = ~0ULL;
+  FK_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
   return 0;
 }
 

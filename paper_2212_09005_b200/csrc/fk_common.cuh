@@ -198,6 +198,37 @@ __device__ __forceinline__ uint64_t reg_slot(const uint32_t *regs, int i) {
   }
 }
 
+// --- L2 cache-policy hints (createpolicy + .L2::cache_hint) -----------------
+// Small, hot side structures (reservation words) are kept with evict_last so
+// that the stream of random table sectors (evict_first) does not push them
+// out of L2.
+__device__ __forceinline__ uint64_t l2_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void red_min_u32(uint32_t *a, uint32_t v, uint64_t pol) {
+  asm volatile("red.relaxed.gpu.global.min.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(a), "r"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_cg_u32(const uint32_t *a, uint64_t pol) {
+  uint32_t v;
+  asm volatile("ld.global.cg.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_u32(uint32_t *a, uint32_t v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(a), "r"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_stream_u64(const uint64_t *a, uint64_t pol) {
+  uint64_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(v) : "l"(a), "l"(pol));
+  return v;
+}
+
 // Error plumbing for the C ABI: never throw, return a negative cudaError_t.
 #define FK_CHECK_LAUNCH()                                 \
   do {                                                    \

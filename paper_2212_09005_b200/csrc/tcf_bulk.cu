@@ -317,82 +317,82 @@ __global__ void __launch_bounds__(256) k_btcf_query(BDev P, const uint64_t *__re
 }
 
 // ---------------------------------------------------------------------------
-// sequential two-choice routing (btcf_route, ck:408-444) by windowed
-// deterministic reservations.  Leftover k (in sorted order) may decide once
-// it holds the minimum pending index on both of its blocks: every earlier
-// leftover that could change those blocks' committed load has decided.
+// sequential two-choice routing (btcf_route, ck:408-444)
 // ---------------------------------------------------------------------------
-struct RouteScratch {
-  uint32_t *res;       // per block: min pending leftover index
-  uint32_t *carry[2];  // leftovers carried to the next round
-  unsigned *ctl;       // [0..1] carry counts
-  int64_t window;
-};
-
-__global__ void __launch_bounds__(256) k_btcf_route(const uint32_t *__restrict__ lb1, const uint32_t *__restrict__ lb2,
-                                                    int64_t m, uint32_t *__restrict__ load, uint32_t B,
-                                                    int32_t *__restrict__ dest, RouteScratch X) {
-  cg::grid_group grid = cg::this_grid();
-  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
-  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  int64_t F = 0, nc = 0;
-  int cur = 0;
-  for (;;) {
-    int64_t room = X.window - nc;
-    room = room < 0 ? 0 : room;
-    int64_t Fend = F + room < m ? F + room : m;
-    int64_t total = (Fend - F) + nc;
-    const uint32_t *cin = X.carry[cur];
-    uint32_t *cout = X.carry[cur ^ 1];
-    for (int64_t e = tid; e < total; e += nthreads) {
-      uint32_t k = e < nc ? __ldcg(cin + e) : (uint32_t)(F + e - nc);
-      uint32_t a = lb1[k], b = lb2[k];
-      atomicMin(&X.res[a], k);
-      if (b != a) atomicMin(&X.res[b], k);
-    }
-    grid.sync();
-    if (tid == 0) X.ctl[cur] = 0;
-    for (int64_t e0 = tid - (threadIdx.x & 31);; e0 += nthreads) {
-      if (e0 >= total) break;  // warp-uniform
-      int64_t e = e0 + (threadIdx.x & 31);
-      bool ok = e < total;
-      uint32_t k = 0, a = 0, b = 0;
-      bool hold = false;
-      if (ok) {
-        k = e < nc ? __ldcg(cin + e) : (uint32_t)(F + e - nc);
-        a = lb1[k];
-        b = lb2[k];
-        hold = __ldcg(&X.res[a]) == k && __ldcg(&X.res[b]) == k;
-      }
-      bool carry = ok && !hold;
-      unsigned bal = __ballot_sync(0xFFFFFFFFu, carry);
-      unsigned basepos = 0;
-      if ((threadIdx.x & 31) == 0 && bal) basepos = atomicAdd(&X.ctl[cur ^ 1], (unsigned)__popc(bal));
-      basepos = __shfl_sync(0xFFFFFFFFu, basepos, 0);
-      if (carry) cout[basepos + __popc(bal & ((1u << (threadIdx.x & 31)) - 1u))] = k;
-      if (hold) {
-        uint32_t l1 = __ldcg(&load[a]), l2 = __ldcg(&load[b]);
-        uint32_t pick = l1 <= l2 ? a : b;  // tie -> primary (ck:431)
-        uint32_t lp = pick == a ? l1 : l2;
-        int32_t d;
-        if (lp >= B) {
-          pick = pick == a ? b : a;
-          lp = pick == a ? l1 : l2;
-          d = lp >= B ? -1 : (int32_t)pick;
-        } else {
-          d = (int32_t)pick;
-        }
-        if (d >= 0) load[d] = lp + 1;
-        dest[k] = d;
-        X.res[a] = kNone;
-        X.res[b] = kNone;
-      }
-    }
-    grid.sync();
-    nc = (int64_t)__ldcg(&X.ctl[cur ^ 1]);
-    cur ^= 1;
-    F = Fend;
-    if (F >= m && nc == 0) break;
+// The reference routes the leftovers one by one in (b1, word) order, each
+// decision reading the committed load of both candidate blocks.  Sorted by
+// b1, consecutive leftovers share a block, so the dependency chain is long
+// (6405 deep for a 0.9-load batch into 2^20 slots) and parallel
+// reservations would need thousands of grid-wide rounds.  The walk is
+// therefore one warp: the per-block load counters live in shared memory
+// (global memory when nb does not fit), leftovers stream in through
+// coalesced 32-wide loads, and the next leftover's two counters are fetched
+// before the current decision is written back and patched in registers
+// (store-to-load forwarding), so the chain costs one short dependent step
+// per leftover.
+template <bool SMEM>
+__global__ void __launch_bounds__(32) k_btcf_route_seq(const uint32_t *__restrict__ lb1,
+                                                       const uint32_t *__restrict__ lb2, int64_t m,
+                                                       const uint32_t *__restrict__ fill, uint64_t nb,
+                                                       uint32_t *__restrict__ gload, uint32_t B,
+                                                       int32_t *__restrict__ dest) {
+  // Every lane runs the identical walk on broadcast reads and stores the same
+  // value, so each lane's next read sees its own store: no cross-lane
+  // synchronisation on the chain.  Counters for leftovers j+1 and j+2 are
+  // read ahead and patched with the decisions of j (and j+1).
+  extern __shared__ uint32_t sload[];
+  uint32_t *load = SMEM ? sload : gload;
+  const unsigned lane = threadIdx.x;
+  if (SMEM) {
+    for (uint64_t i = lane; i < nb; i += 32) sload[i] = fill[i];
+    __syncwarp();
+  }
+  if (m <= 0) return;
+  uint32_t ca = lane < m ? lb1[lane] : 0, cb = lane < m ? lb2[lane] : 0;
+  uint32_t na = 32 + lane < m ? lb1[32 + lane] : 0, nb2 = 32 + lane < m ? lb2[32 + lane] : 0;
+  // pipeline registers: (a, b, la, lb) for the current leftover and the next
+  uint32_t a0 = __shfl_sync(0xFFFFFFFFu, ca, 0), b0 = __shfl_sync(0xFFFFFFFFu, cb, 0);
+  uint32_t l0a = load[a0], l0b = load[b0];
+  uint32_t a1 = __shfl_sync(0xFFFFFFFFu, ca, 1 & 31), b1 = __shfl_sync(0xFFFFFFFFu, cb, 1 & 31);
+  uint32_t l1a = load[a1], l1b = load[b1];
+  int32_t mine = 0;
+  // one leftover: decide k, forward the write into the read-ahead slots and
+  // read ahead leftover k + 2 (whose blocks are a2/b2)
+  // Decision (ck:429-442): pick = b1 if load(b1) <= load(b2) else b2; if the
+  // pick is full try the other; both full -> backing.  Since the pick holds
+  // the smaller load, "pick full" implies "both full", so the rule is: the
+  // smaller-load block (tie -> b1) unless min(load) >= B.  Written branch-free
+  // to keep the loop-carried chain short.
+  auto step = [&](int j, uint32_t a2, uint32_t b2) {
+    uint32_t l2a = load[a2], l2b = load[b2];  // read ahead (a2/b2 are 0 past the end)
+    const bool pa = l0a <= l0b;
+    const uint32_t lp = pa ? l0a : l0b;
+    const uint32_t dsel = pa ? a0 : b0;
+    const bool ok = lp < B;
+    const uint32_t v = lp + 1;
+    if (ok) load[dsel] = v;
+    const uint32_t dd = ok ? dsel : 0xFFFFFFFFu;
+    l1a = a1 == dd ? v : l1a;
+    l1b = b1 == dd ? v : l1b;
+    l2a = a2 == dd ? v : l2a;
+    l2b = b2 == dd ? v : l2b;
+    if ((int)lane == j) mine = ok ? (int32_t)dsel : -1;
+    a0 = a1; b0 = b1; l0a = l1a; l0b = l1b;
+    a1 = a2; b1 = b2; l1a = l2a; l1b = l2b;
+  };
+  for (int64_t base = 0; base < m; base += 32) {
+    const int cnt = m - base < 32 ? (int)(m - base) : 32;
+    // leftovers j + 2 < 32 come from this chunk's registers, the last two
+    // from the next chunk's (loaded a full chunk earlier)
+    for (int j = 0; j < 30 && j < cnt; j++)
+      step(j, __shfl_sync(0xFFFFFFFFu, ca, j + 2), __shfl_sync(0xFFFFFFFFu, cb, j + 2));
+    for (int j = 30; j < cnt; j++)
+      step(j, __shfl_sync(0xFFFFFFFFu, na, j - 30), __shfl_sync(0xFFFFFFFFu, nb2, j - 30));
+    if (base + lane < m) dest[base + lane] = mine;
+    ca = na;
+    cb = nb2;
+    na = base + 64 + lane < m ? lb1[base + 64 + lane] : 0;
+    nb2 = base + 64 + lane < m ? lb2[base + 64 + lane] : 0;
   }
 }
 
@@ -712,27 +712,20 @@ int btcf_insert(const BDev &P, const uint64_t *keys, int64_t n, uint64_t *failed
   if (m > 0) {
     uint32_t *lb1 = S.get<uint32_t>(m), *lb2 = S.get<uint32_t>(m), *load = S.get<uint32_t>(P.nb);
     int32_t *dest = S.get<int32_t>(m);
-    RouteScratch X;
-    X.res = S.get<uint32_t>(P.nb);
-    int64_t window = 1 << 18;
-    if (const char *e = getenv("FK_ROUTE_WINDOW")) window = atoll(e) > 0 ? atoll(e) : window;
-    X.window = window < m ? window : m;
-    X.carry[0] = S.get<uint32_t>(X.window);
-    X.carry[1] = S.get<uint32_t>(X.window);
-    X.ctl = S.get<unsigned>(4);
-    FK_P(lb1); FK_P(lb2); FK_P(load); FK_P(dest); FK_P(X.res); FK_P(X.carry[0]); FK_P(X.carry[1]); FK_P(X.ctl);
+    FK_P(lb1); FK_P(lb2); FK_P(load); FK_P(dest);
     k_left_blocks<<<grid_for(m), 256, 0, st>>>(P, keys, sval, lpos, m, lb1, lb2);
     FK_CHECK_LAUNCH();
-    FK_S(cudaMemcpyAsync(load, P.fill, P.nb * 4, cudaMemcpyDeviceToDevice, st));
-    FK_S(cudaMemsetAsync(X.res, 0xFF, P.nb * 4, st));
-    FK_S(cudaMemsetAsync(X.ctl, 0, 16, st));
-    int grid = coop_grid((const void *)k_btcf_route, 256);
-    if (!grid) return FK_E_ARG;
-    int64_t need = (X.window + 255) / 256;
-    if (need < grid) grid = (int)(need < 1 ? 1 : need);
     uint32_t Bu = (uint32_t)P.B;
-    void *args[] = {(void *)&lb1, (void *)&lb2, (void *)&m, (void *)&load, (void *)&Bu, (void *)&dest, (void *)&X};
-    FK_S(cudaLaunchCooperativeKernel((const void *)k_btcf_route, dim3(grid), dim3(256), args, 0, st));
+    size_t sm = (size_t)P.nb * 4;
+    if (sm <= 200 * 1024) {
+      if (sm > 48 * 1024)
+        FK_S(cudaFuncSetAttribute(k_btcf_route_seq<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      k_btcf_route_seq<true><<<1, 32, sm, st>>>(lb1, lb2, m, P.fill, P.nb, load, Bu, dest);
+    } else {
+      FK_S(cudaMemcpyAsync(load, P.fill, P.nb * 4, cudaMemcpyDeviceToDevice, st));
+      k_btcf_route_seq<false><<<1, 32, 0, st>>>(lb1, lb2, m, P.fill, P.nb, load, Bu, dest);
+    }
+    FK_CHECK_LAUNCH();
     // group by destination; segment 0 = backing (tcf_bulk.py:225-234)
     uint64_t *k2 = S.get<uint64_t>(m), *skey2 = S.get<uint64_t>(m);
     uint32_t *v2 = S.get<uint32_t>(m), *sval2 = S.get<uint32_t>(m);

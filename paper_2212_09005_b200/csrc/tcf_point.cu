@@ -51,12 +51,23 @@ static int run(const fk_tcf_geom *g, int op, const TcfDev &P, const TcfCall &c, 
 }
 
 static int64_t ord_window(int64_t n) {
-  int64_t w = 1 << 20;  // keys introduced per round (tunable: FK_ORD_WINDOW)
+  int64_t w = 1 << 18;  // keys introduced per round (tunable: FK_ORD_WINDOW)
   if (const char *e = getenv("FK_ORD_WINDOW")) {
     long long v = atoll(e);
     if (v > 0) w = v;
   }
   return w < n ? w : (n < 1 ? 1 : n);
+}
+
+static int ord_res_shift() {
+  int rs = 2;  // blocks per reservation word = 2^rs (tunable: FK_ORD_RES_SHIFT)
+  if (const char *e = getenv("FK_ORD_RES_SHIFT")) rs = atoi(e);
+  return rs < 0 ? 0 : (rs > 16 ? 16 : rs);
+}
+
+static int ord_hints() {
+  const char *e = getenv("FK_ORD_HINTS");
+  return e ? atoi(e) != 0 : 1;
 }
 
 static size_t ord_ws_layout(const fk_tcf_geom *g, int64_t n, size_t *off) {
@@ -65,7 +76,7 @@ static size_t ord_ws_layout(const fk_tcf_geom *g, int64_t n, size_t *off) {
   auto take = [&](size_t bytes) { size_t o = a; a += (bytes + 255) & ~(size_t)255; return o; };
   int64_t cap = n < 1 ? 1 : n;
   int64_t w = ord_window(n);
-  off[0] = take((size_t)g->num_blocks * 4);
+  off[0] = take((size_t)((g->num_blocks >> ord_res_shift()) + 1) * 4);
   off[1] = take((size_t)(g->backing_slots ? g->backing_slots : 1) * 4);
   off[2] = take((size_t)cap * 4);
   off[3] = take((size_t)cap);
@@ -90,7 +101,9 @@ static int prep_ordered(const fk_tcf_geom *g, int64_t n, void *ws, size_t ws_byt
   X->carry[1] = (uint32_t *)(b + off[6]);
   X->defer_cap = n < 1 ? 1 : n;
   X->window = ord_window(n);
-  FK_TRY(cudaMemsetAsync(X->res, 0xFF, (size_t)g->num_blocks * 4, st));
+  X->res_shift = ord_res_shift();
+  X->hints = ord_hints();
+  FK_TRY(cudaMemsetAsync(X->res, 0xFF, (size_t)((g->num_blocks >> X->res_shift) + 1) * 4, st));
   FK_TRY(cudaMemsetAsync(X->bres, 0xFF, (size_t)(g->backing_slots ? g->backing_slots : 1) * 4, st));
   FK_TRY(cudaMemsetAsync(X->ctl, 0, 64, st));
   return 0;

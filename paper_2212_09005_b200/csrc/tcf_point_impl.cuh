@@ -122,6 +122,22 @@ struct Chunk {
       if (j >= j0 && j < cnt && !live_word(at(j))) return j;
     return -1;
   }
+  // Branch-free lowest match for 16-bit slots whose word is the tag itself
+  // (tag_bits == 16: no value bits; tags are >= 2, so EMPTY/TOMBSTONE never
+  // match): one __vcmpeq2 per register pair of slots.
+  __device__ __forceinline__ int first_match_eq16(uint32_t tag) const {
+    static_assert(sizeof(S) == 2, "16-bit slots only");
+    const uint32_t pat = tag | (tag << 16);
+    uint32_t bits = 0;
+#pragma unroll
+    for (int i = 0; i < NREG; i++) {
+      uint32_t m = __vcmpeq2(r[i], pat);
+      bits |= ((m & 1u) | ((m >> 15) & 2u)) << (2 * i);
+    }
+    if (BF == 0) bits &= cnt >= 32 ? 0xFFFFFFFFu : ((1u << cnt) - 1u);
+    return bits ? __ffs(bits) - 1 : -1;
+  }
+
   // first index >= j0 holding a live word whose tag bits equal tag, else -1
   __device__ __forceinline__ int first_match(int j0, uint64_t tag, uint64_t fmask) const {
 #pragma unroll
@@ -153,7 +169,12 @@ __global__ void __launch_bounds__(256) k_tcf_query(TcfDev P, const uint64_t *__r
       uint64_t b = which ? k.b2 : k.b1;
       Chunk<S, G, BF> c;
       c.template load<false>(blocks + b * (uint64_t)P.B, P.B, t.lane);
-      int j = c.first_match(0, k.tag, P.fmask);
+      int j;
+      if constexpr (sizeof(S) == 2 && Chunk<S, G, BF>::C <= 32) {
+        j = P.f == 16 ? c.first_match_eq16((uint32_t)k.tag) : c.first_match(0, k.tag, P.fmask);
+      } else {
+        j = c.first_match(0, k.tag, P.fmask);
+      }
       unsigned bal = t.ballot(j >= 0);
       if (bal) {
         int leader = __ffs(bal) - 1;
@@ -338,6 +359,8 @@ struct OrdScratch {
   unsigned int *ctl;    // [0..1] carry counts, [2] defer count, [3..4] backing-phase round flags
   int64_t defer_cap;
   int64_t window;       // keys introduced per round
+  int res_shift;        // reservation granularity: 2^res_shift blocks per word
+  int hints;            // 1: L2 evict_last on reservation words, evict_first on streams
 };
 
 // CTA-wide OR of a predicate (all threads of the CTA must call).
@@ -437,6 +460,7 @@ __global__ void __launch_bounds__(256, 4)
   int64_t nc = 0;
   int cur = 0;
   unsigned round = 0;
+  const uint64_t pol_keep = l2_evict_last(), pol_stream = l2_evict_first();
 
   for (;;) {
     int64_t room = Wn - nc;
@@ -459,7 +483,7 @@ __global__ void __launch_bounds__(256, 4)
 #pragma unroll
       for (int j = 0; j < KB; j++) {
         if (!ok[j]) continue;
-        KeyInfo ki = key_info(P, keys[idx[j]]);
+        KeyInfo ki = key_info(P, X.hints ? ld_stream_u64(keys + idx[j], pol_stream) : keys[idx[j]]);
         b1[j] = (uint32_t)ki.b1;
         b2[j] = (uint32_t)ki.b2;
       }
@@ -467,8 +491,14 @@ __global__ void __launch_bounds__(256, 4)
 #pragma unroll
         for (int j = 0; j < KB; j++) {
           if (!ok[j]) continue;
-          atomicMin(&X.res[b1[j]], idx[j]);
-          if (b2[j] != b1[j]) atomicMin(&X.res[b2[j]], idx[j]);
+          uint32_t g1 = b1[j] >> X.res_shift, g2 = b2[j] >> X.res_shift;
+          if (X.hints) {
+            red_min_u32(&X.res[g1], idx[j], pol_keep);
+            if (g2 != g1) red_min_u32(&X.res[g2], idx[j], pol_keep);
+          } else {
+            atomicMin(&X.res[g1], idx[j]);
+            if (g2 != g1) atomicMin(&X.res[g2], idx[j]);
+          }
         }
       }
     }
@@ -491,14 +521,17 @@ __global__ void __launch_bounds__(256, 4)
 #pragma unroll
       for (int j = 0; j < KB; j++) {
         if (!ok[j]) continue;
-        KeyInfo ki = key_info(P, keys[idx[j]]);
+        KeyInfo ki = key_info(P, X.hints ? ld_stream_u64(keys + idx[j], pol_stream) : keys[idx[j]]);
         b1[j] = (uint32_t)ki.b1;
         b2[j] = (uint32_t)ki.b2;
         word[j] = OP == 0 ? ((P.f >= 64 ? 0 : ((values ? values[idx[j]] : 0) << P.f)) | ki.tag) : ki.tag;
       }
 #pragma unroll
       for (int j = 0; j < KB; j++)
-        hold[j] = ok[j] && __ldcg(&X.res[b1[j]]) == idx[j] && __ldcg(&X.res[b2[j]]) == idx[j];
+        hold[j] = ok[j] && (X.hints ? ld_cg_u32(&X.res[b1[j] >> X.res_shift], pol_keep)
+                                    : __ldcg(&X.res[b1[j] >> X.res_shift])) == idx[j] &&
+                  (X.hints ? ld_cg_u32(&X.res[b2[j] >> X.res_shift], pol_keep)
+                           : __ldcg(&X.res[b2[j] >> X.res_shift])) == idx[j];
       Chunk<S, G, BF> c1[KB];
       S *blocks = reinterpret_cast<S *>(P.blocks);
 #pragma unroll
@@ -552,8 +585,14 @@ __global__ void __launch_bounds__(256, 4)
               X.defer_pend[slot] = 1;
             }
           }
-          X.res[b1[j]] = kNoRes;  // only the holder writes these words now
-          X.res[b2[j]] = kNoRes;
+          // only the holder writes these words now
+          if (X.hints) {
+            st_u32(&X.res[b1[j] >> X.res_shift], kNoRes, pol_keep);
+            st_u32(&X.res[b2[j] >> X.res_shift], kNoRes, pol_keep);
+          } else {
+            X.res[b1[j] >> X.res_shift] = kNoRes;
+            X.res[b2[j] >> X.res_shift] = kNoRes;
+          }
         }
       }
     }

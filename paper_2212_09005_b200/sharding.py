@@ -80,6 +80,19 @@ class _Router:
         self.torch, self.group, self.world = torch, group, world
         self.log2g = _log2_exact(world)
         self.seed, self.shift, self.ops = seed, shift, ops
+        self.stage = False  # gloo moves host tensors only: stage device buffers through the host
+        if world > 1:
+            import torch.distributed as dist
+            self.stage = dist.get_backend(group) == "gloo"
+
+    def _a2a(self, out, inp, out_splits=None, in_splits=None):
+        import torch.distributed as dist
+        if self.stage and inp.is_cuda:
+            o = out.cpu()
+            dist.all_to_all_single(o, inp.cpu(), out_splits, in_splits, group=self.group)
+            out.copy_(o)
+        else:
+            dist.all_to_all_single(out, inp, out_splits, in_splits, group=self.group)
 
     def route(self, keys, vals=None):
         """-> (keys that this rank owns, their values, plan for unroute)."""
@@ -89,15 +102,15 @@ class _Router:
         import torch.distributed as dist
         ko, vo, perm, counts = self.ops.partition(keys, vals, self.seed, self.shift, self.log2g)
         rcounts = torch.empty_like(counts)
-        dist.all_to_all_single(rcounts, counts, group=self.group)
+        self._a2a(rcounts, counts)
         send = counts.tolist()
         recv = rcounts.tolist()
         rk = torch.empty(sum(recv), dtype=keys.dtype, device=keys.device)
-        dist.all_to_all_single(rk, ko, recv, send, group=self.group)
+        self._a2a(rk, ko, recv, send)
         rv = None
         if vals is not None:
             rv = torch.empty(sum(recv), dtype=vals.dtype, device=vals.device)
-            dist.all_to_all_single(rv, vo, recv, send, group=self.group)
+            self._a2a(rv, vo, recv, send)
         return rk, rv, (perm, send, recv)
 
     def unroute(self, res, plan):
@@ -105,19 +118,22 @@ class _Router:
         rank's own keys, in its input order."""
         if plan is None:
             return res
-        import torch.distributed as dist
         perm, send, recv = plan
         back = self.torch.empty(sum(send), dtype=res.dtype, device=res.device)
-        dist.all_to_all_single(back, res.contiguous(), send, recv, group=self.group)
+        self._a2a(back, res.contiguous(), send, recv)
         return self.ops.unpermute(perm, back)
+
+    def _coll_device(self):
+        if self.stage or not self.torch.cuda.is_available():
+            return "cpu"
+        return "cuda"
 
     def any_flag(self, flag):
         """Max of a small int over ranks (error propagation after a batch)."""
         if self.world == 1:
             return int(flag)
         import torch.distributed as dist
-        t = self.torch.tensor([int(flag)], dtype=self.torch.int64,
-                              device="cuda" if self.torch.cuda.is_available() else "cpu")
+        t = self.torch.tensor([int(flag)], dtype=self.torch.int64, device=self._coll_device())
         dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
         return int(t.item())
 
@@ -125,8 +141,7 @@ class _Router:
         if self.world == 1:
             return list(values)
         import torch.distributed as dist
-        t = self.torch.tensor(list(values), dtype=self.torch.int64,
-                              device="cuda" if self.torch.cuda.is_available() else "cpu")
+        t = self.torch.tensor(list(values), dtype=self.torch.int64, device=self._coll_device())
         dist.all_reduce(t, group=self.group)
         return t.tolist()
 
