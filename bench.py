@@ -128,25 +128,10 @@ def counter_stream(seed, tag, n):
 
 
 def device_keys(torch, seed, tag, n, device):
-    """Same keys as counter_stream, generated on the device (chunked numpy
-    would take seconds at 2^28 scale; this is setup, not timed)."""
-    from paper_2212_09005_b200.hashing import mix64
-    base = mix64((seed ^ tag) & ((1 << 64) - 1))
-    out = torch.empty(n, dtype=torch.int64, device=device)
-    step = 1 << 26
-    for lo in range(0, n, step):
-        m = min(step, n - lo)
-        x = torch.arange(lo, lo + m, dtype=torch.int64, device=device) + np.int64(np.uint64(base).view(np.int64))
-        # SplitMix64 finalizer in int64 arithmetic (wrapping), logical shifts via masks
-        def lsr(v, s):
-            return (v >> s) & ((1 << (64 - s)) - 1)
-        x = x ^ lsr(x, 30)
-        x = x * np.int64(np.uint64(0xBF58476D1CE4E5B9).view(np.int64))
-        x = x ^ lsr(x, 27)
-        x = x * np.int64(np.uint64(0x94D049BB133111EB).view(np.int64))
-        x = x ^ lsr(x, 31)
-        out[lo:lo + m] = x
-    return out
+    """Same keys as counter_stream, generated on the device by the
+    fk_counter_stream kernel (setup, not timed)."""
+    from paper_2212_09005_b200.workloads import counter_stream_device
+    return counter_stream_device(seed, tag, n, device)
 
 
 def random_sector_ceiling(torch, filt, stream, reps=3):
@@ -429,10 +414,24 @@ def _workload_setup(args, rank, world, dev, torch):
                 "64-bit keys, one insert_batch to %.2f load + pos/neg query_batch + delete_batch"
                 % (log_slots, log_slots - 7, args.load))
         return filt, ops, {"keys": keys, "negs": negs}, desc, ("bulk_tcf", log_slots, args.load)
-    # GQF, C2: duplicate-heavy ur_count keys (counts U{1..100}), naive bulk insert
     from paper_2212_09005_b200 import Gqf
     from paper_2212_09005_b200.sharding import ShardedGqf
     from paper_2212_09005_b200.workloads import WorkloadSpec, gen_keys
+    if args.workload == "gqf_kmer":
+        # C4: Zipfian k-mer-like counting at load factor args.load
+        q = args.log_slots if args.log_slots_set else 28
+        w = kmer_zipf_workload(torch, q, args.load, seed, dev)
+        filt = ShardedGqf(q=q + (world.bit_length() - 1)) if world > 1 else Gqf(q=q)
+        x = {"occ": w["occ"], "uniq": w["uniq"]}
+        ops = [("bulk_insert", lambda d: filt.bulk_insert(d["occ"]), w["n_occ"]),
+               ("count", lambda d: filt.count_many(d["uniq"]), w["n_distinct"]),
+               ("bulk_delete", lambda d: filt.bulk_delete(d["uniq"]), w["n_distinct"])]
+        desc = ("C4: GQF q=%d r=8 per GPU, k-mer-like keys: %d distinct with Zipf(%.1f) multiplicities on "
+                "[1, %d] (%d occurrences, shuffled), sized for load factor %.2f; naive bulk_insert of every "
+                "occurrence + count_many(distinct) + bulk_delete(distinct, all copies)"
+                % (q, w["n_distinct"], w["s"], w["cmax"], w["n_occ"], args.load))
+        return filt, ops, x, desc, ("gqf_kmer", q, args.load)
+    # GQF, C2: duplicate-heavy ur_count keys (counts U{1..100}), naive bulk insert
     q = args.log_slots if args.log_slots_set else 22
     occ = gen_keys(WorkloadSpec("ur_count", n=int(args.load * (1 << q)) // 4, seed=seed))
     uniq = np.unique(occ)
@@ -444,6 +443,65 @@ def _workload_setup(args, rank, world, dev, torch):
     desc = ("C2: GQF q=%d r=8 per GPU, ur_count keys (%d distinct x U{1..100} = %d occurrences), naive bulk_insert "
             "of every occurrence + count_many(distinct) + bulk_delete(distinct, all copies)" % (q, len(uniq), len(occ)))
     return filt, ops, x, desc, ("gqf", q, args.load)
+
+
+def _expected_group_len(counts, r, rng):
+    """Mean slots per distinct fingerprint under the count-group codec
+    (fk/countgroups.py:28-52) for uniformly random remainders."""
+    rem = rng.integers(0, 1 << r, len(counts))
+    c = counts.astype(np.int64)
+    base = (1 << r) - 1
+    v = np.where(rem > 0, (c - 2) // np.maximum(rem, 1), 0)
+    nd = np.zeros_like(v)
+    t = v.copy()
+    while (t > 0).any():
+        nd += t > 0
+        t //= base
+    ln = np.where((rem == 0) | (c <= 2), c, 3 + nd)
+    return float(ln.mean())
+
+
+def _kmer_counts(q, alpha, seed, s, cmax, r):
+    from paper_2212_09005_b200.workloads import zipf_bounded
+    rng = np.random.default_rng(0x5EED0000 + seed)
+    mean_len = _expected_group_len(zipf_bounded(rng, s, cmax, 1 << 20), r, rng)
+    d = max(1, int(alpha * (1 << q) / mean_len))
+    return zipf_bounded(rng, s, cmax, d), mean_len
+
+
+def kmer_zipf_host(q, alpha, seed, s=1.5, cmax=100, r=8):
+    """Host twin of kmer_zipf_workload (same distinct keys and multiplicities;
+    host shuffle) for the CPU baseline sample."""
+    from paper_2212_09005_b200.workloads import TAG_BASES
+    counts, _ = _kmer_counts(q, alpha, seed, s, cmax, r)
+    uniq = counter_stream(seed, TAG_BASES, len(counts))
+    occ = np.repeat(uniq, counts)
+    np.random.default_rng(seed).shuffle(occ)
+    return occ, uniq
+
+
+def kmer_zipf_workload(torch, q, alpha, seed, dev, s=1.5, cmax=100, r=8):
+    """C4 keys (BASELINE.json configs[3]): a k-mer-count spectrum -- D
+    distinct uniform 64-bit keys (counter_stream, TAG_BASES) whose
+    multiplicities are bounded Zipf(s) on [1, cmax] drawn with the
+    reference's own rejection-inversion sampler (fk/workloads.py:81-118), each
+    key repeated that many times and the stream shuffled (the structure of
+    the reference's ur_count, fk/workloads.py:66-71, with Zipfian instead of
+    uniform counts).  D is sized so the canonical table fills alpha * 2^q
+    slots (plain Zipf ranks leave the table nearly empty).
+    The multiplicities are host numpy draws; keys, repetition and shuffle are
+    generated on the device (setup, not timed)."""
+    from paper_2212_09005_b200.workloads import TAG_BASES
+    counts, mean_len = _kmer_counts(q, alpha, seed, s, cmax, r)
+    d = len(counts)
+    uniq = device_keys(torch, seed, TAG_BASES, d, dev)
+    cnt = torch.from_numpy(counts).to(dev)
+    occ = torch.repeat_interleave(uniq, cnt)
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+    occ = occ[torch.randperm(occ.numel(), device=dev, generator=g)]
+    return {"occ": occ, "uniq": uniq, "counts": cnt, "n_occ": int(occ.numel()), "n_distinct": d,
+            "s": s, "cmax": cmax, "mean_slots_per_key": mean_len}
 
 
 def run_workload(args, rank, world, local_rank):
@@ -542,6 +600,19 @@ def cpu_baseline_workload(key):
         dt = time.perf_counter() - t
         ops = 4 * n
         what = "bulk TCF 2^%d, insert_batch+2x query_batch+delete_batch, workers=%d" % (log_slots, threads)
+    elif kind == "gqf_kmer":
+        # bounded sample: the same spectrum and load factor on a q=22 table
+        qs = min(log_slots, 22)
+        occ, uniq = kmer_zipf_host(qs, load, 1)
+        f = ref_model.RefGqf(qs)
+        t = time.perf_counter()
+        f.bulk_insert(occ, workers=threads)
+        f.count_many(uniq, threads)
+        f.bulk_delete(uniq, workers=threads)
+        dt = time.perf_counter() - t
+        ops = len(occ) + 2 * len(uniq)
+        what = ("GQF q=%d (scaled from q=%d) k-mer Zipf spectrum at load %.2f, naive bulk_insert + count_many + "
+                "bulk_delete, workers=%d" % (qs, log_slots, load, threads))
     else:
         from paper_2212_09005_b200.workloads import WorkloadSpec, gen_keys
         occ = gen_keys(WorkloadSpec("ur_count", n=int(load * (1 << log_slots)) // 4, seed=1))
@@ -644,7 +715,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["tcf", "bulk_tcf", "gqf"], default="tcf")
+    ap.add_argument("--workload", choices=["tcf", "bulk_tcf", "gqf", "gqf_kmer"], default="tcf")
     ap.add_argument("--log-slots", type=int, default=None)
     ap.add_argument("--load", type=float, default=0.9)
     ap.add_argument("--group-width", type=int, default=1)

@@ -82,6 +82,12 @@ int fk_hash_streams(const uint64_t *keys, int64_t n, uint64_t seed, int bits, ui
 int fk_sector_gather(const void *table, int64_t table_bytes, int64_t n, uint64_t salt, uint32_t *sink,
                      void *stream);
 
+/* Device key generation: out[i] = mix64(mix64(seed ^ tag) + start + i),
+ * bit-identical to workloads.counter_stream (fk/workloads.py:23-26) and
+ * therefore to the reference CLI's uniform and negative-query key streams
+ * (TAG_UNIFORM / TAG_FPR, fk/workloads.py:61-64, :205-208). */
+int fk_counter_stream(uint64_t seed, uint64_t tag, uint64_t start, int64_t n, uint64_t *out, void *stream);
+
 /* Exact x % d on device through the fast-mod path (tests only). */
 int fk_fastmod_check(const uint64_t *x, int64_t n, uint64_t d, uint64_t *out, void *stream);
 

@@ -38,6 +38,26 @@ __global__ void __launch_bounds__(256) k_sector_gather(const uint32_t *__restric
   if (acc == 0x9E3779B9u) sink[blockIdx.x & 31] = acc;  // keeps the loads live
 }
 
+// counter_stream (workloads.py:23-26): mix64(mix64(seed ^ tag) + i) for
+// i in [start, start + n) -- the uniform key generator, exactly distinct.
+// Two keys per thread as one 128-bit store.
+__global__ void __launch_bounds__(256) k_counter_stream(uint64_t base, int64_t n, uint64_t *__restrict__ out) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; 2 * p < n; p += stride) {
+    int64_t i = 2 * p;
+    uint64_t a = mix64(base + (uint64_t)i);
+    if (i + 1 < n && (((uintptr_t)(out + i)) & 15) == 0) {
+      ulonglong2 v;
+      v.x = a;
+      v.y = mix64(base + (uint64_t)i + 1);
+      *reinterpret_cast<ulonglong2 *>(out + i) = v;
+    } else {
+      out[i] = a;
+      if (i + 1 < n) out[i + 1] = mix64(base + (uint64_t)i + 1);
+    }
+  }
+}
+
 }  // namespace fk
 
 using namespace fk;
@@ -80,6 +100,18 @@ int fk_hash_streams(const uint64_t *keys, int64_t n, uint64_t seed, int bits, ui
   if (grid > num_sms() * 16) grid = num_sms() * 16;
   k_hash_streams<<<grid, 256, 0, (cudaStream_t)stream>>>(keys, n, seed, m, nb, make_fastmod(nb ? nb : 1), bsize,
                                                          make_fastmod(bsize ? bsize : 1), out5);
+  FK_CHECK_LAUNCH();
+  return 0;
+}
+
+int fk_counter_stream(uint64_t seed, uint64_t tag, uint64_t start, int64_t n, uint64_t *out, void *stream) {
+  if (n < 0 || (n && !out)) return FK_E_ARG;
+  if (n == 0) return 0;
+  int64_t pairs = (n + 1) / 2;
+  int64_t blocks = (pairs + 255) / 256;
+  int cap = num_sms() * 8;
+  k_counter_stream<<<(int)(blocks < cap ? blocks : cap), 256, 0, (cudaStream_t)stream>>>(mix64(seed ^ tag) + start, n,
+                                                                                      out);
   FK_CHECK_LAUNCH();
   return 0;
 }

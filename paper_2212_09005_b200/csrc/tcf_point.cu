@@ -50,8 +50,26 @@ static int run(const fk_tcf_geom *g, int op, const TcfDev &P, const TcfCall &c, 
   }
 }
 
-static int64_t ord_window(int64_t n) {
-  int64_t w = 1 << 18;  // keys introduced per round (tunable: FK_ORD_WINDOW)
+// Reservation granularity: 2^rs blocks per word, keeping the word array at
+// <= 2^22 words (16 MiB, L2-resident next to the streamed keys); measured
+// best at C3 (nb = 2^24 -> rs = 2).  Tunable: FK_ORD_RES_SHIFT.
+static int ord_res_shift(int64_t nb) {
+  int rs = 0;
+  while ((nb >> rs) > (1LL << 22)) rs++;
+  if (const char *e = getenv("FK_ORD_RES_SHIFT")) rs = atoi(e);
+  return rs < 0 ? 0 : (rs > 16 ? 16 : rs);
+}
+
+// Keys introduced per round, as a fraction of the reservation words: 1/4 up
+// to 2^18 words, 1/8 up to 2^20, else 1/16, capped at 2^18 (measured on the
+// B200, profiles/r1c_ord_tune.jsonl: small tables are bound by the fixed
+// per-round cost of ~9-12 us, so a wide window wins despite more lost bids;
+// C3 (2^22 words) is best at 2^18).
+// Tunable: FK_ORD_WINDOW.
+static int64_t ord_window(int64_t nb, int64_t n) {
+  int64_t ng = nb >> ord_res_shift(nb);
+  int64_t w = ng <= (1 << 18) ? ng / 4 : (ng <= (1 << 20) ? ng / 8 : ng / 16);
+  w = w < 4096 ? 4096 : (w > (1 << 18) ? (1 << 18) : w);
   if (const char *e = getenv("FK_ORD_WINDOW")) {
     long long v = atoll(e);
     if (v > 0) w = v;
@@ -59,10 +77,9 @@ static int64_t ord_window(int64_t n) {
   return w < n ? w : (n < 1 ? 1 : n);
 }
 
-static int ord_res_shift() {
-  int rs = 2;  // blocks per reservation word = 2^rs (tunable: FK_ORD_RES_SHIFT)
-  if (const char *e = getenv("FK_ORD_RES_SHIFT")) rs = atoi(e);
-  return rs < 0 ? 0 : (rs > 16 ? 16 : rs);
+static int env_int(const char *name, int dflt) {
+  const char *e = getenv(name);
+  return e ? atoi(e) : dflt;
 }
 
 static int ord_hints() {
@@ -75,8 +92,8 @@ static size_t ord_ws_layout(const fk_tcf_geom *g, int64_t n, size_t *off) {
   size_t a = 0;
   auto take = [&](size_t bytes) { size_t o = a; a += (bytes + 255) & ~(size_t)255; return o; };
   int64_t cap = n < 1 ? 1 : n;
-  int64_t w = ord_window(n);
-  off[0] = take((size_t)((g->num_blocks >> ord_res_shift()) + 1) * 4);
+  int64_t w = ord_window(g->num_blocks, n);
+  off[0] = take((size_t)((g->num_blocks >> ord_res_shift(g->num_blocks)) + 1) * 4);
   off[1] = take((size_t)(g->backing_slots ? g->backing_slots : 1) * 4);
   off[2] = take((size_t)cap * 4);
   off[3] = take((size_t)cap);
@@ -100,9 +117,11 @@ static int prep_ordered(const fk_tcf_geom *g, int64_t n, void *ws, size_t ws_byt
   X->carry[0] = (uint32_t *)(b + off[5]);
   X->carry[1] = (uint32_t *)(b + off[6]);
   X->defer_cap = n < 1 ? 1 : n;
-  X->window = ord_window(n);
-  X->res_shift = ord_res_shift();
+  X->window = ord_window(g->num_blocks, n);
+  X->res_shift = ord_res_shift(g->num_blocks);
   X->hints = ord_hints();
+  // fewer grid-barrier participants when a round holds few keys (measured)
+  X->ctas_per_sm = env_int("FK_ORD_CTAS_PER_SM", g->num_blocks <= (1 << 16) ? 1 : (g->num_blocks <= (1 << 20) ? 2 : 0));
   FK_TRY(cudaMemsetAsync(X->res, 0xFF, (size_t)((g->num_blocks >> X->res_shift) + 1) * 4, st));
   FK_TRY(cudaMemsetAsync(X->bres, 0xFF, (size_t)(g->backing_slots ? g->backing_slots : 1) * 4, st));
   FK_TRY(cudaMemsetAsync(X->ctl, 0, 64, st));

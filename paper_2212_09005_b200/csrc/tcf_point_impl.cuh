@@ -356,11 +356,13 @@ struct OrdScratch {
   uint32_t *carry[2];   // keys carried to the next round (double-buffered)
   uint32_t *defer_idx;  // input indices deferred to the backing phase (unordered)
   uint8_t *defer_pend;
-  unsigned int *ctl;    // [0..1] carry counts, [2] defer count, [3..4] backing-phase round flags
+  unsigned int *ctl;    // [0..1] carry counts, [2] defer count, [3..4] backing-phase round flags,
+                        // [5] main rounds, [6] backing rounds, [7] keys carried (sum over rounds)
   int64_t defer_cap;
   int64_t window;       // keys introduced per round
   int res_shift;        // reservation granularity: 2^res_shift blocks per word
   int hints;            // 1: L2 evict_last on reservation words, evict_first on streams
+  int ctas_per_sm;      // 0: occupancy limit; else cap (fewer grid-barrier participants)
 };
 
 // CTA-wide OR of a predicate (all threads of the CTA must call).
@@ -471,34 +473,38 @@ __global__ void __launch_bounds__(256, 4)
     uint32_t *cout = X.carry[cur ^ 1];
 
     // ---- reserve --------------------------------------------------------
-    for (int64_t base = tid; base < total; base += tiles * KB) {
-      uint32_t idx[KB], b1[KB], b2[KB];
-      bool ok[KB];
+    // One chunk of KB keys per tile (the host caps the window at tiles*KB):
+    // the key's blocks and tag stay in registers for the commit pass.
+    uint32_t idx[KB], b1[KB], b2[KB];
+    uint64_t tg[KB];
+    bool ok[KB], hold[KB];
 #pragma unroll
-      for (int j = 0; j < KB; j++) {
-        int64_t e = base + (int64_t)j * tiles;
-        ok[j] = e < total;
-        idx[j] = ok[j] ? (e < nc ? __ldcg(cin + e) : (uint32_t)(F + e - nc)) : 0u;
-      }
+    for (int j = 0; j < KB; j++) {
+      int64_t e = tid + (int64_t)j * tiles;
+      ok[j] = e < total;
+      idx[j] = ok[j] ? (e < nc ? __ldcg(cin + e) : (uint32_t)(F + e - nc)) : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < KB; j++) {
+      b1[j] = b2[j] = 0;
+      tg[j] = 0;
+      if (!ok[j]) continue;
+      KeyInfo ki = key_info(P, X.hints ? ld_stream_u64(keys + idx[j], pol_stream) : keys[idx[j]]);
+      b1[j] = (uint32_t)ki.b1;
+      b2[j] = (uint32_t)ki.b2;
+      tg[j] = ki.tag;
+    }
+    if (t.lane == 0) {
 #pragma unroll
       for (int j = 0; j < KB; j++) {
         if (!ok[j]) continue;
-        KeyInfo ki = key_info(P, X.hints ? ld_stream_u64(keys + idx[j], pol_stream) : keys[idx[j]]);
-        b1[j] = (uint32_t)ki.b1;
-        b2[j] = (uint32_t)ki.b2;
-      }
-      if (t.lane == 0) {
-#pragma unroll
-        for (int j = 0; j < KB; j++) {
-          if (!ok[j]) continue;
-          uint32_t g1 = b1[j] >> X.res_shift, g2 = b2[j] >> X.res_shift;
-          if (X.hints) {
-            red_min_u32(&X.res[g1], idx[j], pol_keep);
-            if (g2 != g1) red_min_u32(&X.res[g2], idx[j], pol_keep);
-          } else {
-            atomicMin(&X.res[g1], idx[j]);
-            if (g2 != g1) atomicMin(&X.res[g2], idx[j]);
-          }
+        uint32_t g1 = b1[j] >> X.res_shift, g2 = b2[j] >> X.res_shift;
+        if (X.hints) {
+          red_min_u32(&X.res[g1], idx[j], pol_keep);
+          if (g2 != g1) red_min_u32(&X.res[g2], idx[j], pol_keep);
+        } else {
+          atomicMin(&X.res[g1], idx[j]);
+          if (g2 != g1) atomicMin(&X.res[g2], idx[j]);
         }
       }
     }
@@ -506,26 +512,7 @@ __global__ void __launch_bounds__(256, 4)
 
     // ---- commit ---------------------------------------------------------
     if (blockIdx.x == 0 && threadIdx.x == 0) X.ctl[cur] = 0;  // list `cur` is consumed this round
-    for (int64_t base = tid;; base += tiles * KB) {
-      // warp-uniform trip count: lanes past the end still join the shuffles
-      if (!__any_sync(0xFFFFFFFFu, base < total)) break;
-      uint32_t idx[KB], b1[KB], b2[KB];
-      uint64_t word[KB];
-      bool ok[KB], hold[KB];
-#pragma unroll
-      for (int j = 0; j < KB; j++) {
-        int64_t e = base + (int64_t)j * tiles;
-        ok[j] = e < total;
-        idx[j] = ok[j] ? (e < nc ? __ldcg(cin + e) : (uint32_t)(F + e - nc)) : 0u;
-      }
-#pragma unroll
-      for (int j = 0; j < KB; j++) {
-        if (!ok[j]) continue;
-        KeyInfo ki = key_info(P, X.hints ? ld_stream_u64(keys + idx[j], pol_stream) : keys[idx[j]]);
-        b1[j] = (uint32_t)ki.b1;
-        b2[j] = (uint32_t)ki.b2;
-        word[j] = OP == 0 ? ((P.f >= 64 ? 0 : ((values ? values[idx[j]] : 0) << P.f)) | ki.tag) : ki.tag;
-      }
+    {
 #pragma unroll
       for (int j = 0; j < KB; j++)
         hold[j] = ok[j] && (X.hints ? ld_cg_u32(&X.res[b1[j] >> X.res_shift], pol_keep)
@@ -537,7 +524,7 @@ __global__ void __launch_bounds__(256, 4)
 #pragma unroll
       for (int j = 0; j < KB; j++)
         if (hold[j]) c1[j].template load<true>(blocks + (uint64_t)b1[j] * P.B, P.B, t.lane);
-      // carry the losers: one warp-aggregated atomicAdd per pass
+      // carry the losers: one warp-aggregated atomicAdd (every lane joins)
       {
         unsigned mine = 0;
 #pragma unroll
@@ -560,17 +547,18 @@ __global__ void __launch_bounds__(256, 4)
       }
 #pragma unroll
       for (int j = 0; j < KB; j++) {
-        if (!ok[j] || !hold[j]) continue;
+        if (!hold[j]) continue;
         bool defer;
         if (OP == 0) {
-          uint8_t code = commit_insert<S, G, BF>(P, t, b1[j], b2[j], word[j], c1[j]);
+          uint64_t word = (P.f >= 64 || !values ? 0 : (values[idx[j]] << P.f)) | tg[j];
+          uint8_t code = commit_insert<S, G, BF>(P, t, b1[j], b2[j], word, c1[j]);
           defer = code == 4;
           if (!defer && t.lane == 0) {
             out[idx[j]] = code;
             n_a++;
           }
         } else {
-          int done = commit_delete<S, G, BF>(P, t, b1[j], b2[j], word[j], c1[j]);
+          int done = commit_delete<S, G, BF>(P, t, b1[j], b2[j], tg[j], c1[j]);
           defer = !done && P.bsize;
           if (!defer && t.lane == 0) {
             out[idx[j]] = done ? 1 : 0;
@@ -601,8 +589,11 @@ __global__ void __launch_bounds__(256, 4)
     cur ^= 1;
     F = Fend;
     round++;
+    if (blockIdx.x == 0 && threadIdx.x == 0) X.ctl[7] += (unsigned)nc;
     if (F >= n && nc == 0) break;
   }
+  if (blockIdx.x == 0 && threadIdx.x == 0) X.ctl[5] = round;
+  const unsigned main_rounds = round;
 
   // ---- backing phase: deferred keys in input-index order -------------------
   grid.sync();
@@ -693,6 +684,7 @@ __global__ void __launch_bounds__(256, 4)
       if (cnt == 0) break;
     }
   }
+  if (blockIdx.x == 0 && threadIdx.x == 0) X.ctl[6] = round - main_rounds;
   if (t.lane == 0) {
     if (OP == 0) {
       if (n_a) atomicAdd((unsigned long long *)&counters[0], (unsigned long long)n_a);
@@ -715,7 +707,12 @@ static int launch_ordered(const TcfDev &P, const uint64_t *keys, const uint64_t 
   int per_sm = 0;
   FK_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
   if (per_sm < 1) return FK_E_ARG;
+  if (X.ctas_per_sm > 0 && X.ctas_per_sm < per_sm) per_sm = X.ctas_per_sm;
   int grid = per_sm * num_sms();
+  // one chunk of kOrdKB keys per tile and round (the kernel keeps them in
+  // registers between its reserve and commit passes)
+  int64_t cap = (int64_t)grid * (256 / G) * kOrdKB;
+  if (X.window > cap) X.window = cap;
   void *args[] = {(void *)&P, (void *)&keys, (void *)&values, (void *)&n, (void *)&out, (void *)&counters, (void *)&X};
   FK_TRY(cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(256), args, 0, st));
   return 0;

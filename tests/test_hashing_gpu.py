@@ -63,3 +63,24 @@ def test_fastmod_exact(d):
     _lib.check(lib.fk_fastmod_check(_lib.dptr(xt), len(x), d, _lib.dptr(out), None), "fastmod")
     torch.cuda.synchronize()
     assert np.array_equal(out.cpu().numpy().view(np.uint64), x % np.uint64(d))
+
+
+def test_counter_stream_device_matches_host():
+    """fk_counter_stream == workloads.counter_stream (fk/workloads.py:23-26),
+    including odd lengths, a start offset and a wrap past 2^64."""
+    import torch
+    from paper_2212_09005_b200 import _lib
+    from paper_2212_09005_b200.workloads import (TAG_FPR, TAG_UNIFORM, counter_stream,
+                                                 counter_stream_device)
+    for seed, tag, n in ((1, TAG_UNIFORM, 1), (2, TAG_FPR, 7), (0, TAG_UNIFORM, 1_000_003),
+                         (12345, 0xFFFFFFFFFFFFFFFF, 4097)):
+        got = counter_stream_device(seed, tag, n).cpu().numpy().view(np.uint64)
+        assert np.array_equal(got, counter_stream(seed, tag, n))
+    # start offset = a window of the full stream; odd (8-byte aligned) output
+    full = counter_stream(5, TAG_UNIFORM, 5000)
+    out = torch.zeros(4001, dtype=torch.int64, device="cuda")
+    lib = _lib.load()
+    _lib.check(lib.fk_counter_stream(5, TAG_UNIFORM, 999, 4000, ctypes.c_void_p(out.data_ptr() + 8), None), "cs")
+    torch.cuda.synchronize()
+    assert np.array_equal(out[1:].cpu().numpy().view(np.uint64), full[999:4999])
+    assert int(out[0]) == 0
