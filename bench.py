@@ -60,8 +60,8 @@ BYTES_PER_OP = {
 SECTORS_PER_OP = {"insert": 1.260, "query_pos": 1.1437, "query_neg": 2.0, "delete": 1.1437}
 
 KERNEL_OF = {
-    ("ordered", "insert"): "k_tcf_ordered<u16,G=1,B=16,KB=4,OP=insert>",
-    ("ordered", "delete"): "k_tcf_ordered<u16,G=1,B=16,KB=4,OP=delete>",
+    ("ordered", "insert"): "k_tcf_ordered<u16,G=1,B=16,KB=2,OP=insert>",
+    ("ordered", "delete"): "k_tcf_ordered<u16,G=1,B=16,KB=2,OP=delete>",
     ("concurrent", "insert"): "k_tcf_insert_cas<u16,G=1,B=16>",
     ("concurrent", "delete"): "k_tcf_delete_cas<u16,G=1,B=16>",
 }

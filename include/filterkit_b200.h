@@ -212,6 +212,19 @@ int fk_gqf_count(const fk_gqf_geom *g, const fk_gqf_tables *t, const uint64_t *k
 int fk_gqf_find_run(const fk_gqf_geom *g, const fk_gqf_tables *t, const int64_t *quotients, int64_t n,
                     int64_t *se, void *stream);
 
+/* Structure validation on the device (replaces the host checks of
+ * Gqf.validate, gqf.py:430-492, which decode every run in Python), derived
+ * from the bit vectors alone by global rank/select.  Synchronous; out (HOST
+ * memory, 24 int64) gets: out[0] = bitmask of failed checks (1<<1 occupieds/
+ * runends counts differ, 1<<2 quotient beyond logical table, 1<<3 run past
+ * physical table, 1<<5 negative run, 1<<7 region hard bound crossed, 1<<8
+ * offset != derived, 1<<11 undecodable run, 1<<12 unsorted groups),
+ * out[8 + c] = first offending quotient (region for c = 8), out[1] = used
+ * slots, out[2] = decoded total, out[3] = decoded distinct, out[4] = non-zero
+ * slots inside runs, out[5] = non-zero slots in the table.  The caller
+ * compares out[1..3] with _stats and out[4] with out[5]. */
+int fk_gqf_validate(const fk_gqf_geom *g, const fk_gqf_tables *t, int64_t *out, void *stream);
+
 /* Rebuild the derived spill index from occupieds/runends (after the host
  * wrote the image); asynchronous. */
 int fk_gqf_rebuild_index(const fk_gqf_geom *g, const fk_gqf_tables *t, void *stream);

@@ -681,4 +681,104 @@ __global__ void k_region_bounds(const uint64_t *__restrict__ fps_s, int64_t n, i
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Device-side structure validation (Gqf.validate, gqf.py:430-492), derived
+// from the bit vectors alone (global rank/select; the spill index is not
+// trusted).  Each failed check sets its code's bit in v[0] and atomicMin's
+// the first offending quotient / region / slot into v[8 + code]; v[1..4]
+// accumulate used slots, decoded total, decoded distinct, non-zero slots
+// inside runs; v[5] = non-zero slots anywhere.
+// ---------------------------------------------------------------------------
+enum GqfCheck {
+  kVRankMismatch = 1, kVQuotBeyond = 2, kVRunPastPhys = 3, kVNegativeRun = 5, kVHardBound = 7,
+  kVOffset = 8, kVUndecodable = 11, kVUnsorted = 12
+};
+constexpr int kValidateWords = 8 + 16;
+
+__device__ __forceinline__ void vfail(int64_t *v, int code, int64_t pos) {
+  atomicOr((unsigned long long *)&v[0], 1ull << code);
+  atomicMin((long long *)&v[8 + code], (long long)pos);
+}
+
+// k-th (0-based) set bit of bv given the exclusive per-word prefix ranks.
+__device__ __forceinline__ int64_t select_global(const uint64_t *bv, const int64_t *rank, int64_t nw, int64_t k) {
+  int64_t lo = 0, hi = nw;  // last word whose rank <= k
+  while (hi - lo > 1) {
+    int64_t mid = (lo + hi) >> 1;
+    if (rank[mid] <= k) lo = mid; else hi = mid;
+  }
+  uint64_t w = bv[lo];
+  for (int64_t c = k - rank[lo]; c > 0; c--) w &= w - 1;
+  return (lo << 6) + __ffsll((long long)w) - 1;
+}
+
+template <typename S>
+__global__ void k_gqf_validate_runs(GqfDev T, int64_t nw, const int64_t *__restrict__ ro,
+                                    const int64_t *__restrict__ rr, int64_t *__restrict__ v) {
+  const S *slots = reinterpret_cast<const S *>(T.slots);
+  const int64_t logical = 1LL << T.q;
+  unsigned long long used = 0, total = 0, distinct = 0, nz = 0;
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t ow = T.occ[w];
+    if (!ow) continue;
+    int64_t i = ro[w];  // rank of this word's first occupied quotient
+    int64_t prev = i ? select_global(T.run, rr, nw, i - 1) : -1;
+    while (ow) {
+      int64_t x = (w << 6) + __ffsll((long long)ow) - 1;
+      ow &= ow - 1;
+      int64_t end = select_after_dev(T.run, prev, 1, T.phys);
+      if (end < 0) { vfail(v, kVRankMismatch, x); return; }
+      int64_t st = x > prev + 1 ? x : prev + 1;
+      if (x >= logical) vfail(v, kVQuotBeyond, x);
+      if (end >= T.phys) vfail(v, kVRunPastPhys, x);
+      if (st > end) { vfail(v, kVNegativeRun, x); prev = end; continue; }
+      if ((end >> kRegionBits) > (x >> kRegionBits) + 1) vfail(v, kVHardBound, x);
+      used += (unsigned long long)(end - st + 1);
+      int64_t lastrem = -1;
+      for (int64_t p = st; p <= end;) {
+        uint64_t h, cnt;
+        int64_t nx;
+        if (!parse_group_dev<S>(slots, p, end, T.r, &h, &cnt, &nx)) { vfail(v, kVUndecodable, x); break; }
+        if ((int64_t)h <= lastrem) vfail(v, kVUnsorted, x);
+        lastrem = (int64_t)h;
+        total += cnt;
+        distinct++;
+        for (int64_t j = p; j < nx; j++) nz += slots[j] != 0;
+        p = nx;
+      }
+      prev = end;
+    }
+  }
+  if (used) atomicAdd((unsigned long long *)&v[1], used);
+  if (total) atomicAdd((unsigned long long *)&v[2], total);
+  if (distinct) atomicAdd((unsigned long long *)&v[3], distinct);
+  if (nz) atomicAdd((unsigned long long *)&v[4], nz);
+}
+
+// derived spill of every region (gqf.py:452-455) against _offsets
+__global__ void k_gqf_validate_offsets(GqfDev T, int64_t nw, const int64_t *__restrict__ ro,
+                                       const int64_t *__restrict__ rr, int64_t *__restrict__ v) {
+  for (int64_t h = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; h < T.nregions;
+       h += (int64_t)gridDim.x * blockDim.x) {
+    int64_t b = h << kRegionBits;
+    int64_t k = (b >> 6) < nw ? ro[b >> 6] : ro[nw - 1] + __popcll(T.occ[nw - 1]);  // occupied quotients < b
+    int64_t derived = 0;
+    if (k > 0) {
+      int64_t e = select_global(T.run, rr, nw, k - 1);
+      derived = e - b + 1 > 0 ? e - b + 1 : 0;
+    }
+    if (derived != (int64_t)T.offs[h]) vfail(v, kVOffset, h);
+  }
+}
+
+template <typename S>
+__global__ void k_count_nonzero(const S *__restrict__ slots, int64_t n, int64_t *__restrict__ v) {
+  unsigned long long c = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    c += slots[i] != 0;
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd((unsigned long long *)&v[5], c);
+}
+
 }  // namespace fk

@@ -27,6 +27,7 @@ namespace fk {
 
 constexpr uint32_t kNoRes = 0xFFFFFFFFu;
 
+
 struct TcfDev {
   void *blocks;
   void *backing;
@@ -206,6 +207,91 @@ __global__ void __launch_bounds__(256) k_tcf_query(TcfDev P, const uint64_t *__r
 }
 
 // ---------------------------------------------------------------------------
+// Register-resident fast path for the benchmarked geometry (16 x u16 slots =
+// one 32-byte sector, G = 1): a block is 8 registers and every decision is a
+// 16-bit mask (bit s = slot s), so nothing is ever indexed dynamically and
+// the kernels keep no block state in local memory (the generic Chunk path
+// does, and a grid barrier's L1 invalidation makes that expensive).
+// ---------------------------------------------------------------------------
+template <typename S, int G, int BF>
+constexpr bool kFast16 = sizeof(S) == 2 && G == 1 && BF == 16;
+
+__device__ __forceinline__ uint32_t live16(const uint32_t (&r)[8]) {  // slot > TOMBSTONE
+  uint32_t m = 0;
+#pragma unroll
+  for (int i = 0; i < 8; i++) {
+    uint32_t g = __vcmpgtu2(r[i], 0x00010001u);
+    m |= ((g & 1u) | ((g >> 15) & 2u)) << (2 * i);
+  }
+  return m;
+}
+
+// live slots whose tag bits equal tag (tags are >= 2, so the live test only
+// matters when value bits sit above the tag)
+__device__ __forceinline__ uint32_t match16(const uint32_t (&r)[8], uint32_t tag, uint32_t fmask) {
+  const uint32_t pat = tag | (tag << 16), fm2 = fmask | (fmask << 16);
+  uint32_t m = 0;
+#pragma unroll
+  for (int i = 0; i < 8; i++) {
+    uint32_t g = __vcmpeq2(r[i] & fm2, pat) & __vcmpgtu2(r[i], 0x00010001u);
+    m |= ((g & 1u) | ((g >> 15) & 2u)) << (2 * i);
+  }
+  return m;
+}
+
+template <bool CGL>
+__device__ __forceinline__ void load16(const uint16_t *blk, uint32_t (&r)[8]) {
+  load_chunk<32, CGL>(blk, r);
+}
+
+// commit_insert on exclusively reserved blocks, mask form (same policy)
+__device__ __forceinline__ uint8_t commit_insert16(const TcfDev &P, uint32_t b1, uint32_t b2, uint16_t word,
+                                                   const uint32_t (&r1)[8]) {
+  uint16_t *blocks = reinterpret_cast<uint16_t *>(P.blocks);
+  uint16_t *blk1 = blocks + (uint64_t)b1 * 16, *blk2 = blocks + (uint64_t)b2 * 16;
+  uint32_t l1 = live16(r1);
+  int u1 = __popc(l1);
+  if (u1 < P.cut) {  // cut <= B, so a free slot exists
+    blk1[__ffs(~l1 & 0xFFFFu) - 1] = word;
+    return kPrimary;
+  }
+  uint32_t r2[8];
+  load16<true>(blk2, r2);
+  uint32_t l2 = live16(r2);
+  bool first1 = u1 <= __popc(l2);
+  uint32_t fa = ~(first1 ? l1 : l2) & 0xFFFFu, fb = ~(first1 ? l2 : l1) & 0xFFFFu;
+  if (fa) {
+    (first1 ? blk1 : blk2)[__ffs(fa) - 1] = word;
+    return (first1 || b1 == b2) ? kPrimary : kSecondary;
+  }
+  if (fb) {
+    (first1 ? blk2 : blk1)[__ffs(fb) - 1] = word;
+    return (!first1 || b1 == b2) ? kPrimary : kSecondary;
+  }
+  return 4;
+}
+
+__device__ __forceinline__ int commit_delete16(const TcfDev &P, uint32_t b1, uint32_t b2, uint32_t tag,
+                                               const uint32_t (&r1)[8]) {
+  uint16_t *blocks = reinterpret_cast<uint16_t *>(P.blocks);
+  const uint32_t fm = (uint32_t)(P.fmask & 0xFFFFu);
+  uint32_t m = match16(r1, tag, fm);
+  if (m) {
+    blocks[(uint64_t)b1 * 16 + __ffs(m) - 1] = 1;
+    return 1;
+  }
+  uint32_t r2[8];
+  load16<true>(blocks + (uint64_t)b2 * 16, r2);
+  m = match16(r2, tag, fm);
+  if (m) {
+    blocks[(uint64_t)b2 * 16 + __ffs(m) - 1] = 1;
+    return 1;
+  }
+  return 0;
+}
+
+
+// ---------------------------------------------------------------------------
 // concurrent (free-threaded CAS) insert / delete
 // ---------------------------------------------------------------------------
 
@@ -301,8 +387,26 @@ __global__ void __launch_bounds__(256)
   for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G; i < n; i += tiles) {
     KeyInfo k = key_info(P, keys[i]);
     bool done = false;
+    const bool fast = kFast16<S, G, BF> && P.f == 16;  // slot word == tag: the CAS expects the tag
+    if (fast) {
 #pragma unroll 1
-    for (int which = 0; which < 2 && !done; which++) {
+      for (int which = 0; which < 2 && !done; which++) {
+        uint16_t *blk = reinterpret_cast<uint16_t *>(blocks + (which ? k.b2 : k.b1) * (uint64_t)P.B);
+        uint32_t r[8];
+        load16<true>(blk, r);
+        uint32_t m = match16(r, (uint32_t)k.tag, (uint32_t)(P.fmask & 0xFFFFu));
+        while (m) {  // first live match, next match on a lost race (ck:328-339)
+          int j = __ffs(m) - 1;
+          m &= m - 1;
+          if (cas_slot<uint16_t>(blk + j, (uint16_t)k.tag, (uint16_t)1)) {
+            done = true;
+            break;
+          }
+        }
+      }
+    }
+#pragma unroll 1
+    for (int which = 0; which < 2 && !done && !fast; which++) {
       S *blk = blocks + (which ? k.b2 : k.b1) * (uint64_t)P.B;
       Chunk<S, G, BF> c;
       c.template load<true>(blk, P.B, t.lane);
@@ -363,6 +467,7 @@ struct OrdScratch {
   int res_shift;        // reservation granularity: 2^res_shift blocks per word
   int hints;            // 1: L2 evict_last on reservation words, evict_first on streams
   int ctas_per_sm;      // 0: occupancy limit; else cap (fewer grid-barrier participants)
+  int prefetch;         // 1: the reserve pass prefetches each key's b1 block into L2
 };
 
 // CTA-wide OR of a predicate (all threads of the CTA must call).
@@ -493,6 +598,10 @@ __global__ void __launch_bounds__(256, 4)
       b1[j] = (uint32_t)ki.b1;
       b2[j] = (uint32_t)ki.b2;
       tg[j] = ki.tag;
+      // the commit pass reads b1 after the barrier: start the DRAM fetch now
+      if (X.prefetch && t.lane == 0)
+        asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(reinterpret_cast<const S *>(P.blocks) +
+                                                                 (uint64_t)b1[j] * P.B));
     }
     if (t.lane == 0) {
 #pragma unroll
@@ -519,11 +628,18 @@ __global__ void __launch_bounds__(256, 4)
                                     : __ldcg(&X.res[b1[j] >> X.res_shift])) == idx[j] &&
                   (X.hints ? ld_cg_u32(&X.res[b2[j] >> X.res_shift], pol_keep)
                            : __ldcg(&X.res[b2[j] >> X.res_shift])) == idx[j];
-      Chunk<S, G, BF> c1[KB];
+      constexpr bool fast = kFast16<S, G, BF>;
+      constexpr int KC = fast ? 1 : KB;      // generic path: one Chunk per key
+      constexpr int KR = fast ? KB : 1;      // fast path: 8 registers per key
+      Chunk<S, G, BF> c1[KC];
+      uint32_t r1[KR][8];
       S *blocks = reinterpret_cast<S *>(P.blocks);
 #pragma unroll
-      for (int j = 0; j < KB; j++)
-        if (hold[j]) c1[j].template load<true>(blocks + (uint64_t)b1[j] * P.B, P.B, t.lane);
+      for (int j = 0; j < KB; j++) {
+        if (!hold[j]) continue;
+        if constexpr (fast) load16<true>(reinterpret_cast<uint16_t *>(blocks) + (uint64_t)b1[j] * 16, r1[j]);
+        else c1[j].template load<true>(blocks + (uint64_t)b1[j] * P.B, P.B, t.lane);
+      }
       // carry the losers: one warp-aggregated atomicAdd (every lane joins)
       {
         unsigned mine = 0;
@@ -551,14 +667,18 @@ __global__ void __launch_bounds__(256, 4)
         bool defer;
         if (OP == 0) {
           uint64_t word = (P.f >= 64 || !values ? 0 : (values[idx[j]] << P.f)) | tg[j];
-          uint8_t code = commit_insert<S, G, BF>(P, t, b1[j], b2[j], word, c1[j]);
+          uint8_t code;
+          if constexpr (fast) code = commit_insert16(P, b1[j], b2[j], (uint16_t)word, r1[j]);
+          else code = commit_insert<S, G, BF>(P, t, b1[j], b2[j], word, c1[j]);
           defer = code == 4;
           if (!defer && t.lane == 0) {
             out[idx[j]] = code;
             n_a++;
           }
         } else {
-          int done = commit_delete<S, G, BF>(P, t, b1[j], b2[j], tg[j], c1[j]);
+          int done;
+          if constexpr (fast) done = commit_delete16(P, b1[j], b2[j], (uint32_t)tg[j], r1[j]);
+          else done = commit_delete<S, G, BF>(P, t, b1[j], b2[j], tg[j], c1[j]);
           defer = !done && P.bsize;
           if (!defer && t.lane == 0) {
             out[idx[j]] = done ? 1 : 0;
@@ -698,20 +818,23 @@ __global__ void __launch_bounds__(256, 4)
 // Dispatch over (G, compile-time B) for one slot type -------------------------
 // BF=16 is the vectorised fast path for the default/benchmarked geometry
 // (B=16); BF=32 the CG-32 sweep point (B=32, u16); everything else BF=0.
-constexpr int kOrdKB = 4;  // items per thread per pass in the ordered kernel
+// keys per tile per round in the ordered kernel: 2 on the register-resident
+// G=1 path (4 spills at the 64-register cap of 4 CTAs/SM), 4 otherwise
+template <int G>
+constexpr int kOrdKB = G == 1 ? 2 : 4;
 
 template <typename S, int G, int BF, int OP>
 static int launch_ordered(const TcfDev &P, const uint64_t *keys, const uint64_t *values, int64_t n, uint8_t *out,
                           int64_t *counters, OrdScratch X, cudaStream_t st) {
-  auto kern = k_tcf_ordered<S, G, BF, kOrdKB, OP>;
+  auto kern = k_tcf_ordered<S, G, BF, kOrdKB<G>, OP>;
   int per_sm = 0;
   FK_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
   if (per_sm < 1) return FK_E_ARG;
   if (X.ctas_per_sm > 0 && X.ctas_per_sm < per_sm) per_sm = X.ctas_per_sm;
   int grid = per_sm * num_sms();
-  // one chunk of kOrdKB keys per tile and round (the kernel keeps them in
+  // one chunk of kOrdKB<G> keys per tile and round (the kernel keeps them in
   // registers between its reserve and commit passes)
-  int64_t cap = (int64_t)grid * (256 / G) * kOrdKB;
+  int64_t cap = (int64_t)grid * (256 / G) * kOrdKB<G>;
   if (X.window > cap) X.window = cap;
   void *args[] = {(void *)&P, (void *)&keys, (void *)&values, (void *)&n, (void *)&out, (void *)&counters, (void *)&X};
   FK_TRY(cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(256), args, 0, st));

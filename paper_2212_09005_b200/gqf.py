@@ -360,7 +360,52 @@ class Gqf:
                 "mean_cluster": float(lengths.mean())}
 
     def validate(self):
-        """Structural invariants against the global derivation (gqf.py:430-492)."""
+        """Structural invariants (gqf.py:430-492), checked on the device by
+        fk_gqf_validate (global rank/select over the bit vectors, every run
+        decoded in parallel).  On a violation, tables small enough to decode
+        on the host re-run the reference's host checks so the message names
+        the same first failure; larger ones report the device's first one."""
+        first = self._device_validate()
+        if first is None:
+            return
+        if self.params.physical_slots <= (1 << 22):
+            self._validate_host()
+        raise ValidationError(first)
+
+    _VCHECKS = [(1, "occupieds and runends set-bit counts differ"),
+                (2, "occupied quotient beyond logical table (quotient %d)"),
+                (3, "run extends past physical table (quotient %d)"),
+                (5, "run with negative length (quotient %d)"),
+                (7, "run crossed its region hard bound (quotient %d)"),
+                (8, "region %d offset != derived")]
+
+    def _device_validate(self):
+        """None if the table is valid, else the first failure's message."""
+        out = np.zeros(24, dtype=np.int64)
+        with self._op_lock:
+            self._sync_in()
+            rc = self._lib.fk_gqf_validate(ctypes.byref(self._geom), ctypes.byref(self._tables(self._cur)),
+                                           out.ctypes.data_as(ctypes.c_void_p), _lib.stream_ptr(self._torch))
+            _lib.check(rc, "gqf validate")
+        mask = int(out[0])
+        for code, msg in self._VCHECKS:
+            if mask >> code & 1:
+                return msg % int(out[8 + code]) if "%d" in msg else msg
+        if int(out[1]) != self.occupied_slots:
+            return "used slots %d != occupied counter %d" % (int(out[1]), self.occupied_slots)
+        if int(out[5]) != int(out[4]):
+            return "free slots hold residual data"
+        for code, msg in ((11, "run of quotient %d does not decode"), (12, "run of quotient %d has unsorted groups")):
+            if mask >> code & 1:
+                return msg % int(out[8 + code])
+        if int(out[2]) != self.total_items:
+            return "decoded total %d != items counter %d" % (int(out[2]), self.total_items)
+        if int(out[3]) != self.distinct_items:
+            return "decoded distinct %d != distinct counter %d" % (int(out[3]), self.distinct_items)
+        return None
+
+    def _validate_host(self):
+        """The reference's host-side checks over the mirrored image."""
         p = self.params
         phys = p.physical_slots
         quotients, starts, ends = self._derive_structure()

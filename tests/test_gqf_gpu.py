@@ -268,3 +268,64 @@ def test_shift_instrumentation():
     g = Gqf(q=13, r=8, seed=28)
     g.insert_many(np.random.default_rng(12).integers(0, 2 ** 50, 3000, dtype=np.uint64))
     assert g.shifted_slots > 0
+
+
+def _host_raises(g):
+    from paper_2212_09005_b200 import ValidationError
+    try:
+        g._validate_host()
+    except ValidationError:
+        return True
+    return False
+
+
+@pytest.mark.parametrize("r", [8, 16])
+def test_device_validate_agrees_with_host(r):
+    """fk_gqf_validate flags exactly the tables the reference's host checks
+    reject (gqf.py:430-492), over valid fills and a catalogue of corruptions."""
+    from paper_2212_09005_b200 import Gqf
+    rng = np.random.default_rng(11 + r)
+    g = Gqf(q=14, r=r, seed=5)
+    keys = rng.integers(0, 2 ** 40, 2500, dtype=np.uint64)
+    g.bulk_insert(keys, rng.integers(1, 300, 2500).astype(np.uint64))
+    assert g._device_validate() is None and not _host_raises(g)
+    base = {n: getattr(g, n).copy() for n in ("_slots", "_occupieds", "_runends", "_offsets", "_stats")}
+
+    def restore():
+        for n, a in base.items():
+            getattr(g, n)[:] = a
+
+    used = np.flatnonzero(g._slots)
+    corruptions = [
+        ("_slots", lambda a: a.__setitem__(int(np.flatnonzero(a == 0)[-1]), 7)),      # residual data
+        ("_slots", lambda a: a.__setitem__(int(used[len(used) // 2]), 0)),             # group damage
+        ("_slots", lambda a: a.__setitem__(int(used[len(used) // 3]), a[used[len(used) // 3]] ^ 0x5)),
+        ("_offsets", lambda a: a.__setitem__(1, a[1] + 1)),
+        ("_stats", lambda a: a.__setitem__(0, a[0] + 1)),
+        ("_stats", lambda a: a.__setitem__(1, a[1] - 1)),
+        ("_stats", lambda a: a.__setitem__(2, a[2] + 3)),
+        ("_runends", lambda a: a.__setitem__(3, a[3] ^ (1 << 17))),                    # count mismatch
+        ("_occupieds", lambda a: a.__setitem__(5, a[5] ^ (1 << 40))),
+    ]
+    for name, fn in corruptions:
+        fn(getattr(g, name))
+        host = _host_raises(g)
+        dev = g._device_validate()
+        assert host == (dev is not None), (name, dev)
+        restore()
+    assert g._device_validate() is None
+
+
+def test_device_validate_large_table():
+    """q=24 (16.8 M slots): validation runs on the device in well under a
+    second; the host decode loop would take minutes."""
+    import time
+    import torch
+    from paper_2212_09005_b200 import Gqf
+    g = Gqf(q=24, r=8)
+    keys = torch.randint(-2 ** 62, 2 ** 62, (6_000_000,), dtype=torch.int64, device="cuda")
+    g.bulk_insert(keys)
+    t = time.perf_counter()
+    g.validate()
+    assert time.perf_counter() - t < 5.0
+    assert g.total_items == 6_000_000
