@@ -143,6 +143,14 @@ class Tcf:
                                   dt.itemsize, p.cut_slots, p.probe_limit, p.tile_width,
                                   p.seed & ((1 << 64) - 1))
         self._op_lock = threading.Lock()
+        self._pipe = None  # HostPipeline, created on the first large host-side batch
+
+    def _pipe_wants(self, keys):
+        from ._pipeline import PIPE_CHUNK
+        if self._kind(keys) == "cuda":
+            return False
+        n = keys.numel() if isinstance(keys, self._torch.Tensor) else len(keys)
+        return n >= 2 * (self._pipe.chunk if self._pipe is not None else PIPE_CHUNK)
 
     @property
     def backend(self):
@@ -168,6 +176,55 @@ class Tcf:
         else:
             kind = "numpy"
         return _lib.to_device_u64(torch, keys, self._device), kind
+
+    def _kind(self, keys):
+        torch = self._torch
+        if isinstance(keys, torch.Tensor):
+            return "cuda" if keys.is_cuda else "host"
+        return "numpy"
+
+    def _pipelined(self, keys, op, out_dtype):
+        """Host-resident batch through the chunked H2D / kernel / D2H pipeline
+        (_pipeline.py); returns results in the caller's kind."""
+        torch = self._torch
+        from ._pipeline import HostPipeline
+        if self._pipe is None:
+            self._pipe = HostPipeline(torch, self._device)
+        kind = self._kind(keys)
+        if kind == "host":
+            hk = keys.reshape(-1)
+            hk = hk.view(torch.int64) if hk.dtype in (torch.int64, torch.uint64) else hk.to(torch.int64)
+        else:
+            hk = torch.from_numpy(np.ascontiguousarray(np.asarray(keys, dtype=np.uint64).reshape(-1))
+                                  .view(np.int64))
+        mode = _MODES[self.mode]
+        geom, lib = ctypes_byref(self._geom), self._lib
+        with self._op_lock:
+            self._t.before_device_op()
+            ws, wsb = self._workspace(min(hk.numel(), self._pipe.chunk), mode) if op != "query" else (None, 0)
+
+            def launch(din, dout):
+                k, o, m = din[0], dout[0], din[0].numel()
+                sp = _lib.stream_ptr(torch)
+                if op == "insert":
+                    rc = lib.fk_tcf_insert(geom, self._t.ptr("blocks"), self._t.ptr("backing"), _lib.dptr(k), 0,
+                                           None, m, _lib.dptr(o), _lib.dptr(self._counters_dev), mode,
+                                           _lib.dptr(ws), wsb, sp)
+                elif op == "delete":
+                    rc = lib.fk_tcf_delete(geom, self._t.ptr("blocks"), self._t.ptr("backing"), _lib.dptr(k), 0,
+                                           m, _lib.dptr(o), _lib.dptr(self._counters_dev), mode, _lib.dptr(ws),
+                                           wsb, sp)
+                else:
+                    rc = lib.fk_tcf_query(geom, self._t.ptr("blocks"), self._t.ptr("backing"), _lib.dptr(k), 0,
+                                          m, _lib.dptr(o), None, sp)
+                _lib.check(rc, "tcf " + op)
+
+            out, = self._pipe.run([hk], [out_dtype], launch)
+            if op != "query":
+                self._t.after_device_write()
+        if op != "insert":
+            out = out.bool()
+        return out if kind == "host" else out.numpy()
 
     def _ret(self, t, kind):
         if kind == "cuda":
@@ -225,6 +282,8 @@ class Tcf:
     def insert_many(self, keys, values=None):
         """Insert a batch; returns a Placement code per key (no raise)."""
         torch = self._torch
+        if values is None and self._pipe_wants(keys):
+            return self._pipelined(keys, "insert", torch.uint8)
         k, on_dev = self._keys_in(keys)
         n = k.numel()
         v = self._check_values(values, n, on_dev)
@@ -250,6 +309,8 @@ class Tcf:
         return bool(found[0]), int(values[0])
 
     def query_many(self, keys):
+        if self._pipe_wants(keys):
+            return self._pipelined(keys, "query", self._torch.uint8)
         return self._query(keys, False)[0]
 
     def query_values_many(self, keys):
@@ -279,6 +340,8 @@ class Tcf:
 
     def delete_many(self, keys):
         torch = self._torch
+        if self._pipe_wants(keys):
+            return self._pipelined(keys, "delete", torch.uint8)
         k, on_dev = self._keys_in(keys)
         n = k.numel()
         removed = torch.empty(n, dtype=torch.uint8, device=self._device)

@@ -206,3 +206,40 @@ def test_ordered_tunables_do_not_change_results(oracle, monkeypatch, window, res
     assert np.array_equal(f.delete_many(d), o.delete_many(d))
     _same_tables(f, o)
     assert f.counters == o.counters
+
+
+@pytest.mark.parametrize("mode", ["ordered", "concurrent"])
+@pytest.mark.parametrize("host_kind", ["numpy", "pinned"])
+def test_host_pipeline_matches_device_path(oracle, mode, host_kind):
+    """Host-side batches stream through the chunked H2D/kernel/D2H pipeline;
+    in ordered mode the chunks give exactly the one-launch (= sequential)
+    result, and queries are pure functions of the table in both modes."""
+    import torch
+    from paper_2212_09005_b200 import Tcf
+    from paper_2212_09005_b200._pipeline import HostPipeline
+    keys = counter_keys(41, 300_007)
+    negs = counter_keys(42, 200_003)
+    f = Tcf(num_blocks=1 << 15, mode=mode)
+    f._pipe = HostPipeline(torch, f._device, chunk=1 << 16)  # 5 chunks
+    hk = keys if host_kind == "numpy" else torch.from_numpy(keys.view(np.int64)).pin_memory()
+    hn = negs if host_kind == "numpy" else torch.from_numpy(negs.view(np.int64)).pin_memory()
+    codes = f.insert_many(hk)
+    got = {"pos": f.query_many(hk), "neg": f.query_many(hn)}
+    if host_kind == "pinned":
+        assert isinstance(codes, torch.Tensor) and not codes.is_cuda
+        codes, got = codes.numpy(), {k: v.numpy() for k, v in got.items()}
+    assert got["pos"].dtype == bool and got["pos"].all()
+    # queries on the same image through the device path
+    dn = torch.from_numpy(negs.view(np.int64)).cuda()
+    assert np.array_equal(got["neg"], f.query_many(dn).cpu().numpy())
+    if mode == "ordered":
+        o = _oracle(f, oracle)
+        assert np.array_equal(codes, o.insert_many(keys))
+        _same_tables(f, o)
+    rem = f.delete_many(hk)
+    rem = rem if host_kind == "numpy" else rem.numpy()
+    assert rem.all()
+    if mode == "ordered":
+        assert np.array_equal(rem, o.delete_many(keys).astype(bool))
+        _same_tables(f, o)
+    f.validate()
