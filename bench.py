@@ -58,6 +58,10 @@ BYTES_PER_OP = {
 # L2-resident): b2 read on 26.0% of inserts / 14.37% of positive queries and
 # deletes, both blocks on every negative query.
 SECTORS_PER_OP = {"insert": 1.260, "query_pos": 1.1437, "query_neg": 2.0, "delete": 1.1437}
+# Insert/delete write one sector back: the first block touched is a random
+# read-modify-write, the rest (b2 on 26.0% of inserts / 14.37% of deletes)
+# plain random reads.  (rmw, extra reads) per op:
+RMW_PER_OP = {"insert": (1.0, 0.260), "delete": (1.0, 0.1437), "query_pos": (0.0, 1.1437), "query_neg": (0.0, 2.0)}
 
 KERNEL_OF = {
     ("ordered", "insert"): "k_tcf_ordered<u16,G=1,B=16,KB=2,OP=insert>",
@@ -154,9 +158,28 @@ def random_sector_ceiling(torch, filt, stream, reps=3):
     b.synchronize()
     ms = a.elapsed_time(b) / reps
     sps = n / (ms / 1e3)
-    return {"sectors_per_s": sps, "useful_gbs": 32 * sps / 1e9, "table_bytes": tab.numel(),
-            "how": "fk_sector_gather: %d random 32-B sector loads (ld.global.v8) over the %d MiB block table, "
-                   "mean of %d, CUDA events" % (n, tab.numel() >> 20, reps)}
+    # read-modify-write ceiling on a scratch table of the same size
+    scratch = torch.zeros_like(tab)
+    _lib.check(lib.fk_sector_rmw(_lib.dptr(scratch), scratch.numel(), n, 1, sp), "rmw")
+    a.record(stream)
+    for r in range(reps):
+        _lib.check(lib.fk_sector_rmw(_lib.dptr(scratch), scratch.numel(), n, 2 + r, sp), "rmw")
+    b.record(stream)
+    b.synchronize()
+    rmw = n / (a.elapsed_time(b) / reps / 1e3)
+    del scratch
+    return {"sectors_per_s": sps, "useful_gbs": 32 * sps / 1e9, "rmw_sectors_per_s": rmw,
+            "table_bytes": tab.numel(),
+            "how": "fk_sector_gather: %d random 32-B sector loads (ld.global.v8) over the %d MiB block table; "
+                   "fk_sector_rmw: the same stream as load + 16-bit store back (the insert/delete pattern) on a "
+                   "scratch table of the same size; mean of %d, CUDA events" % (n, tab.numel() >> 20, reps)}
+
+
+def op_ceiling(op, ceiling):
+    """Achievable ops/s of `op` if every access ran at the measured random
+    ceilings: 1 read-modify-write and/or extra random sector reads per op."""
+    rmw, reads = RMW_PER_OP[op]
+    return 1.0 / (rmw / ceiling["rmw_sectors_per_s"] + reads / ceiling["sectors_per_s"])
 
 
 def ncu_traffic(mode, op, n):
@@ -197,7 +220,7 @@ def count_launches(torch, step):
         return None
 
 
-def concurrent_mode(torch, nb, args, keys, negs, stream, steps=2):
+def concurrent_mode(torch, nb, args, keys, negs, stream, ceiling=None, steps=2):
     """The paper's free-threaded CAS mode on the same workload (secondary
     numbers; not bit-identical to the sequential reference)."""
     from paper_2212_09005_b200 import Tcf
@@ -221,6 +244,9 @@ def concurrent_mode(torch, nb, args, keys, negs, stream, steps=2):
             for i, op in enumerate(("insert", "query_pos", "query_neg", "delete")):
                 res.setdefault(op, []).append(evs[i].elapsed_time(evs[i + 1]))
     out = {op: {"ops_per_s": n / (np.mean(v) / 1e3), "ms": float(np.mean(v))} for op, v in res.items()}
+    if ceiling:
+        for op in out:
+            out[op]["frac_of_random_access_ceiling"] = out[op]["ops_per_s"] / op_ceiling(op, ceiling)
     out["step_ops_per_s"] = 4 * n / (sum(np.mean(v) for v in res.values()) / 1e3)
     del f
     torch.cuda.empty_cache()
@@ -351,13 +377,15 @@ def run_ours(args, rank, world, local_rank):
         per_op[op] = {"ops_per_s": rate, "ms": per_op_ms[op], "achieved_gbs": gbs,
                       "frac_of_%s_hbm" % peak_kind: gbs / peak,
                       "random_sectors_per_op": SECTORS_PER_OP[op],
-                      "frac_of_random_sector_ceiling": SECTORS_PER_OP[op] * rate / ceiling["sectors_per_s"]}
+                      "frac_of_random_sector_ceiling": SECTORS_PER_OP[op] * rate / ceiling["sectors_per_s"],
+                      "random_access_ceiling_ops_per_s": op_ceiling(op, ceiling),
+                      "frac_of_random_access_ceiling": rate / op_ceiling(op, ceiling)}
     achieved = BYTES_PER_OP[dom] * n / (per_op_ms[dom] / 1e3) / 1e9
     traffic = ncu_traffic(args.mode, dom, n)
     launches = count_launches(torch, step) if not args.no_launch_count else None
     conc = None
     if args.mode == "ordered" and not args.no_concurrent and world == 1:
-        conc = concurrent_mode(torch, nb, args, keys, negs, stream)
+        conc = concurrent_mode(torch, nb, args, keys, negs, stream, ceiling)
     result = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",

@@ -88,6 +88,11 @@ int fk_sector_gather(const void *table, int64_t table_bytes, int64_t n, uint64_t
  * (TAG_UNIFORM / TAG_FPR, fk/workloads.py:61-64, :205-208). */
 int fk_counter_stream(uint64_t seed, uint64_t tag, uint64_t start, int64_t n, uint64_t *out, void *stream);
 
+/* Measurement kernel (not a reference function): n random 32-byte sector
+ * read-modify-writes (load the sector, store one 16-bit word back) over the
+ * table -- the insert/delete access pattern; overwrites table contents. */
+int fk_sector_rmw(void *table, int64_t table_bytes, int64_t n, uint64_t salt, void *stream);
+
 /* Exact x % d on device through the fast-mod path (tests only). */
 int fk_fastmod_check(const uint64_t *x, int64_t n, uint64_t d, uint64_t *out, void *stream);
 

@@ -60,6 +60,7 @@ _SIGS = {
     "fk_device_l2_fetch_bytes": (c_i32, []),
     "fk_hash_streams": (c_i32, [c_vp, c_i64, c_u64, c_i32, c_u64, c_u64, c_vp, c_vp]),
     "fk_sector_gather": (c_i32, [c_vp, c_i64, c_i64, c_u64, c_vp, c_vp]),
+    "fk_sector_rmw": (c_i32, [c_vp, c_i64, c_i64, c_u64, c_vp]),
     "fk_fastmod_check": (c_i32, [c_vp, c_i64, c_u64, c_vp, c_vp]),
     "fk_counter_stream": (c_i32, [c_u64, c_u64, c_u64, c_i64, c_vp, c_vp]),
     "fk_tcf_workspace_bytes": (c_sz, [ctypes.POINTER(TcfGeom), c_i64, c_i32]),

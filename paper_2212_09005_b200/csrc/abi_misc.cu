@@ -38,6 +38,24 @@ __global__ void __launch_bounds__(256) k_sector_gather(const uint32_t *__restric
   if (acc == 0x9E3779B9u) sink[blockIdx.x & 31] = acc;  // keeps the loads live
 }
 
+// Random 32-byte sector read-modify-write: load a random sector, bump one
+// 16-bit word of it, store it back -- the access pattern of a TCF insert or
+// delete that lands in its first block (the measured ceiling for those ops).
+__global__ void __launch_bounds__(256) k_sector_rmw(uint32_t *__restrict__ table, uint64_t nsec, FastMod m,
+                                                    int64_t n, uint64_t salt) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t h = mix64((uint64_t)i ^ salt);
+    uint64_t b = fmod64(h, m);
+    uint32_t r[8];
+    load_chunk<32, true>(table + 8 * b, r);
+    uint32_t x = 0;
+#pragma unroll
+    for (int j = 0; j < 8; j++) x += r[j];
+    uint16_t *w = reinterpret_cast<uint16_t *>(table + 8 * b) + (h >> 60);
+    *w = (uint16_t)(x | 2);
+  }
+}
+
 // counter_stream (workloads.py:23-26): mix64(mix64(seed ^ tag) + i) for
 // i in [start, start + n) -- the uniform key generator, exactly distinct.
 // Two keys per thread as one 128-bit store.
@@ -124,6 +142,15 @@ int fk_sector_gather(const void *table, int64_t table_bytes, int64_t n, uint64_t
   int grid = num_sms() * 8;
   k_sector_gather<<<grid, 256, 0, (cudaStream_t)stream>>>((const uint32_t *)table, nsec, make_fastmod(nsec), n, salt,
                                                           sink);
+  FK_CHECK_LAUNCH();
+  return 0;
+}
+
+int fk_sector_rmw(void *table, int64_t table_bytes, int64_t n, uint64_t salt, void *stream) {
+  if (n < 0 || table_bytes < 32 || ((uintptr_t)table & 31)) return FK_E_ARG;
+  if (n == 0) return 0;
+  uint64_t nsec = (uint64_t)table_bytes / 32;
+  k_sector_rmw<<<num_sms() * 8, 256, 0, (cudaStream_t)stream>>>((uint32_t *)table, nsec, make_fastmod(nsec), n, salt);
   FK_CHECK_LAUNCH();
   return 0;
 }
