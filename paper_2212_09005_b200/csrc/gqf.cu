@@ -207,10 +207,19 @@ int count_t(const fk_gqf_geom *g, const fk_gqf_tables *t, const uint64_t *keys, 
   return 0;
 }
 
+// apply_t flags: dry run (steps 1-12 only; res->code = 1 if the batch would
+// need the exact sequential path), or go straight to the exact path.
+constexpr int kApplyDry = 1, kApplyForceExact = 2;
+// Point-order batches longer than this that may hit a capacity error first
+// apply their longest provably safe prefix canonically (found by binary
+// search over dry runs) and run only the rest through the one-thread
+// sequential kernel.
+constexpr int64_t kExactSeqDirect = 2048;
+
 template <typename S_t>
 int apply_t(const fk_gqf_geom *g, const fk_gqf_tables *cur, const fk_gqf_tables *nxt, const uint64_t *keys,
             int keys_are_fps, const uint64_t *deltas, int64_t n, int op, int order, uint8_t *found,
-            fk_gqf_result *res, cudaStream_t st) {
+            fk_gqf_result *res, cudaStream_t st, int flags = 0) {
   Scratch S(st);
   const int qr = g->q + g->r;
   const uint64_t fmask = qr >= 64 ? ~0ull : ((1ull << qr) - 1);
@@ -323,8 +332,8 @@ int apply_t(const fk_gqf_geom *g, const fk_gqf_tables *cur, const fk_gqf_tables 
   }
 
   // 12. would the sequential reference have raised?  (inserts only)
-  bool exact = false, load_possible = false;
-  if (!is_del && G > 0) {
+  bool exact = (flags & kApplyForceExact) != 0, load_possible = exact;
+  if (!is_del && G > 0 && !exact) {
     int64_t *cfirst = S.get<int64_t>(G), *cfs = S.get<int64_t>(G);
     unsigned *flags = S.get<unsigned>(4);
     if (S.err) return -(int)S.err;
@@ -345,6 +354,47 @@ int apply_t(const fk_gqf_geom *g, const fk_gqf_tables *cur, const fk_gqf_tables 
     // occupancy below the ceiling rules LOAD_CAPACITY out for any order
     exact = h_flags != 0 || h_occ >= g->max_occupied;
     load_possible = h_occ >= g->max_occupied;
+  }
+
+  if (flags & kApplyDry) {
+    res->code = exact ? 1 : 0;
+    return 0;
+  }
+  if (exact && order == FK_ORDER_POINT && !(flags & kApplyForceExact) && n > kExactSeqDirect) {
+    // 13''. the reference fails at the first key whose insertion overflows;
+    // "the canonical layout of a prefix is safe" is monotone in the prefix
+    // length (inserts only grow clusters and occupancy) and implies that the
+    // reference raised nothing on it, so the longest safe prefix is applied
+    // canonically and only the keys after it run sequentially.
+    int64_t lo = 0, hi = n;
+    while (hi - lo > 1) {
+      int64_t mid = lo + (hi - lo) / 2;
+      fk_gqf_result r2{};
+      int rc = apply_t<S_t>(g, cur, nxt, keys, keys_are_fps, deltas, mid, op, order, nullptr, &r2, st, kApplyDry);
+      if (rc) return rc;
+      if (r2.code == 0) lo = mid; else hi = mid;
+    }
+    const fk_gqf_tables *c2 = cur, *n2 = nxt;
+    if (lo > 0) {
+      fk_gqf_result r3{};
+      int rc = apply_t<S_t>(g, cur, nxt, keys, keys_are_fps, deltas, lo, op, order, nullptr, &r3, st);
+      if (rc) return rc;
+      if (r3.code) return FK_E_INVARIANT;  // a safe prefix cannot fail
+      res->shifted += r3.shifted;
+      if (r3.swapped) {
+        res->swapped = 1;
+        c2 = nxt;
+        n2 = cur;
+      }
+    }
+    fk_gqf_result r4{};
+    int rc = apply_t<S_t>(g, c2, n2, keys + lo, keys_are_fps, deltas ? deltas + lo : nullptr, n - lo, op, order,
+                          nullptr, &r4, st, kApplyForceExact);
+    if (rc) return rc;
+    res->code = r4.code;
+    res->fail_index = r4.fail_index >= 0 ? r4.fail_index + lo : -1;
+    res->shifted += r4.shifted;
+    return 0;
   }
 
   if (exact) {

@@ -329,3 +329,38 @@ def test_device_validate_large_table():
     g.validate()
     assert time.perf_counter() - t < 5.0
     assert g.total_items == 6_000_000
+
+
+@pytest.mark.parametrize("with_counts", [False, True])
+def test_capacity_large_point_batch_prefix_path(oracle, with_counts):
+    """Point batches longer than the direct sequential threshold apply their
+    longest safe prefix canonically and only the tail sequentially: the
+    partial image (hence the failing index) still equals the reference's."""
+    from paper_2212_09005_b200 import CapacityError, Gqf
+    rng = np.random.default_rng(5 + with_counts)
+    keys = rng.integers(0, 2 ** 52, 9000, dtype=np.uint64)
+    cnt = rng.integers(1, 6, 9000).astype(np.uint64) if with_counts else None
+    g = Gqf(q=13, r=8, seed=4)
+    o = _oracle(g, oracle)
+    code, idx = o.insert_many(keys, cnt)
+    assert code == 1 and idx > 2048
+    with pytest.raises(CapacityError):
+        g.insert_many(keys, cnt)
+    same_image(g, o)
+    g.validate()
+
+
+def test_shift_bound_inside_large_point_batch(oracle):
+    from paper_2212_09005_b200 import CapacityError, Gqf
+    g = Gqf(q=15, r=8, seed=3)
+    o = _oracle(g, oracle)
+    rng = np.random.default_rng(9)
+    keys = rng.integers(0, 2 ** 52, 4000, dtype=np.uint64)
+    keys[2600] = craft(g, [(100, 0)])[0]
+    cnt = np.ones(4000, dtype=np.uint64)
+    cnt[2600] = 20_000
+    code, idx = o.insert_many(keys, cnt)
+    assert code == 2 and idx == 2600
+    with pytest.raises(CapacityError, match="hard bound"):
+        g.insert_many(keys, cnt)
+    same_image(g, o)
