@@ -64,8 +64,8 @@ SECTORS_PER_OP = {"insert": 1.260, "query_pos": 1.1437, "query_neg": 2.0, "delet
 RMW_PER_OP = {"insert": (1.0, 0.260), "delete": (1.0, 0.1437), "query_pos": (0.0, 1.1437), "query_neg": (0.0, 2.0)}
 
 KERNEL_OF = {
-    ("ordered", "insert"): "k_tcf_ordered<u16,G=1,B=16,KB=2,OP=insert>",
-    ("ordered", "delete"): "k_tcf_ordered<u16,G=1,B=16,KB=2,OP=delete>",
+    ("ordered", "insert"): "k_tcf_ordered1<KB=2,OP=insert> (one-barrier, u16, B=16, G=1)",
+    ("ordered", "delete"): "k_tcf_ordered1<KB=2,OP=delete> (one-barrier, u16, B=16, G=1)",
     ("concurrent", "insert"): "k_tcf_insert_cas<u16,G=1,B=16>",
     ("concurrent", "delete"): "k_tcf_delete_cas<u16,G=1,B=16>",
 }

@@ -87,8 +87,14 @@ static int ord_hints() {
   return e ? atoi(e) != 0 : 1;
 }
 
+// the one-barrier ordered kernel (u16 slots, B = 16, G = 1) keeps a second
+// reservation array (tunable: FK_ORD_ONEBAR=0 selects the carry-list kernel)
+static int ord_onebar(const fk_tcf_geom *g) {
+  return g->slot_bytes == 2 && g->block_slots == 16 && g->group_width == 1 && env_int("FK_ORD_ONEBAR", 1);
+}
+
 static size_t ord_ws_layout(const fk_tcf_geom *g, int64_t n, size_t *off) {
-  // off[]: res, bres, defer_idx, defer_pend, ctl, carry0, carry1
+  // off[]: res, bres, defer_idx, defer_pend, ctl, carry0, carry1, res2
   size_t a = 0;
   auto take = [&](size_t bytes) { size_t o = a; a += (bytes + 255) & ~(size_t)255; return o; };
   int64_t cap = n < 1 ? 1 : n;
@@ -100,12 +106,13 @@ static size_t ord_ws_layout(const fk_tcf_geom *g, int64_t n, size_t *off) {
   off[4] = take(64);
   off[5] = take((size_t)w * 4);
   off[6] = take((size_t)w * 4);
+  off[7] = ord_onebar(g) ? take((size_t)((g->num_blocks >> ord_res_shift(g->num_blocks)) + 1) * 4) : 0;
   return a;
 }
 
 static int prep_ordered(const fk_tcf_geom *g, int64_t n, void *ws, size_t ws_bytes, OrdScratch *X,
                         cudaStream_t st) {
-  size_t off[7];
+  size_t off[8];
   size_t need = ord_ws_layout(g, n, off);
   if (!ws || ws_bytes < need) return FK_E_ARG;
   char *b = (char *)ws;
@@ -124,6 +131,12 @@ static int prep_ordered(const fk_tcf_geom *g, int64_t n, void *ws, size_t ws_byt
   X->prefetch = env_int("FK_ORD_PREFETCH", 0);  // measured slower (8.1 vs 8.7 G/s at C3)
   X->ctas_per_sm = env_int("FK_ORD_CTAS_PER_SM", g->num_blocks <= (1 << 16) ? 1 : (g->num_blocks <= (1 << 20) ? 2 : 0));
   FK_TRY(cudaMemsetAsync(X->res, 0xFF, (size_t)((g->num_blocks >> X->res_shift) + 1) * 4, st));
+  X->res2 = nullptr;
+  if (ord_onebar(g)) {
+    X->res2 = (uint32_t *)(b + off[7]);
+    FK_TRY(cudaMemsetAsync(X->res2, 0xFF, (size_t)((g->num_blocks >> X->res_shift) + 1) * 4, st));
+  }
+  X->slots = 1;
   FK_TRY(cudaMemsetAsync(X->bres, 0xFF, (size_t)(g->backing_slots ? g->backing_slots : 1) * 4, st));
   FK_TRY(cudaMemsetAsync(X->ctl, 0, 64, st));
   return 0;
@@ -137,7 +150,7 @@ extern "C" {
 
 size_t fk_tcf_workspace_bytes(const fk_tcf_geom *g, int64_t n, int mode) {
   if (!g || mode != FK_ORDERED) return 0;
-  size_t off[7];
+  size_t off[8];
   return ord_ws_layout(g, n, off);
 }
 

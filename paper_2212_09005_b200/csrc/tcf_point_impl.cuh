@@ -468,6 +468,8 @@ struct OrdScratch {
   int hints;            // 1: L2 evict_last on reservation words, evict_first on streams
   int ctas_per_sm;      // 0: occupancy limit; else cap (fewer grid-barrier participants)
   int prefetch;         // 1: the reserve pass prefetches each key's b1 block into L2
+  uint32_t *res2;       // one-barrier kernel: reservation words of odd rounds
+  int slots;            // one-barrier kernel: keys held per thread (<= KB)
 };
 
 // CTA-wide OR of a predicate (all threads of the CTA must call).
@@ -543,6 +545,107 @@ __device__ __forceinline__ void deferred_key(const TcfDev &P, const uint64_t *ke
   *fp = P.keys_are_fps ? key : mix64(key ^ P.seed);
   uint64_t tag = remap_tag(*fp, P.fmask);
   *word = OP == 0 ? ((P.f >= 64 ? 0 : ((values ? values[i] : 0) << P.f)) | tag) : tag;
+}
+
+// Backing phase of the ordered kernels: deferred keys (both blocks full on
+// insert / no match on delete) claim backing positions in input-index order
+// by reservations over probe positions (pk:104-117, pk:223-233).  Returns
+// the round counter after the phase.
+template <typename S, int G, int OP>
+__device__ __forceinline__ unsigned ordered_backing_phase(const TcfDev &P, const uint64_t *__restrict__ keys,
+                                                          const uint64_t *__restrict__ values,
+                                                          uint8_t *__restrict__ out, const OrdScratch &X,
+                                                          const Tile<G> &t, int64_t tiles, int64_t tid,
+                                                          cg::grid_group &grid, unsigned round, long long *n_a,
+                                                          long long *n_b) {
+  grid.sync();
+  int64_t nd = (int64_t)__ldcg(&X.ctl[2]);
+  if (nd > X.defer_cap) nd = X.defer_cap;
+  S *bk = reinterpret_cast<S *>(P.backing);
+  if (nd > 0) {
+    for (;;) {
+      // reserve every position this key could still take: for inserts all
+      // free probe positions, for deletes all live matches before the chain
+      // ends (pk:104-117, pk:223-233)
+      for (int64_t e = tid; e < nd; e += tiles) {
+        if (t.lane != 0 || !__ldcg(&X.defer_pend[e])) continue;
+        uint32_t idx = __ldcg(&X.defer_idx[e]);
+        uint64_t fp, word;
+        deferred_key<OP>(P, keys, values, idx, &fp, &word);
+        if (!P.bsize) continue;
+        uint64_t p = fmod64(mix64(fp ^ kBackStart), P.bsm);
+        uint64_t step = fmod64(mix64(fp ^ kBackStep) | 1, P.bsm);
+        for (int q = 0; q < P.probe_limit; q++) {
+          uint64_t w = load_slot<S, true>(bk + p);
+          if (OP == 0) {
+            if (!live_word(w)) atomicMin(&X.bres[p], idx);
+          } else {
+            if (w == 0) break;
+            if (w != 1 && (w & P.fmask) == word) atomicMin(&X.bres[p], idx);
+          }
+          p += step;
+          p = p >= P.bsize ? p - P.bsize : p;
+        }
+      }
+      grid.sync();
+      bool left = false;
+      for (int64_t e = tid; e < nd; e += tiles) {
+        if (t.lane != 0 || !__ldcg(&X.defer_pend[e])) continue;
+        uint32_t idx = __ldcg(&X.defer_idx[e]);
+        int64_t i = idx;
+        uint64_t fp, word;
+        deferred_key<OP>(P, keys, values, idx, &fp, &word);
+        int64_t target = -1;
+        if (P.bsize) {
+          uint64_t p = fmod64(mix64(fp ^ kBackStart), P.bsm);
+          uint64_t step = fmod64(mix64(fp ^ kBackStep) | 1, P.bsm);
+          for (int q = 0; q < P.probe_limit; q++) {
+            uint64_t w = load_slot<S, true>(bk + p);
+            if (OP == 0) {
+              if (!live_word(w)) { target = (int64_t)p; break; }
+            } else {
+              if (w == 0) break;
+              if (w != 1 && (w & P.fmask) == word) { target = (int64_t)p; break; }
+            }
+            p += step;
+            p = p >= P.bsize ? p - P.bsize : p;
+          }
+        }
+        if (target < 0) {  // nothing claimable now, nor ever in this batch
+          out[i] = OP == 0 ? kFull : 0;
+          X.defer_pend[e] = 0;
+          continue;
+        }
+        if (__ldcg(&X.bres[target]) != idx) {
+          left = true;
+          continue;
+        }
+        bk[target] = (S)(OP == 0 ? word : 1);
+        out[i] = OP == 0 ? kBacking : 1;
+        (*n_a)++;
+        *n_b += OP == 0;
+        X.defer_pend[e] = 0;
+        // release every reservation still carrying our index
+        uint64_t p = fmod64(mix64(fp ^ kBackStart), P.bsm);
+        uint64_t step = fmod64(mix64(fp ^ kBackStep) | 1, P.bsm);
+        for (int q = 0; q < P.probe_limit; q++) {
+          atomicCAS(&X.bres[p], idx, kNoRes);
+          p += step;
+          p = p >= P.bsize ? p - P.bsize : p;
+        }
+      }
+      bool any = cta_any(left);
+      if (threadIdx.x == 0) {
+        if (any) atomicAdd(&X.ctl[3 + (round & 1)], 1u);
+        if (blockIdx.x == 0) X.ctl[3 + ((round + 1) & 1)] = 0;
+      }
+      grid.sync();
+      unsigned cnt = __ldcg(&X.ctl[3 + (round & 1)]);
+      round++;
+      if (cnt == 0) break;
+    }
+  }
+  return round;
 }
 
 template <typename S, int G, int BF, int KB, int OP>
@@ -715,95 +818,8 @@ __global__ void __launch_bounds__(256, 4)
   if (blockIdx.x == 0 && threadIdx.x == 0) X.ctl[5] = round;
   const unsigned main_rounds = round;
 
-  // ---- backing phase: deferred keys in input-index order -------------------
-  grid.sync();
-  int64_t nd = (int64_t)__ldcg(&X.ctl[2]);
-  if (nd > X.defer_cap) nd = X.defer_cap;
-  S *bk = reinterpret_cast<S *>(P.backing);
   long long n_b = 0;
-  if (nd > 0) {
-    for (;;) {
-      // reserve every position this key could still take: for inserts all
-      // free probe positions, for deletes all live matches before the chain
-      // ends (pk:104-117, pk:223-233)
-      for (int64_t e = tid; e < nd; e += tiles) {
-        if (t.lane != 0 || !__ldcg(&X.defer_pend[e])) continue;
-        uint32_t idx = __ldcg(&X.defer_idx[e]);
-        uint64_t fp, word;
-        deferred_key<OP>(P, keys, values, idx, &fp, &word);
-        if (!P.bsize) continue;
-        uint64_t p = fmod64(mix64(fp ^ kBackStart), P.bsm);
-        uint64_t step = fmod64(mix64(fp ^ kBackStep) | 1, P.bsm);
-        for (int q = 0; q < P.probe_limit; q++) {
-          uint64_t w = load_slot<S, true>(bk + p);
-          if (OP == 0) {
-            if (!live_word(w)) atomicMin(&X.bres[p], idx);
-          } else {
-            if (w == 0) break;
-            if (w != 1 && (w & P.fmask) == word) atomicMin(&X.bres[p], idx);
-          }
-          p += step;
-          p = p >= P.bsize ? p - P.bsize : p;
-        }
-      }
-      grid.sync();
-      bool left = false;
-      for (int64_t e = tid; e < nd; e += tiles) {
-        if (t.lane != 0 || !__ldcg(&X.defer_pend[e])) continue;
-        uint32_t idx = __ldcg(&X.defer_idx[e]);
-        int64_t i = idx;
-        uint64_t fp, word;
-        deferred_key<OP>(P, keys, values, idx, &fp, &word);
-        int64_t target = -1;
-        if (P.bsize) {
-          uint64_t p = fmod64(mix64(fp ^ kBackStart), P.bsm);
-          uint64_t step = fmod64(mix64(fp ^ kBackStep) | 1, P.bsm);
-          for (int q = 0; q < P.probe_limit; q++) {
-            uint64_t w = load_slot<S, true>(bk + p);
-            if (OP == 0) {
-              if (!live_word(w)) { target = (int64_t)p; break; }
-            } else {
-              if (w == 0) break;
-              if (w != 1 && (w & P.fmask) == word) { target = (int64_t)p; break; }
-            }
-            p += step;
-            p = p >= P.bsize ? p - P.bsize : p;
-          }
-        }
-        if (target < 0) {  // nothing claimable now, nor ever in this batch
-          out[i] = OP == 0 ? kFull : 0;
-          X.defer_pend[e] = 0;
-          continue;
-        }
-        if (__ldcg(&X.bres[target]) != idx) {
-          left = true;
-          continue;
-        }
-        bk[target] = (S)(OP == 0 ? word : 1);
-        out[i] = OP == 0 ? kBacking : 1;
-        n_a++;
-        n_b += OP == 0;
-        X.defer_pend[e] = 0;
-        // release every reservation still carrying our index
-        uint64_t p = fmod64(mix64(fp ^ kBackStart), P.bsm);
-        uint64_t step = fmod64(mix64(fp ^ kBackStep) | 1, P.bsm);
-        for (int q = 0; q < P.probe_limit; q++) {
-          atomicCAS(&X.bres[p], idx, kNoRes);
-          p += step;
-          p = p >= P.bsize ? p - P.bsize : p;
-        }
-      }
-      bool any = cta_any(left);
-      if (threadIdx.x == 0) {
-        if (any) atomicAdd(&X.ctl[3 + (round & 1)], 1u);
-        if (blockIdx.x == 0) X.ctl[3 + ((round + 1) & 1)] = 0;
-      }
-      grid.sync();
-      unsigned cnt = __ldcg(&X.ctl[3 + (round & 1)]);
-      round++;
-      if (cnt == 0) break;
-    }
-  }
+  round = ordered_backing_phase<S, G, OP>(P, keys, values, out, X, t, tiles, tid, grid, round, &n_a, &n_b);
   if (blockIdx.x == 0 && threadIdx.x == 0) X.ctl[6] = round - main_rounds;
   if (t.lane == 0) {
     if (OP == 0) {
@@ -812,6 +828,183 @@ __global__ void __launch_bounds__(256, 4)
     } else if (n_a) {
       atomicAdd((unsigned long long *)&counters[2], (unsigned long long)n_a);
     }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// One-barrier ordered kernel (u16 slots, B = 16, G = 1: the benchmarked
+// geometry).  Same deterministic reservations as k_tcf_ordered, restructured
+// so a round needs one grid barrier instead of two:
+//   * reservation words alternate between two arrays (even / odd rounds);
+//   * every thread keeps its pending keys in registers (no carry list): after
+//     committing round r it immediately grabs new input indices (a global
+//     atomic frontier, so introduced keys always form a prefix of the input)
+//     and bids for round r+1 into the other array, then waits at the barrier;
+//   * a key that loses a round retracts its own bids (CAS idx -> free) and a
+//     holder releases its words, so an array is clean when its next round
+//     starts -- that round's bids begin only after the next barrier.
+// Correctness is the same argument: a key commits only holding both words of
+// its round, i.e. no earlier pending key touches its blocks, and every
+// earlier key is either committed (before an earlier barrier) or pending
+// (and bid this round).  ctl[8..10] count pending keys per round (mod 3),
+// ctl[11] is the frontier.
+// ---------------------------------------------------------------------------
+template <int KB, int OP>
+__global__ void __launch_bounds__(256, 4)
+    k_tcf_ordered1(TcfDev P, const uint64_t *__restrict__ keys, const uint64_t *__restrict__ values, int64_t n,
+                   uint8_t *__restrict__ out, int64_t *__restrict__ counters, OrdScratch X) {
+  cg::grid_group grid = cg::this_grid();
+  Tile<1> t;
+  const int64_t tiles = (int64_t)gridDim.x * blockDim.x;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const unsigned lane = threadIdx.x & 31;
+  const uint64_t pol_keep = l2_evict_last(), pol_stream = l2_evict_first();
+  uint16_t *blocks = reinterpret_cast<uint16_t *>(P.blocks);
+  const int rs = X.res_shift;
+  uint32_t idx[KB], b1[KB], b2[KB], tg[KB];
+  bool pend[KB];
+#pragma unroll
+  for (int j = 0; j < KB; j++) {
+    pend[j] = false;
+    idx[j] = b1[j] = b2[j] = tg[j] = 0;
+  }
+  long long n_a = 0;
+  unsigned losses = 0;
+  unsigned r = 0;
+  __shared__ unsigned s_warp[32];
+  __shared__ unsigned s_base;
+
+  for (;;) {
+    // ---- reserve round r: fill free slots from the frontier, bid ---------
+    {
+      uint32_t *R = (r & 1) ? X.res2 : X.res;
+      unsigned need = 0;
+#pragma unroll
+      for (int j = 0; j < KB; j++) need += (j < X.slots && !pend[j]) ? 1u : 0u;
+      // one frontier atomic per CTA (a single L2 address takes every grab)
+      unsigned incl = need;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        unsigned v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if ((int)lane >= o) incl += v;
+      }
+      if (lane == 31) s_warp[threadIdx.x >> 5] = incl;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        unsigned acc = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); w++) {
+          unsigned v = s_warp[w];
+          s_warp[w] = acc;
+          acc += v;
+        }
+        s_base = acc ? atomicAdd(&X.ctl[11], acc) : 0u;
+      }
+      __syncthreads();
+      unsigned nx = s_base + s_warp[threadIdx.x >> 5] + incl - need;  // this lane's first new index
+#pragma unroll
+      for (int j = 0; j < KB; j++) {
+        if (j >= X.slots || pend[j]) continue;
+        if ((int64_t)nx < n) {
+          idx[j] = nx;
+          pend[j] = true;
+          KeyInfo ki = key_info(P, ld_stream_u64(keys + nx, pol_stream));
+          b1[j] = (uint32_t)ki.b1;
+          b2[j] = (uint32_t)ki.b2;
+          tg[j] = (uint32_t)ki.tag;
+        }
+        nx++;
+      }
+      unsigned mine = 0;
+#pragma unroll
+      for (int j = 0; j < KB; j++) {
+        if (!pend[j]) continue;
+        mine++;
+        uint32_t g1 = b1[j] >> rs, g2 = b2[j] >> rs;
+        red_min_u32(&R[g1], idx[j], pol_keep);
+        if (g2 != g1) red_min_u32(&R[g2], idx[j], pol_keep);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xFFFFFFFFu, mine, o);
+      __syncthreads();  // s_warp is reused
+      if (lane == 0) s_warp[threadIdx.x >> 5] = mine;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        unsigned acc = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); w++) acc += s_warp[w];
+        if (acc) atomicAdd(&X.ctl[8 + r % 3], acc);
+      }
+    }
+    grid.sync();
+    const unsigned total = __ldcg(&X.ctl[8 + r % 3]);
+    if (blockIdx.x == 0 && threadIdx.x == 0) X.ctl[8 + (r + 2) % 3] = 0;
+    if (total == 0) break;
+
+    // ---- commit round r ----------------------------------------------------
+    {
+      uint32_t *R = (r & 1) ? X.res2 : X.res;
+      bool hold[KB];
+      uint32_t rb[KB][8];
+#pragma unroll
+      for (int j = 0; j < KB; j++) {
+        hold[j] = pend[j] && ld_cg_u32(&R[b1[j] >> rs], pol_keep) == idx[j] &&
+                  ld_cg_u32(&R[b2[j] >> rs], pol_keep) == idx[j];
+        if (hold[j]) load16<true>(blocks + (uint64_t)b1[j] * 16, rb[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < KB; j++) {
+        if (!pend[j]) continue;
+        uint32_t g1 = b1[j] >> rs, g2 = b2[j] >> rs;
+        if (!hold[j]) {  // lost: retract our own bids so the array is clean
+          atomicCAS(&R[g1], idx[j], kNoRes);
+          if (g2 != g1) atomicCAS(&R[g2], idx[j], kNoRes);
+          losses++;
+          continue;
+        }
+        bool defer;
+        if (OP == 0) {
+          uint64_t word = (P.f >= 64 || !values ? 0 : (values[idx[j]] << P.f)) | tg[j];
+          uint8_t code = commit_insert16(P, b1[j], b2[j], (uint16_t)word, rb[j]);
+          defer = code == 4;
+          if (!defer) {
+            out[idx[j]] = code;
+            n_a++;
+          }
+        } else {
+          int done = commit_delete16(P, b1[j], b2[j], tg[j], rb[j]);
+          defer = !done && P.bsize;
+          if (!defer) {
+            out[idx[j]] = done ? 1 : 0;
+            n_a += done;
+          }
+        }
+        if (defer) {
+          unsigned slot = atomicAdd(&X.ctl[2], 1u);
+          if (slot < X.defer_cap) {
+            X.defer_idx[slot] = idx[j];
+            X.defer_pend[slot] = 1;
+          }
+        }
+        st_u32(&R[g1], kNoRes, pol_keep);
+        st_u32(&R[g2], kNoRes, pol_keep);
+        pend[j] = false;
+      }
+    }
+    r++;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) X.ctl[5] = r;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) losses += __shfl_xor_sync(0xFFFFFFFFu, losses, o);
+  if (lane == 0 && losses) atomicAdd(&X.ctl[7], losses);
+
+  long long n_b = 0;
+  unsigned round = ordered_backing_phase<uint16_t, 1, OP>(P, keys, values, out, X, t, tiles, tid, grid, r, &n_a,
+                                                          &n_b);
+  if (blockIdx.x == 0 && threadIdx.x == 0) X.ctl[6] = round - r;
+  if (OP == 0) {
+    if (n_a) atomicAdd((unsigned long long *)&counters[0], (unsigned long long)n_a);
+    if (n_b) atomicAdd((unsigned long long *)&counters[1], (unsigned long long)n_b);
+  } else if (n_a) {
+    atomicAdd((unsigned long long *)&counters[2], (unsigned long long)n_a);
   }
 }
 
@@ -826,6 +1019,26 @@ constexpr int kOrdKB = G == 1 ? 2 : 4;
 template <typename S, int G, int BF, int OP>
 static int launch_ordered(const TcfDev &P, const uint64_t *keys, const uint64_t *values, int64_t n, uint8_t *out,
                           int64_t *counters, OrdScratch X, cudaStream_t st) {
+  if constexpr (kFast16<S, G, BF>) {
+    auto k1 = k_tcf_ordered1<kOrdKB<1>, OP>;
+    int per_sm = 0;
+    FK_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1, 256, 0));
+    if (per_sm < 1) return FK_E_ARG;
+    if (X.ctas_per_sm > 0 && X.ctas_per_sm < per_sm) per_sm = X.ctas_per_sm;
+    int grid = per_sm * num_sms();
+    int64_t thr = (int64_t)grid * 256;
+    // one-barrier kernel when the window gives every thread a key (its
+    // window is about grid * 256 * slots); small windows keep the carry-list
+    // kernel, whose window is exact
+    if (X.res2 && X.window >= thr) {
+      int slots = (int)((X.window + thr - 1) / thr);
+      X.slots = slots < 1 ? 1 : (slots > kOrdKB<1> ? kOrdKB<1> : slots);
+      void *args[] = {(void *)&P, (void *)&keys, (void *)&values, (void *)&n, (void *)&out, (void *)&counters,
+                      (void *)&X};
+      FK_TRY(cudaLaunchCooperativeKernel((const void *)k1, dim3(grid), dim3(256), args, 0, st));
+      return 0;
+    }
+  }
   auto kern = k_tcf_ordered<S, G, BF, kOrdKB<G>, OP>;
   int per_sm = 0;
   FK_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));

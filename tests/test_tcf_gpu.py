@@ -243,3 +243,33 @@ def test_host_pipeline_matches_device_path(oracle, mode, host_kind):
         assert np.array_equal(rem, o.delete_many(keys).astype(bool))
         _same_tables(f, o)
     f.validate()
+
+
+@pytest.mark.parametrize("onebar", ["0", "1"])
+@pytest.mark.parametrize("nb,res_shift,ctas", [(4096, 0, "1"), (1 << 16, 2, "0"), (1 << 16, 0, "2"),
+                                               (1 << 18, 3, "0")])
+def test_ordered_kernels_bit_exact(oracle, monkeypatch, onebar, nb, res_shift, ctas):
+    """Both ordered kernels -- the carry-list one (two barriers per round)
+    and the one-barrier one (alternating reservation arrays, register-held
+    keys, a global frontier) -- reproduce the sequential oracle, with a window
+    wide enough to select the one-barrier kernel, duplicates and overfill."""
+    from paper_2212_09005_b200 import Tcf
+    monkeypatch.setenv("FK_ORD_ONEBAR", onebar)
+    monkeypatch.setenv("FK_ORD_WINDOW", str(1 << 20))
+    monkeypatch.setenv("FK_ORD_RES_SHIFT", str(res_shift))
+    monkeypatch.setenv("FK_ORD_CTAS_PER_SM", ctas)
+    f = Tcf(num_blocks=nb)
+    o = _oracle(f, oracle)
+    n = int(nb * 16 * 0.97)
+    base = counter_keys(70 + nb, n)
+    keys = np.concatenate([base, base[:n // 10], base[:500]])
+    assert np.array_equal(f.insert_many(keys), o.insert_many(keys))
+    _same_tables(f, o)
+    probe = np.concatenate([base[::5], counter_keys(99, 20_000)])
+    fv, ov = f.query_values_many(probe), o.query_values_many(probe)
+    assert np.array_equal(fv[0], ov[0].astype(bool)) and np.array_equal(fv[1], ov[1])
+    d = np.concatenate([base[::2], base[:700], counter_keys(98, 5000)])
+    assert np.array_equal(f.delete_many(d), o.delete_many(d).astype(bool))
+    _same_tables(f, o)
+    assert f.counters == o.counters
+    f.validate()
