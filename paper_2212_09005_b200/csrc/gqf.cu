@@ -264,7 +264,11 @@ int apply_t(const fk_gqf_geom *g, const fk_gqf_tables *cur, const fk_gqf_tables 
   k_new_counts<<<blocks_for(m), 256, 0, st>>>(c_old, sums, m, is_del ? 1 : 0, c_new);
 
   // 7. delete found flags: sequential semantics via a segmented prefix sum
-  if (is_del && found) {
+  if (is_del && found && m == n) {
+    // no fingerprint repeats in the batch: a key is found iff its
+    // fingerprint was present
+    k_found_distinct<<<blocks_for(n), 256, 0, st>>>(c_old, idx_s, n, found);
+  } else if (is_del && found) {
     uint64_t *pre = S.get<uint64_t>(n);
     if (S.err) return -(int)S.err;
     if (order == FK_ORDER_POINT) {

@@ -243,6 +243,15 @@ __global__ void k_new_counts(const uint64_t *__restrict__ c_old, const uint64_t 
 
 // found flags for deletes: element j (in processing order within its fp
 // segment) finds the key iff the deltas processed before it leave a count.
+// found flags of a delete batch without repeated fingerprints: sorted item j
+// is input idx_s[j], its exclusive prefix is 0, so (as in k_found_flags)
+// found iff the fingerprint was present
+__global__ void k_found_distinct(const uint64_t *__restrict__ c_old, const uint32_t *__restrict__ idx_s, int64_t n,
+                                 uint8_t *__restrict__ found) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+    found[idx_s[j]] = c_old[j] > 0 ? 1 : 0;
+}
+
 __global__ void k_found_flags(const uint64_t *__restrict__ fps_s, const uint64_t *__restrict__ pre,
                               const uint32_t *__restrict__ idx_s, const uint64_t *__restrict__ uniq,
                               const uint64_t *__restrict__ c_old, int64_t m, int64_t n, uint8_t *__restrict__ found) {

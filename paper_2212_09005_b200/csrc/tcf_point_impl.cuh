@@ -470,6 +470,7 @@ struct OrdScratch {
   int prefetch;         // 1: the reserve pass prefetches each key's b1 block into L2
   uint32_t *res2;       // one-barrier kernel: reservation words of odd rounds
   int slots;            // one-barrier kernel: keys held per thread (<= KB)
+  int spec;             // one-barrier kernel: load b1 blocks before the reservation check
 };
 
 // CTA-wide OR of a predicate (all threads of the CTA must call).
@@ -944,11 +945,23 @@ __global__ void __launch_bounds__(256, 4)
       uint32_t *R = (r & 1) ? X.res2 : X.res;
       bool hold[KB];
       uint32_t rb[KB][8];
+      if (X.spec) {
+        // speculative: the b1 block load overlaps the reservation-word
+        // loads (losers, ~13 %, fetch their block for nothing)
 #pragma unroll
-      for (int j = 0; j < KB; j++) {
-        hold[j] = pend[j] && ld_cg_u32(&R[b1[j] >> rs], pol_keep) == idx[j] &&
-                  ld_cg_u32(&R[b2[j] >> rs], pol_keep) == idx[j];
-        if (hold[j]) load16<true>(blocks + (uint64_t)b1[j] * 16, rb[j]);
+        for (int j = 0; j < KB; j++)
+          if (pend[j]) load16<true>(blocks + (uint64_t)b1[j] * 16, rb[j]);
+#pragma unroll
+        for (int j = 0; j < KB; j++)
+          hold[j] = pend[j] && ld_cg_u32(&R[b1[j] >> rs], pol_keep) == idx[j] &&
+                    ld_cg_u32(&R[b2[j] >> rs], pol_keep) == idx[j];
+      } else {
+#pragma unroll
+        for (int j = 0; j < KB; j++) {
+          hold[j] = pend[j] && ld_cg_u32(&R[b1[j] >> rs], pol_keep) == idx[j] &&
+                    ld_cg_u32(&R[b2[j] >> rs], pol_keep) == idx[j];
+          if (hold[j]) load16<true>(blocks + (uint64_t)b1[j] * 16, rb[j]);
+        }
       }
 #pragma unroll
       for (int j = 0; j < KB; j++) {
