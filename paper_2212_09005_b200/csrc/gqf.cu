@@ -283,7 +283,13 @@ int apply_t(const fk_gqf_geom *g, const fk_gqf_tables *cur, const fk_gqf_tables 
       FK_CU(cub_excl_scan_by_key(S, rf, rd, rp, n));
       k_reverse_u64<<<blocks_for(n), 256, 0, st>>>(rp, n, pre);
     }
-    k_found_flags<<<blocks_for(n), 256, 0, st>>>(fps_s, pre, idx_s, uniq, c_old, m, n, found);
+    // segment (unique fingerprint) of every sorted item: exclusive sum of
+    // segment heads, instead of a binary search per item
+    int64_t *heads = S.get<int64_t>(n), *seg = S.get<int64_t>(n);
+    if (S.err) return -(int)S.err;
+    k_seg_heads<<<blocks_for(n), 256, 0, st>>>(fps_s, n, heads);
+    FK_CU(cub_excl_sum_i64(S, heads, seg, n));
+    k_found_flags<<<blocks_for(n), 256, 0, st>>>(pre, idx_s, seg, c_old, n, found);
   }
 
   // 8. decode the old table into sorted (fp, count) items

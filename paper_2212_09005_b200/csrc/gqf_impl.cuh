@@ -252,18 +252,20 @@ __global__ void k_found_distinct(const uint64_t *__restrict__ c_old, const uint3
     found[idx_s[j]] = c_old[j] > 0 ? 1 : 0;
 }
 
-__global__ void k_found_flags(const uint64_t *__restrict__ fps_s, const uint64_t *__restrict__ pre,
-                              const uint32_t *__restrict__ idx_s, const uint64_t *__restrict__ uniq,
-                              const uint64_t *__restrict__ c_old, int64_t m, int64_t n, uint8_t *__restrict__ found) {
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
-    uint64_t f = fps_s[j];
-    int64_t lo = 0, hi = m - 1;
-    while (lo < hi) {
-      int64_t mid = (lo + hi) >> 1;
-      if (uniq[mid] < f) lo = mid + 1; else hi = mid;
-    }
-    found[idx_s[j]] = pre[j] < c_old[lo] ? 1 : 0;
-  }
+// 1 where a sorted fingerprint starts a new segment, after the first item
+// (so the exclusive sum of heads is the item's segment index)
+__global__ void k_seg_heads(const uint64_t *__restrict__ fps_s, int64_t n, int64_t *__restrict__ heads) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+    heads[j] = (j + 1 < n && fps_s[j + 1] != fps_s[j]) ? 1 : 0;
+}
+
+// found flag of sorted item j: its copies before it in processing order
+// (pre[j]) leave something of the old count of its fingerprint
+__global__ void k_found_flags(const uint64_t *__restrict__ pre, const uint32_t *__restrict__ idx_s,
+                              const int64_t *__restrict__ seg, const uint64_t *__restrict__ c_old, int64_t n,
+                              uint8_t *__restrict__ found) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+    found[idx_s[j]] = pre[j] < c_old[seg[j]] ? 1 : 0;
 }
 
 __global__ void k_reverse_u64(const uint64_t *__restrict__ a, int64_t n, uint64_t *__restrict__ b) {
