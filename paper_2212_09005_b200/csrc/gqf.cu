@@ -1,6 +1,7 @@
 // gqf.cu -- host side of the GQF C ABI: count / find_run / index rebuild /
 // insert+delete batches (canonical rebuild, exact sequential fallback).
 #include <cub/cub.cuh>
+#include <stdlib.h>
 
 #include <vector>
 
@@ -198,6 +199,70 @@ int validate_t(const fk_gqf_geom *g, const fk_gqf_tables *t, int64_t *out, cudaS
   return 0;
 }
 
+// a batch touching at most this many distinct fingerprints takes the
+// region-local path (tunable: FK_GQF_SMALL; 0 disables)
+inline int64_t small_batch_limit(const fk_gqf_geom *g) {
+  const char *e = getenv("FK_GQF_SMALL");
+  if (e) return atoll(e);
+  int64_t lim = g->quotient_regions * 2;
+  return lim < (1 << 16) ? lim : (1 << 16);
+}
+
+// Region-local insert of a sorted batch into a copy of `cur` written to
+// `nxt`.  Returns 0 when applied (tables swapped), 1 when a region reported
+// a capacity failure (nothing applied; the caller runs the full path), or a
+// negative error.
+template <typename S_t>
+int apply_small_t(const fk_gqf_geom *g, const fk_gqf_tables *cur, const fk_gqf_tables *nxt, const uint64_t *fps_s,
+                  const uint64_t *del_s, int64_t n, fk_gqf_result *res, cudaStream_t st) {
+  Scratch S(st);
+  const int64_t nqr = g->quotient_regions;
+  int64_t *rb = S.get<int64_t>(nqr + 1);
+  if (S.err) return -(int)S.err;
+  k_region_bounds<<<blocks_for(nqr + 1), 256, 0, st>>>(fps_s, n, g->r + kRegionBits, nqr, rb);
+  std::vector<int64_t> hrb(nqr + 1);
+  FK_CU(cudaMemcpyAsync(hrb.data(), rb, (nqr + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  // the copy the regions are applied to
+  FK_CU(cudaMemcpyAsync(nxt->slots, cur->slots, (size_t)g->phys * sizeof(S_t), cudaMemcpyDeviceToDevice, st));
+  FK_CU(cudaMemcpyAsync(nxt->occupieds, cur->occupieds, (size_t)(g->phys >> 6) * 8, cudaMemcpyDeviceToDevice, st));
+  FK_CU(cudaMemcpyAsync(nxt->runends, cur->runends, (size_t)(g->phys >> 6) * 8, cudaMemcpyDeviceToDevice, st));
+  FK_CU(cudaMemcpyAsync(nxt->offsets, cur->offsets, (size_t)g->num_regions * 4, cudaMemcpyDeviceToDevice, st));
+  FK_CU(cudaMemcpyAsync(nxt->stats, cur->stats, 3 * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+  FK_CU(cudaStreamSynchronize(st));
+  std::vector<int32_t> lists[2];
+  for (int64_t r = 0; r < nqr; r++)
+    if (hrb[r + 1] > hrb[r]) lists[r & 1].push_back((int32_t)r);
+  const size_t most = lists[0].size() > lists[1].size() ? lists[0].size() : lists[1].size();
+  int32_t *dlist = S.get<int32_t>(most), *fail = S.get<int32_t>(most);
+  int32_t *scr = S.get<int32_t>(most * SeqGqf<S_t>::kGapCap);
+  unsigned long long *moved = S.get<unsigned long long>(1);
+  if (S.err) return -(int)S.err;
+  FK_CU(cudaMemsetAsync(moved, 0, sizeof(unsigned long long), st));
+  GqfDev T1 = make_dev(g, nxt);
+  for (int parity = 0; parity < 2; parity++) {
+    const std::vector<int32_t> &L = lists[parity];
+    if (L.empty()) continue;
+    FK_CU(cudaMemcpyAsync(dlist, L.data(), L.size() * 4, cudaMemcpyHostToDevice, st));
+    FK_CU(cudaMemsetAsync(fail, 0, L.size() * 4, st));
+    k_gqf_insert_regions<S_t><<<blocks_for((int64_t)L.size(), 64), 64, 0, st>>>(T1, fps_s, del_s, rb, dlist,
+                                                                            (int64_t)L.size(), scr, fail, moved);
+    FK_CHECK_LAUNCH();
+    std::vector<int32_t> hf(L.size());
+    FK_CU(cudaMemcpyAsync(hf.data(), fail, L.size() * 4, cudaMemcpyDeviceToHost, st));
+    FK_CU(cudaStreamSynchronize(st));
+    for (int32_t f : hf)
+      if (f) return f < 0 ? FK_E_INVARIANT : 1;
+  }
+  unsigned long long hm = 0;
+  FK_CU(cudaMemcpyAsync(&hm, moved, sizeof(hm), cudaMemcpyDeviceToHost, st));
+  int rc = rebuild_index(g, nxt, st);
+  if (rc) return rc;
+  FK_CU(cudaStreamSynchronize(st));
+  res->swapped = 1;
+  res->shifted = (int64_t)hm;
+  return 0;
+}
+
 template <typename S_t>
 int count_t(const fk_gqf_geom *g, const fk_gqf_tables *t, const uint64_t *keys, int keys_are_fps, int64_t n,
             uint64_t *counts, cudaStream_t st) {
@@ -256,6 +321,14 @@ int apply_t(const fk_gqf_geom *g, const fk_gqf_tables *cur, const fk_gqf_tables 
   int64_t m = 0;
   FK_CU(cudaMemcpyAsync(&m, d_num, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   FK_CU(cudaStreamSynchronize(st));
+
+  // 4'. small insert batches: region-local sequential inserts on a copy of
+  // the table (the canonical result whenever nothing overflows); any
+  // capacity failure discards the copy and falls through to the full path
+  if (!is_del && !(flags & (kApplyDry | kApplyForceExact)) && m > 0 && m <= small_batch_limit(g)) {
+    int rc = apply_small_t<S_t>(g, cur, nxt, uniq, sums, m, res, st);  // one insert per fingerprint
+    if (rc <= 0) return rc;  // done (0) or an error (< 0); 1 = fall through
+  }
 
   // 5-6. old counts through the (pure) count query, new absolute counts
   uint64_t *c_old = S.get<uint64_t>(m), *c_new = S.get<uint64_t>(m);

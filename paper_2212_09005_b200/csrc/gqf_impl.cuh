@@ -679,6 +679,33 @@ __global__ void k_gqf_exact_regions(GqfDev T, const uint64_t *__restrict__ fps_s
   }
 }
 
+// Small batches: the reference's region-parallel insert (gqf.py:309-353,
+// even regions then odd ones) on the listed regions only, one thread per
+// region.  Without a capacity error its result is the canonical table
+// (SURVEY H2), at a cost proportional to the batch, not the table.
+template <typename S>
+__global__ void k_gqf_insert_regions(GqfDev T, const uint64_t *__restrict__ fps_s,
+                                     const uint64_t *__restrict__ deltas_s, const int64_t *__restrict__ rb,
+                                     const int32_t *__restrict__ list, int64_t nlist, int32_t *scratch,
+                                     int32_t *__restrict__ fail_code, unsigned long long *__restrict__ moved) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nlist; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = list[t];
+    SeqGqf<S> G{reinterpret_cast<S *>(T.slots), T.occ, T.run, T.offs, T.stats, T.phys, T.r,
+                scratch + (size_t)t * SeqGqf<S>::kGapCap};
+    unsigned long long mv_total = 0;
+    for (int64_t k = rb[g]; k < rb[g + 1]; k++) {
+      int64_t mv;
+      int code = G.insert_one(T.max_occ, fps_s[k], deltas_s ? deltas_s[k] : 1ull, &mv);
+      if (code) {
+        fail_code[t] = code;
+        break;
+      }
+      mv_total += (unsigned long long)mv;
+    }
+    if (mv_total) atomicAdd(moved, mv_total);
+  }
+}
+
 __global__ void k_region_bounds(const uint64_t *__restrict__ fps_s, int64_t n, int shift, int64_t nqr,
                                 int64_t *__restrict__ rb) {
   for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g <= nqr; g += (int64_t)gridDim.x * blockDim.x) {

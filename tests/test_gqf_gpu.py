@@ -364,3 +364,29 @@ def test_shift_bound_inside_large_point_batch(oracle):
     with pytest.raises(CapacityError, match="hard bound"):
         g.insert_many(keys, cnt)
     same_image(g, o)
+
+
+@pytest.mark.parametrize("r", [8, 16])
+def test_small_batches_region_path_equals_oracle(oracle, monkeypatch, r):
+    """Batches with few distinct fingerprints take the region-local insert
+    path (k_gqf_insert_regions on a copy of the table); the image after every
+    batch must equal the oracle's, with the full rebuild path as control."""
+    from paper_2212_09005_b200 import Gqf
+    rng = np.random.default_rng(20 + r)
+    for limit in ("0", "100000"):
+        monkeypatch.setenv("FK_GQF_SMALL", limit)
+        g = Gqf(q=16, r=r, seed=7)
+        o = _oracle(g, oracle)
+        for step in range(12):
+            keys = rng.integers(0, 2 ** 60, int(rng.integers(1, 3000)), dtype=np.uint64)
+            if step % 3 == 1:
+                keys = np.concatenate([keys, keys[: len(keys) // 2]])  # repeats in the batch
+            cnt = rng.integers(1, 40, len(keys)).astype(np.uint64) if step % 2 else None
+            if step % 4 == 3:
+                g.insert_many(keys, cnt)
+                o.insert_many(keys, cnt)
+            else:
+                g.bulk_insert(keys, cnt)
+                o.bulk_insert(keys, cnt)
+            same_image(g, o)
+        g.validate()
