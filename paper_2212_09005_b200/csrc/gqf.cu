@@ -263,6 +263,52 @@ int apply_small_t(const fk_gqf_geom *g, const fk_gqf_tables *cur, const fk_gqf_t
   return 0;
 }
 
+// Region-local delete of a sorted batch, in place on `cur` (deletes raise
+// no capacity errors); found flags at the items' input positions.
+template <typename S_t>
+int apply_small_delete_t(const fk_gqf_geom *g, const fk_gqf_tables *cur, const uint64_t *fps_s,
+                         const uint64_t *del_s, const uint32_t *idx_s, int64_t n, int order, uint8_t *found,
+                         fk_gqf_result *res, cudaStream_t st) {
+  Scratch S(st);
+  const int64_t nqr = g->quotient_regions;
+  int64_t *rb = S.get<int64_t>(nqr + 1);
+  if (S.err) return -(int)S.err;
+  k_region_bounds<<<blocks_for(nqr + 1), 256, 0, st>>>(fps_s, n, g->r + kRegionBits, nqr, rb);
+  std::vector<int64_t> hrb(nqr + 1);
+  FK_CU(cudaMemcpyAsync(hrb.data(), rb, (nqr + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  FK_CU(cudaStreamSynchronize(st));
+  std::vector<int32_t> lists[2];
+  for (int64_t r = 0; r < nqr; r++)
+    if (hrb[r + 1] > hrb[r]) lists[r & 1].push_back((int32_t)r);
+  const size_t most = lists[0].size() > lists[1].size() ? lists[0].size() : lists[1].size();
+  int32_t *dlist = S.get<int32_t>(most), *fail = S.get<int32_t>(most);
+  unsigned long long *moved = S.get<unsigned long long>(1);
+  if (S.err) return -(int)S.err;
+  FK_CU(cudaMemsetAsync(moved, 0, sizeof(unsigned long long), st));
+  GqfDev T0 = make_dev(g, cur);
+  for (int parity = 0; parity < 2; parity++) {
+    const std::vector<int32_t> &L = lists[parity];
+    if (L.empty()) continue;
+    FK_CU(cudaMemcpyAsync(dlist, L.data(), L.size() * 4, cudaMemcpyHostToDevice, st));
+    FK_CU(cudaMemsetAsync(fail, 0, L.size() * 4, st));
+    k_gqf_delete_regions<S_t><<<blocks_for((int64_t)L.size(), 64), 64, 0, st>>>(
+        T0, fps_s, del_s, idx_s, rb, dlist, (int64_t)L.size(), order == FK_ORDER_BULK ? 1 : 0, found, fail, moved);
+    FK_CHECK_LAUNCH();
+    std::vector<int32_t> hf(L.size());
+    FK_CU(cudaMemcpyAsync(hf.data(), fail, L.size() * 4, cudaMemcpyDeviceToHost, st));
+    FK_CU(cudaStreamSynchronize(st));
+    for (int32_t f : hf)
+      if (f) return FK_E_INVARIANT;
+  }
+  unsigned long long hm = 0;
+  FK_CU(cudaMemcpyAsync(&hm, moved, sizeof(hm), cudaMemcpyDeviceToHost, st));
+  int rc = rebuild_index(g, cur, st);
+  if (rc) return rc;
+  FK_CU(cudaStreamSynchronize(st));
+  res->shifted = (int64_t)hm;
+  return 0;
+}
+
 template <typename S_t>
 int count_t(const fk_gqf_geom *g, const fk_gqf_tables *t, const uint64_t *keys, int keys_are_fps, int64_t n,
             uint64_t *counts, cudaStream_t st) {
@@ -329,6 +375,9 @@ int apply_t(const fk_gqf_geom *g, const fk_gqf_tables *cur, const fk_gqf_tables 
     int rc = apply_small_t<S_t>(g, cur, nxt, uniq, sums, m, res, st);  // one insert per fingerprint
     if (rc <= 0) return rc;  // done (0) or an error (< 0); 1 = fall through
   }
+
+  if (is_del && !(flags & (kApplyDry | kApplyForceExact)) && n <= small_batch_limit(g))
+    return apply_small_delete_t<S_t>(g, cur, fps_s, del_s, idx_s, n, order, found, res, st);
 
   // 5-6. old counts through the (pure) count query, new absolute counts
   uint64_t *c_old = S.get<uint64_t>(m), *c_new = S.get<uint64_t>(m);

@@ -625,6 +625,96 @@ struct SeqGqf {
     *moved_out = moved;
     return 0;
   }
+
+  // Remove slots [rs, re] of quot's run [start, end], left-compacting the
+  // cluster (pk:659-715).  Returns the furthest old slot touched, -1 on an
+  // invariant violation; *moved gets the number of slots moved.
+  __device__ int64_t remove_slots(int64_t quot, int64_t start, int64_t end, int64_t rs, int64_t re, int64_t hard,
+                                  int64_t *moved) const {
+    const int64_t L = re - rs + 1;
+    const bool emptied = L == end - start + 1;
+    int64_t shifted = 0;
+    for (int64_t i = 0; i < end - re; i++) slots[rs + i] = slots[re + 1 + i];
+    shifted += end - re;
+    setb(run, end, 0);
+    int64_t wp;
+    if (emptied) {
+      setb(occ, quot, 0);
+      wp = start;
+    } else {
+      setb(run, end - L, 1);
+      wp = end - L + 1;
+    }
+    int64_t prev_old_end = end, last_old_end = end, nq = quot;
+    for (;;) {
+      nq = select_after_dev(occ, nq, 1, hard);
+      if (nq < 0 || nq > prev_old_end + 1) break;  // a gap: the cluster ends
+      const int64_t s2 = prev_old_end + 1;
+      const int64_t e2 = select_after_dev(run, s2 - 1, 1, hard);
+      if (e2 == -2) return -1;
+      const int64_t ns2 = nq > wp ? nq : wp;
+      if (ns2 == s2) break;
+      for (int64_t i = wp; i < ns2; i++) {  // skipped positions are freed for good
+        slots[i] = 0;
+        setb(run, i, 0);
+      }
+      const int64_t n2 = e2 - s2 + 1;
+      for (int64_t i = 0; i < n2; i++) slots[ns2 + i] = slots[s2 + i];
+      setb(run, e2, 0);
+      setb(run, ns2 + n2 - 1, 1);
+      shifted += n2;
+      wp = ns2 + n2;
+      prev_old_end = e2;
+      last_old_end = e2;
+    }
+    for (int64_t i = wp; i <= last_old_end; i++) {
+      slots[i] = 0;
+      setb(run, i, 0);
+    }
+    *moved = shifted;
+    return last_old_end;
+  }
+
+  // pk:718-752 -> found (0/1), -9 on an invariant violation
+  __device__ int delete_one(uint64_t fp, uint64_t delta, int64_t *moved_out) {
+    const int64_t quot = (int64_t)(fp >> r);
+    const uint64_t rem = fp & ((1ull << r) - 1);
+    const int64_t g = quot >> kRegionBits;
+    int64_t hard = (g + 2) << kRegionBits;
+    if (hard > phys) hard = phys;
+    *moved_out = 0;
+    if (!bit_at(occ, quot)) return 0;
+    int64_t st, en, gs, ge, sp;
+    uint64_t c;
+    if (!run_interval(quot, &st, &en)) return -9;
+    if (!find_group(st, en, rem, &gs, &ge, &c, &sp)) return -9;
+    if (gs < 0) return 0;
+    const uint64_t take = delta < c ? delta : c;
+    const uint64_t c2 = c - take;
+    int64_t rs, re;
+    if (c2 > 0) {
+      const int64_t L = (int64_t)enc_len(rem, c2, r);
+      const int64_t diff = (ge - gs + 1) - L;
+      enc_write<S>(slots, gs, rem, c2, r);
+      add_stats(0, -(int64_t)take, 0);
+      if (diff == 0) return 1;
+      rs = gs + L;
+      re = ge;
+    } else {
+      add_stats(0, -(int64_t)take, -1);
+      rs = gs;
+      re = ge;
+    }
+    int64_t moved = 0;
+    const int64_t last = remove_slots(quot, st, en, rs, re, hard, &moved);
+    if (last < 0) return -9;
+    add_stats(-(re - rs + 1), 0, 0);
+    const int64_t boundary = (g + 1) << kRegionBits;
+    if (boundary < phys && last >= boundary)
+      if (!refresh_offset(g + 1)) return -9;
+    *moved_out = moved;
+    return 1;
+  }
 };
 
 // insert_many semantics: one thread, input order, stop at the first failure
@@ -700,6 +790,36 @@ __global__ void k_gqf_insert_regions(GqfDev T, const uint64_t *__restrict__ fps_
         fail_code[t] = code;
         break;
       }
+      mv_total += (unsigned long long)mv;
+    }
+    if (mv_total) atomicAdd(moved, mv_total);
+  }
+}
+
+// Small delete batches: one thread per touched region of one parity,
+// applying the region's sorted items in the facade's order -- descending for
+// bulk_delete (gqf.py:317-325), ascending (input order) for delete_many --
+// and recording each item's found flag at its input position.
+template <typename S>
+__global__ void k_gqf_delete_regions(GqfDev T, const uint64_t *__restrict__ fps_s, const uint64_t *__restrict__ deltas_s,
+                                     const uint32_t *__restrict__ idx_s, const int64_t *__restrict__ rb,
+                                     const int32_t *__restrict__ list, int64_t nlist, int descending,
+                                     uint8_t *__restrict__ found, int32_t *__restrict__ fail_code,
+                                     unsigned long long *__restrict__ moved) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nlist; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = list[t];
+    SeqGqf<S> G{reinterpret_cast<S *>(T.slots), T.occ, T.run, T.offs, T.stats, T.phys, T.r, nullptr};
+    unsigned long long mv_total = 0;
+    const int64_t lo = rb[g], hi = rb[g + 1];
+    for (int64_t u = 0; u < hi - lo; u++) {
+      const int64_t k = descending ? hi - 1 - u : lo + u;
+      int64_t mv;
+      const int f = G.delete_one(fps_s[k], deltas_s[k], &mv);
+      if (f < 0) {
+        fail_code[t] = f;
+        break;
+      }
+      if (found) found[idx_s[k]] = (uint8_t)f;
       mv_total += (unsigned long long)mv;
     }
     if (mv_total) atomicAdd(moved, mv_total);

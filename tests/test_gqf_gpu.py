@@ -390,3 +390,34 @@ def test_small_batches_region_path_equals_oracle(oracle, monkeypatch, r):
                 o.bulk_insert(keys, cnt)
             same_image(g, o)
         g.validate()
+
+
+@pytest.mark.parametrize("r", [8, 16])
+def test_small_delete_batches_region_path_equals_oracle(oracle, monkeypatch, r):
+    """Small delete batches run the reference's sequential delete per region
+    (descending for bulk_delete, input order for delete_many): found flags
+    and images equal the oracle's, with the rebuild path as control."""
+    from paper_2212_09005_b200 import Gqf
+    for limit in ("0", "100000"):
+        rng = np.random.default_rng(40 + r)
+        monkeypatch.setenv("FK_GQF_SMALL", limit)
+        g = Gqf(q=16, r=r, seed=9)
+        o = _oracle(g, oracle)
+        pool = rng.integers(0, 2 ** 60, 20_000, dtype=np.uint64)
+        cnt = rng.integers(1, 300, len(pool)).astype(np.uint64)
+        monkeypatch.setenv("FK_GQF_SMALL", "0")  # build the table through the rebuild path
+        g.bulk_insert(pool, cnt)
+        o.bulk_insert(pool, cnt)
+        monkeypatch.setenv("FK_GQF_SMALL", limit)
+        same_image(g, o)
+        for step in range(10):
+            d = pool[rng.integers(0, len(pool), int(rng.integers(1, 2000)))]
+            d = np.concatenate([d, d[: len(d) // 3], rng.integers(0, 2 ** 60, 50, dtype=np.uint64)])
+            dc = rng.integers(1, 200, len(d)).astype(np.uint64) if step % 2 else None
+            if step % 3 == 2:
+                got, want = g.delete_many(d, dc), o.delete_many(d, dc)
+            else:
+                got, want = g.bulk_delete(d, dc), o.bulk_delete(d, dc)
+            assert np.array_equal(np.asarray(got).astype(bool), np.asarray(want).astype(bool)), (limit, step)
+            same_image(g, o)
+        g.validate()
