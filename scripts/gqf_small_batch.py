@@ -31,9 +31,14 @@ def main():
                 g.insert_many(keys[i * bs:(i + 1) * bs])
             torch.cuda.synchronize()
             ms = (time.perf_counter() - t) / 10 * 1e3
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            for i in range(10):
+                g.bulk_delete(keys[i * bs:(i + 1) * bs])
+            torch.cuda.synchronize()
+            dms = (time.perf_counter() - t) / 10 * 1e3
             print(json.dumps({"q": q, "path": "full rebuild" if limit == "0" else "region-local",
-                              "batch": bs, "ms_per_call": ms}), flush=True)
-            g.bulk_delete(keys)
+                              "batch": bs, "insert_ms_per_call": ms, "delete_ms_per_call": dms}), flush=True)
 
 
 if __name__ == "__main__":

@@ -403,8 +403,8 @@ def test_small_delete_batches_region_path_equals_oracle(oracle, monkeypatch, r):
         monkeypatch.setenv("FK_GQF_SMALL", limit)
         g = Gqf(q=16, r=r, seed=9)
         o = _oracle(g, oracle)
-        pool = rng.integers(0, 2 ** 60, 20_000, dtype=np.uint64)
-        cnt = rng.integers(1, 300, len(pool)).astype(np.uint64)
+        pool = rng.integers(0, 2 ** 60, 10_000, dtype=np.uint64)
+        cnt = rng.integers(1, 50, len(pool)).astype(np.uint64)
         monkeypatch.setenv("FK_GQF_SMALL", "0")  # build the table through the rebuild path
         g.bulk_insert(pool, cnt)
         o.bulk_insert(pool, cnt)
