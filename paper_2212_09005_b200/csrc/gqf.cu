@@ -1,6 +1,8 @@
 // gqf.cu -- host side of the GQF C ABI: count / find_run / index rebuild /
 // insert+delete batches (canonical rebuild, exact sequential fallback).
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
 #include <stdlib.h>
 
 #include <vector>
@@ -62,6 +64,45 @@ cudaError_t cub_sort_keys(Scratch &S, const uint64_t *kin, uint64_t *kout, int64
   void *tmp = S.get<char>(tb);
   if (!tmp) return S.err;
   return cub::DeviceRadixSort::SortKeys(tmp, tb, kin, kout, n, 0, end_bit, S.st);
+}
+
+cudaError_t cub_sort_keys_u32(Scratch &S, const uint32_t *kin, uint32_t *kout, int64_t n, int end_bit) {
+  size_t tb = 0;
+  cudaError_t e = cub::DeviceRadixSort::SortKeys(nullptr, tb, kin, kout, n, 0, end_bit, S.st);
+  if (e) return e;
+  void *tmp = S.get<char>(tb);
+  if (!tmp) return S.err;
+  return cub::DeviceRadixSort::SortKeys(tmp, tb, kin, kout, n, 0, end_bit, S.st);
+}
+
+cudaError_t cub_sort_pairs_u8_u32(Scratch &S, const uint8_t *kin, uint8_t *kout, const uint32_t *vin, uint32_t *vout,
+                                  int64_t n, int end_bit) {
+  size_t tb = 0;
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, tb, kin, kout, vin, vout, n, 0, end_bit, S.st);
+  if (e) return e;
+  void *tmp = S.get<char>(tb);
+  if (!tmp) return S.err;
+  return cub::DeviceRadixSort::SortPairs(tmp, tb, kin, kout, vin, vout, n, 0, end_bit, S.st);
+}
+
+// fingerprint i of a split sort: (high byte << 32) | low word
+struct WidenSplit {
+  const uint8_t *hi;
+  const uint32_t *lo;
+  __host__ __device__ uint64_t operator()(int64_t i) const {
+    return ((uint64_t)(hi ? hi[i] : 0) << 32) | (uint64_t)lo[i];
+  }
+};
+
+cudaError_t cub_rle_counts_split(Scratch &S, const uint8_t *hi, const uint32_t *lo, uint64_t *uniq, uint64_t *counts,
+                                 int64_t *num, int64_t n) {
+  auto it = thrust::make_transform_iterator(thrust::counting_iterator<int64_t>(0), WidenSplit{hi, lo});
+  size_t tb = 0;
+  cudaError_t e = cub::DeviceRunLengthEncode::Encode(nullptr, tb, it, uniq, counts, num, n, S.st);
+  if (e) return e;
+  void *tmp = S.get<char>(tb);
+  if (!tmp) return S.err;
+  return cub::DeviceRunLengthEncode::Encode(tmp, tb, it, uniq, counts, num, n, S.st);
 }
 
 cudaError_t cub_rle_counts(Scratch &S, const uint64_t *keys, uint64_t *uniq, uint64_t *counts, int64_t *num,
@@ -343,26 +384,64 @@ int apply_t(const fk_gqf_geom *g, const fk_gqf_tables *cur, const fk_gqf_tables 
   res->shifted = 0;
 
   // 1-3. hash, stable sort by fingerprint, deltas in sorted order
-  uint64_t *fps = S.get<uint64_t>(n), *fps_s = S.get<uint64_t>(n), *del_s = S.get<uint64_t>(n);
-  uint32_t *idx = S.get<uint32_t>(n), *idx_s = S.get<uint32_t>(n);
-  if (S.err) return -(int)S.err;
-  k_hash_fps<<<blocks_for(n), 256, 0, st>>>(keys, keys_are_fps, g->seed, fmask, n, fps, idx);
   // Plain counted inserts (no deltas: every occurrence adds one) need
-  // neither the input permutation nor delta sums: a keys-only sort and a
-  // run-length count move 2/3 of the bytes of the pairs sort + reduce.
+  // neither the input permutation nor delta sums.  Their fingerprints
+  // (q + r <= 40 bits) are sorted as u32 low words, after one pass that
+  // buckets them by the <= 8 high bits: 42 instead of 80 bytes moved per
+  // occurrence for q + r = 36; run-length counts then read (high, low) pairs.
   const bool plain_ins = !is_del && deltas == nullptr;
+  const bool split = plain_ins && qr <= 40;
+  uint64_t *fps = nullptr, *fps_s = nullptr, *del_s = nullptr;
+  uint32_t *idx = nullptr, *idx_s = nullptr;
+  uint8_t *hi_s = nullptr;
+  uint32_t *lo_s = nullptr;
   uint64_t *uniq = S.get<uint64_t>(n), *sums = S.get<uint64_t>(n);
   int64_t *d_num = S.get<int64_t>(4);
   if (S.err) return -(int)S.err;
-  if (plain_ins) {
-    FK_CU(cub_sort_keys(S, fps, fps_s, n, qr));
-    FK_CU(cub_rle_counts(S, fps_s, uniq, sums, d_num, n));
+  if (split) {
+    uint32_t *lo = S.get<uint32_t>(n);
+    lo_s = S.get<uint32_t>(n);
+    uint8_t *hi = nullptr;
+    if (qr > 32) {
+      hi = S.get<uint8_t>(n);
+      hi_s = S.get<uint8_t>(n);
+    }
+    if (S.err) return -(int)S.err;
+    k_hash_split<<<blocks_for(n), 256, 0, st>>>(keys, keys_are_fps, g->seed, fmask, n, hi, lo);
+    if (qr <= 32) {
+      FK_CU(cub_sort_keys_u32(S, lo, lo_s, n, qr));
+    } else {
+      uint32_t *lo_p = S.get<uint32_t>(n);
+      const int nseg = 1 << (qr - 32);
+      int64_t *bounds = S.get<int64_t>(nseg + 1);
+      if (S.err) return -(int)S.err;
+      FK_CU(cub_sort_pairs_u8_u32(S, hi, hi_s, lo, lo_p, n, qr - 32));
+      k_u8_bounds<<<1, 256, 0, st>>>(hi_s, n, nseg, bounds);
+      std::vector<int64_t> hb(nseg + 1);
+      FK_CU(cudaMemcpyAsync(hb.data(), bounds, (nseg + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+      FK_CU(cudaStreamSynchronize(st));
+      for (int sgi = 0; sgi < nseg; sgi++)
+        if (hb[sgi + 1] > hb[sgi]) FK_CU(cub_sort_keys_u32(S, lo_p + hb[sgi], lo_s + hb[sgi], hb[sgi + 1] - hb[sgi], 32));
+    }
+    FK_CU(cub_rle_counts_split(S, hi_s, lo_s, uniq, sums, d_num, n));
   } else {
-    FK_CU(cub_sort_pairs(S, fps, fps_s, idx, idx_s, n, qr));
-    const uint64_t dflt = is_del ? (1ull << 63) : 1ull;
-    k_gather_u64<<<blocks_for(n), 256, 0, st>>>(deltas, idx_s, dflt, n, del_s);
-    // 4. unique fingerprints with saturating delta sums
-    FK_CU(cub_reduce_by_key(S, fps_s, uniq, del_s, sums, d_num, n));
+    fps = S.get<uint64_t>(n);
+    fps_s = S.get<uint64_t>(n);
+    del_s = S.get<uint64_t>(n);
+    idx = S.get<uint32_t>(n);
+    idx_s = S.get<uint32_t>(n);
+    if (S.err) return -(int)S.err;
+    k_hash_fps<<<blocks_for(n), 256, 0, st>>>(keys, keys_are_fps, g->seed, fmask, n, fps, idx);
+    if (plain_ins) {
+      FK_CU(cub_sort_keys(S, fps, fps_s, n, qr));
+      FK_CU(cub_rle_counts(S, fps_s, uniq, sums, d_num, n));
+    } else {
+      FK_CU(cub_sort_pairs(S, fps, fps_s, idx, idx_s, n, qr));
+      const uint64_t dflt = is_del ? (1ull << 63) : 1ull;
+      k_gather_u64<<<blocks_for(n), 256, 0, st>>>(deltas, idx_s, dflt, n, del_s);
+      // 4. unique fingerprints with saturating delta sums
+      FK_CU(cub_reduce_by_key(S, fps_s, uniq, del_s, sums, d_num, n));
+    }
   }
   int64_t m = 0;
   FK_CU(cudaMemcpyAsync(&m, d_num, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
@@ -535,6 +614,12 @@ int apply_t(const fk_gqf_geom *g, const fk_gqf_tables *cur, const fk_gqf_tables 
       int32_t *scr = S.get<int32_t>(SeqGqf<S_t>::kGapCap);
       int64_t *out3 = S.get<int64_t>(4);
       if (S.err) return -(int)S.err;
+      if (!fps) {  // the split sort never materialised the input-order fingerprints
+        fps = S.get<uint64_t>(n);
+        idx = S.get<uint32_t>(n);
+        if (S.err) return -(int)S.err;
+        k_hash_fps<<<blocks_for(n), 256, 0, st>>>(keys, keys_are_fps, g->seed, fmask, n, fps, idx);
+      }
       k_gqf_exact_seq<S_t><<<1, 1, 0, st>>>(T0, fps, deltas, n, scr, out3);
       int64_t h3[3];
       FK_CU(cudaMemcpyAsync(h3, out3, 3 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
@@ -553,7 +638,16 @@ int apply_t(const fk_gqf_geom *g, const fk_gqf_tables *cur, const fk_gqf_tables 
       if (S.err) return -(int)S.err;
       FK_CU(cudaMemsetAsync(fail, 0, nqr * sizeof(int32_t), st));
       FK_CU(cudaMemsetAsync(moved, 0, sizeof(unsigned long long), st));
-      if (plain_ins) k_gather_u64<<<blocks_for(n), 256, 0, st>>>(nullptr, idx_s, 1ull, n, del_s);  // all ones
+      if (plain_ins) {
+        if (!fps_s) {  // sorted occurrences from the split sort
+          fps_s = S.get<uint64_t>(n);
+          if (S.err) return -(int)S.err;
+          k_widen_split<<<blocks_for(n), 256, 0, st>>>(hi_s, lo_s, n, fps_s);
+        }
+        if (!del_s) del_s = S.get<uint64_t>(n);
+        if (S.err) return -(int)S.err;
+        k_gather_u64<<<blocks_for(n), 256, 0, st>>>(nullptr, nullptr, 1ull, n, del_s);  // all ones
+      }
       k_region_bounds<<<blocks_for(nqr + 1), 256, 0, st>>>(fps_s, n, g->r + kRegionBits, nqr, rb);
       // the ceiling check reads the shared occupancy counter, so when it can
       // trigger, regions run one after another in the reference's workers=1

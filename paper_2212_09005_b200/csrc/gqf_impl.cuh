@@ -218,6 +218,35 @@ __global__ void k_hash_fps(const uint64_t *__restrict__ keys, int keys_are_fps, 
   }
 }
 
+// fingerprints split into a high byte (bits 32..39, when q + r > 32) and
+// the low 32 bits, for the split sort of plain inserts
+__global__ void k_hash_split(const uint64_t *__restrict__ keys, int keys_are_fps, uint64_t seed, uint64_t fmask,
+                             int64_t n, uint8_t *__restrict__ hi, uint32_t *__restrict__ lo) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t fp = (keys_are_fps ? keys[i] : mix64(keys[i] ^ seed)) & fmask;
+    if (hi) hi[i] = (uint8_t)(fp >> 32);
+    lo[i] = (uint32_t)fp;
+  }
+}
+
+__global__ void k_widen_split(const uint8_t *__restrict__ hi, const uint32_t *__restrict__ lo, int64_t n,
+                              uint64_t *__restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = ((uint64_t)(hi ? hi[i] : 0) << 32) | (uint64_t)lo[i];
+}
+
+// bounds[v] = first index of value v in the sorted high bytes (v <= nseg)
+__global__ void k_u8_bounds(const uint8_t *__restrict__ hs, int64_t n, int nseg, int64_t *__restrict__ bounds) {
+  for (int v = threadIdx.x; v <= nseg; v += blockDim.x) {
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+      int64_t mid = (lo + hi) >> 1;
+      if ((int)hs[mid] < v) lo = mid + 1; else hi = mid;
+    }
+    bounds[v] = lo;
+  }
+}
+
 __global__ void k_gather_u64(const uint64_t *__restrict__ src, const uint32_t *__restrict__ idx,
                              uint64_t dflt, int64_t n, uint64_t *__restrict__ dst) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
