@@ -421,3 +421,35 @@ def test_small_delete_batches_region_path_equals_oracle(oracle, monkeypatch, r):
             assert np.array_equal(np.asarray(got).astype(bool), np.asarray(want).astype(bool)), (limit, step)
             same_image(g, o)
         g.validate()
+
+
+@pytest.mark.parametrize("order", ["point", "bulk"])
+def test_small_batches_hitting_capacity_fall_back_exactly(oracle, monkeypatch, order):
+    """A small batch that overflows (load ceiling) on the region-local path
+    leaves the table untouched there and is replayed by the exact path: the
+    partial image equals the reference's, batch after batch."""
+    from paper_2212_09005_b200 import CapacityError, Gqf
+    rng = np.random.default_rng(77)
+    g = Gqf(q=12, r=8, seed=1)
+    o = _oracle(g, oracle)
+    base = rng.integers(0, 2 ** 60, 3700, dtype=np.uint64)
+    g.bulk_insert(base)
+    o.bulk_insert(base)
+    monkeypatch.setenv("FK_GQF_SMALL", "100000")
+    raised = 0
+    for step in range(40):
+        keys = rng.integers(0, 2 ** 60, 12, dtype=np.uint64)
+        cnt = rng.integers(1, 4, 12).astype(np.uint64)
+        try:
+            if order == "point":
+                g.insert_many(keys, cnt)
+            else:
+                g.bulk_insert(keys, cnt)
+        except CapacityError:
+            raised += 1
+        if order == "point":
+            o.insert_many(keys, cnt)
+        else:
+            o.bulk_insert(keys, cnt)
+        same_image(g, o)
+    assert raised > 0
