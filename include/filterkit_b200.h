@@ -261,6 +261,30 @@ int fk_shard_partition(const uint64_t *keys, const uint64_t *vals, int64_t n, ui
  * back from the owners, restored to input order.  Asynchronous. */
 int fk_shard_unpermute(const uint32_t *perm, const void *src, int64_t n, int elem_bytes, void *dst, void *stream);
 
+/* Fused exchange over peer memory (CUDA IPC mappings; NVLink / NVSwitch
+ * stores between GPUs) -- the data path of the sharded filters without a
+ * collective library.  fk_shard_partition with keys_out = NULL only computes
+ * perm and counts; fk_shard_dispatch then writes key perm[i] of owner o
+ * straight into peer_keys[o][dst_off[o] + i - seg_start[o]] (and its value,
+ * and the tag (rank << 32) | input index into peer_src[o]); after the
+ * owners ran their local op, fk_shard_combine writes each result into
+ * peer_out[tag >> 32][tag & 0xffffffff].  Pointer arrays are DEVICE arrays
+ * of G entries.  Replaces the all-to-all exchange of SURVEY 8(e). */
+int fk_shard_dispatch(const uint64_t *keys, const uint64_t *vals, const uint32_t *perm, int64_t n, uint64_t seed,
+                      int shift, int log2_shards, uint32_t rank, const int64_t *seg_start, const int64_t *dst_off,
+                      uint64_t *const *peer_keys, uint64_t *const *peer_vals, uint64_t *const *peer_src,
+                      void *stream);
+int fk_shard_combine(const uint64_t *src, const void *res, int64_t m, int elem_bytes, void *const *peer_out,
+                     void *stream);
+
+/* Whole-allocation device buffers shareable with the other ranks through
+ * CUDA IPC (handles are 64 bytes; open the other ranks' handles, not your own). */
+int fk_ipc_alloc(int64_t bytes, void **ptr);
+int fk_ipc_free(void *ptr);
+int fk_ipc_get_handle(void *ptr, void *handle_out);
+int fk_ipc_open(const void *handle, void **ptr);
+int fk_ipc_close(void *ptr);
+
 #ifdef __cplusplus
 }
 #endif

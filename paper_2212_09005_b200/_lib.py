@@ -78,6 +78,14 @@ _SIGS = {
     "fk_btcf_merge_lists": (c_i32, [ctypes.POINTER(BtcfGeom), c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "fk_shard_partition": (c_i32, [c_vp, c_vp, c_i64, c_u64, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "fk_shard_unpermute": (c_i32, [c_vp, c_vp, c_i64, c_i32, c_vp, c_vp]),
+    "fk_shard_dispatch": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_u64, c_i32, c_i32, ctypes.c_uint32, c_vp, c_vp, c_vp,
+                                  c_vp, c_vp, c_vp]),
+    "fk_shard_combine": (c_i32, [c_vp, c_vp, c_i64, c_i32, c_vp, c_vp]),
+    "fk_ipc_alloc": (c_i32, [c_i64, ctypes.POINTER(c_vp)]),
+    "fk_ipc_free": (c_i32, [c_vp]),
+    "fk_ipc_get_handle": (c_i32, [c_vp, c_vp]),
+    "fk_ipc_open": (c_i32, [c_vp, ctypes.POINTER(c_vp)]),
+    "fk_ipc_close": (c_i32, [c_vp]),
     "fk_gqf_count": (c_i32, [ctypes.POINTER(GqfGeom), ctypes.POINTER(GqfTables), c_vp, c_i32, c_i64, c_vp, c_vp]),
     "fk_gqf_find_run": (c_i32, [ctypes.POINTER(GqfGeom), ctypes.POINTER(GqfTables), c_vp, c_i64, c_vp, c_vp]),
     "fk_gqf_rebuild_index": (c_i32, [ctypes.POINTER(GqfGeom), ctypes.POINTER(GqfTables), c_vp]),

@@ -14,6 +14,7 @@
 // all-to-all.  fk_shard_unpermute_* scatter the per-key results that come
 // back into input order.
 #include <cub/cub.cuh>
+#include <string.h>
 
 #include "../../include/filterkit_b200.h"
 #include "fk_common.cuh"
@@ -64,6 +65,37 @@ __global__ void k_unpermute(const uint32_t *__restrict__ perm, const T *__restri
     dst[perm[i]] = src[i];
 }
 
+// Fused exchange over peer memory (CUDA IPC mappings of the other ranks'
+// buffers; NVLink / NVSwitch stores between GPUs).  dispatch: the gather of
+// the stable owner partition writes every key straight into its owner's
+// receive buffer, at this rank's offset there, with a (rank, input index)
+// tag; combine: the owner writes each per-key result straight into the
+// source rank's output array at the key's input index.
+__global__ void k_dispatch(const uint64_t *__restrict__ keys, const uint64_t *__restrict__ vals,
+                           const uint32_t *__restrict__ perm, int64_t n, uint64_t seed, int shift, uint32_t gmask,
+                           const int64_t *__restrict__ seg_start, const int64_t *__restrict__ dst_off,
+                           uint64_t *const *__restrict__ pk, uint64_t *const *__restrict__ pv,
+                           uint64_t *const *__restrict__ ps, uint32_t rank) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t p = perm[i];
+    const uint64_t k = keys[p];
+    const uint32_t o = shift >= 64 ? 0u : (uint32_t)(mix64(k ^ seed) >> shift) & gmask;
+    const int64_t j = dst_off[o] + (i - seg_start[o]);
+    pk[o][j] = k;
+    if (vals) pv[o][j] = vals[p];
+    ps[o][j] = ((uint64_t)rank << 32) | p;
+  }
+}
+
+template <typename T>
+__global__ void k_combine(const uint64_t *__restrict__ src, const T *__restrict__ res, int64_t m,
+                          T *const *__restrict__ pout) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t t = src[j];
+    pout[t >> 32][(uint32_t)t] = res[j];
+  }
+}
+
 }  // namespace
 }  // namespace fk
 
@@ -95,8 +127,69 @@ int fk_shard_partition(const uint64_t *keys, const uint64_t *vals, int64_t n, ui
     if (!tmp) return -(int)S.err;
     FK_TRY(cub::DeviceRadixSort::SortPairs(tmp, tb, owner, owner_s, iota, perm, n, 0, log2_shards, st));
   }
-  k_gather2<<<grid_for(n), 256, 0, st>>>(keys, vals, perm, n, keys_out, vals_out);
+  if (keys_out) {  // the peer-memory path gathers inside fk_shard_dispatch instead
+    k_gather2<<<grid_for(n), 256, 0, st>>>(keys, vals, perm, n, keys_out, vals_out);
+    FK_CHECK_LAUNCH();
+  }
+  return 0;
+}
+
+int fk_shard_dispatch(const uint64_t *keys, const uint64_t *vals, const uint32_t *perm, int64_t n, uint64_t seed,
+                      int shift, int log2_shards, uint32_t rank, const int64_t *seg_start, const int64_t *dst_off,
+                      uint64_t *const *peer_keys, uint64_t *const *peer_vals, uint64_t *const *peer_src,
+                      void *stream) {
+  if (n < 0 || log2_shards < 0 || log2_shards > 8 || !peer_keys || !peer_src || (vals && !peer_vals)) return FK_E_ARG;
+  if (n == 0) return 0;
+  const int sh = log2_shards == 0 ? 64 : shift;
+  k_dispatch<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(keys, vals, perm, n, seed, sh,
+                                                            (uint32_t)((1 << log2_shards) - 1), seg_start, dst_off,
+                                                            peer_keys, peer_vals, peer_src, rank);
   FK_CHECK_LAUNCH();
+  return 0;
+}
+
+int fk_shard_combine(const uint64_t *src, const void *res, int64_t m, int elem_bytes, void *const *peer_out,
+                     void *stream) {
+  if (m < 0 || !peer_out) return FK_E_ARG;
+  if (m == 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (elem_bytes == 1)
+    k_combine<uint8_t><<<grid_for(m), 256, 0, st>>>(src, (const uint8_t *)res, m, (uint8_t *const *)peer_out);
+  else if (elem_bytes == 8)
+    k_combine<uint64_t><<<grid_for(m), 256, 0, st>>>(src, (const uint64_t *)res, m, (uint64_t *const *)peer_out);
+  else
+    return FK_E_ARG;
+  FK_CHECK_LAUNCH();
+  return 0;
+}
+
+int fk_ipc_alloc(int64_t bytes, void **ptr) {
+  if (bytes <= 0 || !ptr) return FK_E_ARG;
+  FK_TRY(cudaMalloc(ptr, (size_t)bytes));
+  return 0;
+}
+
+int fk_ipc_free(void *ptr) {
+  if (ptr) FK_TRY(cudaFree(ptr));
+  return 0;
+}
+
+int fk_ipc_get_handle(void *ptr, void *handle_out) {
+  if (!ptr || !handle_out) return FK_E_ARG;
+  FK_TRY(cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t *>(handle_out), ptr));
+  return 0;
+}
+
+int fk_ipc_open(const void *handle, void **ptr) {
+  if (!handle || !ptr) return FK_E_ARG;
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  FK_TRY(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return 0;
+}
+
+int fk_ipc_close(void *ptr) {
+  if (ptr) FK_TRY(cudaIpcCloseMemHandle(ptr));
   return 0;
 }
 

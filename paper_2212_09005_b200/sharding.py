@@ -64,6 +64,17 @@ class CudaShardOps:
                                                _lib.dptr(counts), _lib.stream_ptr(torch)), "shard partition")
         return ko, vo, perm, counts
 
+    def partition_perm(self, keys, seed, shift, log2g):
+        """Stable owner permutation and per-owner counts only (no gather)."""
+        torch = self.torch
+        n = keys.numel()
+        perm = torch.empty(n, dtype=torch.int32, device=keys.device)
+        counts = torch.empty(1 << log2g, dtype=torch.int64, device=keys.device)
+        _lib.check(self.lib.fk_shard_partition(_lib.dptr(keys), None, n, seed & ((1 << 64) - 1), shift, log2g,
+                                               None, None, _lib.dptr(perm), _lib.dptr(counts),
+                                               _lib.stream_ptr(torch)), "shard partition")
+        return perm, counts
+
     def unpermute(self, perm, src):
         torch = self.torch
         out = torch.empty_like(src)
@@ -146,6 +157,163 @@ class _Router:
         return t.tolist()
 
 
+class _PeerBuffers:
+    """Device buffers every rank can store into: allocated whole (cudaMalloc)
+    so a CUDA IPC handle covers them, handles exchanged once per growth, the
+    other ranks' buffers opened into this process (NVLink peer mappings)."""
+
+    NAMES = ("keys", "vals", "src", "out")
+
+    def __init__(self, torch, group, world, rank):
+        self.torch, self.group, self.world, self.rank = torch, group, world, rank
+        self.lib = _lib.load()
+        self.cap = 0
+        self.local = {}   # name -> own device pointer
+        self.peers = {}   # name -> [pointer of rank r's buffer] (own included)
+        self.tables = {}  # name -> int64 CUDA tensor of the pointers (kernel argument)
+
+    def _free(self):
+        for name in self.NAMES:
+            for r, ptr in enumerate(self.peers.get(name, [])):
+                if r != self.rank and ptr:
+                    self.lib.fk_ipc_close(ctypes.c_void_p(ptr))
+            if self.local.get(name):
+                self.lib.fk_ipc_free(ctypes.c_void_p(self.local[name]))
+        self.local, self.peers, self.tables = {}, {}, {}
+
+    def ensure(self, need):
+        """Collective: every rank calls it with its own need (items)."""
+        import torch.distributed as dist
+        torch = self.torch
+        objs = [None] * self.world
+        dist.all_gather_object(objs, int(need), group=self.group)
+        want = max(objs)
+        if want <= self.cap:
+            return
+        cap = max(want, 2 * self.cap, 1 << 16)
+        self._free()
+        handles = {}
+        for name in self.NAMES:
+            ptr = ctypes.c_void_p()
+            _lib.check(self.lib.fk_ipc_alloc(cap * 8, ctypes.byref(ptr)), "ipc alloc")
+            self.local[name] = ptr.value
+            h = ctypes.create_string_buffer(64)
+            _lib.check(self.lib.fk_ipc_get_handle(ptr, h), "ipc handle")
+            handles[name] = h.raw
+        everyone = [None] * self.world
+        dist.all_gather_object(everyone, handles, group=self.group)
+        for name in self.NAMES:
+            ptrs = []
+            for r in range(self.world):
+                if r == self.rank:
+                    ptrs.append(self.local[name])
+                    continue
+                out = ctypes.c_void_p()
+                h = ctypes.create_string_buffer(everyone[r][name], 64)
+                _lib.check(self.lib.fk_ipc_open(h, ctypes.byref(out)), "ipc open")
+                ptrs.append(out.value)
+            self.peers[name] = ptrs
+            self.tables[name] = torch.tensor(ptrs, dtype=torch.int64, device="cuda")
+        self.cap = cap
+
+    def view(self, name, n, dtype):
+        """This rank's own buffer `name` as a CUDA tensor of n items of dtype."""
+        return _DevView.make(self.torch, self.local[name], n, dtype)
+
+    def __del__(self):
+        try:
+            self._free()
+        except Exception:
+            pass
+
+
+class _DevView:
+    """A torch CUDA tensor over a raw device pointer (no ownership)."""
+
+    @staticmethod
+    def make(torch, ptr, n, dtype):
+        itemsize = torch.empty(0, dtype=dtype).element_size()
+
+        class _Iface:
+            __cuda_array_interface__ = {"shape": (int(n),), "typestr": {1: "|u1", 8: "<i8"}[itemsize],
+                                        "data": (int(ptr), False), "version": 3}
+        t = torch.as_tensor(_Iface(), device="cuda")
+        return t.view(dtype) if t.dtype != dtype else t
+
+
+class _PeerRouter(_Router):
+    """Owner routing through peer memory instead of an all-to-all: the
+    dispatch kernel stores every key into its owner's receive buffer, the
+    combine kernel stores every result into its source rank's output buffer
+    (fk_shard_dispatch / fk_shard_combine).  Only per-owner counts (G ints)
+    and a barrier per direction go through torch.distributed."""
+
+    def __init__(self, torch, group, world, seed, shift, ops):
+        super().__init__(torch, group, world, seed, shift, ops)
+        import torch.distributed as dist
+        self.rank = dist.get_rank(group)
+        self.bufs = _PeerBuffers(torch, group, world, self.rank)
+
+    def _barrier(self):
+        import torch.distributed as dist
+        self.torch.cuda.current_stream().synchronize()
+        dist.barrier(group=self.group)
+
+    def route(self, keys, vals=None):
+        torch = self.torch
+        if self.world == 1:
+            return keys, vals, None
+        import torch.distributed as dist
+        perm, counts = self.ops.partition_perm(keys, self.seed, self.shift, self.log2g)
+        c = counts.to(self._coll_device())
+        allc = [torch.empty_like(c) for _ in range(self.world)]
+        dist.all_gather(allc, c, group=self.group)
+        C = np.array([a.tolist() for a in allc], dtype=np.int64)  # C[source][owner]
+        me = self.rank
+        recv_n = int(C[:, me].sum())
+        self.bufs.ensure(max(recv_n, keys.numel()))
+        seg_start = np.concatenate(([0], np.cumsum(C[me])[:-1]))
+        dst_off = np.cumsum(C, axis=0) - C  # rows above: earlier source ranks
+        dev = keys.device
+        ss = torch.tensor(seg_start, dtype=torch.int64, device=dev)
+        do = torch.tensor(dst_off[me], dtype=torch.int64, device=dev)
+        t = self.bufs.tables
+        lib = self.ops.lib
+        _lib.check(lib.fk_shard_dispatch(_lib.dptr(keys), _lib.dptr(vals), _lib.dptr(perm), keys.numel(),
+                                         self.seed & ((1 << 64) - 1), self.shift, self.log2g, me, _lib.dptr(ss),
+                                         _lib.dptr(do), _lib.dptr(t["keys"]),
+                                         _lib.dptr(t["vals"]) if vals is not None else None, _lib.dptr(t["src"]),
+                                         _lib.stream_ptr(torch)), "shard dispatch")
+        self._barrier()  # every rank's keys have landed in its owners' buffers
+        rk = self.bufs.view("keys", recv_n, torch.int64)
+        rv = self.bufs.view("vals", recv_n, torch.int64) if vals is not None else None
+        return rk, rv, (keys.numel(), recv_n)
+
+    def unroute(self, res, plan):
+        if plan is None:
+            return res
+        torch = self.torch
+        n, recv_n = plan
+        res = res.contiguous()
+        eb = res.element_size()
+        src = self.bufs.view("src", recv_n, torch.int64)
+        _lib.check(self.ops.lib.fk_shard_combine(_lib.dptr(src), _lib.dptr(res), recv_n, eb,
+                                                 _lib.dptr(self.bufs.tables["out"]), _lib.stream_ptr(torch)),
+                   "shard combine")
+        self._barrier()  # every owner has stored this rank's results
+        return self.bufs.view("out", n, res.dtype).clone()
+
+
+def _make_router(torch, group, world, seed, shift, ops):
+    """The peer-memory router on CUDA groups of more than one rank (set
+    FK_SHARD_PEER=0 for the all-to-all one); the all-to-all router otherwise
+    (and for the host-side test doubles)."""
+    import os
+    if world > 1 and isinstance(ops, CudaShardOps) and os.environ.get("FK_SHARD_PEER", "1") != "0":
+        return _PeerRouter(torch, group, world, seed, shift, ops)
+    return _Router(torch, group, world, seed, shift, ops)
+
+
 def _world(group):
     import torch.distributed as dist
     if dist.is_available() and dist.is_initialized():
@@ -191,7 +359,7 @@ class ShardedTcf(_Sharded):
         self._local = Tcf(local, mode=mode)
         self.mode = mode
         lg = _log2_exact(self.world)
-        self._router = _Router(self._torch, group, self.world, params.seed, 64 - lg, self._ops)
+        self._router = _make_router(self._torch, group, self.world, params.seed, 64 - lg, self._ops)
 
     def _reset(self):
         self._local._reset()
@@ -246,7 +414,7 @@ class ShardedBulkTcf(_Sharded):
                               probe_limit=params.probe_limit, shortcut_fraction=params.shortcut_fraction)
         self._local = BulkTcf(local)
         lg = _log2_exact(self.world)
-        self._router = _Router(self._torch, group, self.world, params.seed, 64 - lg, self._ops)
+        self._router = _make_router(self._torch, group, self.world, params.seed, 64 - lg, self._ops)
 
     def _reset(self):
         self._local._reset()
@@ -292,7 +460,7 @@ class ShardedGqf(_Sharded):
         self.params = params
         local = GqfParams(q=params.q - lg, r=params.r, seed=params.seed, max_load=params.max_load)
         self._local = Gqf(local)
-        self._router = _Router(self._torch, group, self.world, params.seed, local.q + params.r, self._ops)
+        self._router = _make_router(self._torch, group, self.world, params.seed, local.q + params.r, self._ops)
 
     def _reset(self):
         self._local._reset()

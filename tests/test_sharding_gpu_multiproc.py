@@ -20,13 +20,13 @@ from conftest import ROOT
 pytestmark = pytest.mark.gpu
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, peer="1"):
     import sys
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import torch
     import torch.distributed as dist
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), FK_SHARD_PEER=peer)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         torch.cuda.set_device(0)
@@ -35,6 +35,7 @@ def _worker(rank, world, port, q):
         out = {}
         keys = counter_keys(60 + rank, 20_000)
         st = ShardedTcf(num_blocks=4096)
+        out["router"] = type(st._router).__name__
         out["codes"] = st.insert_many(keys)
         out["found"] = st.query_many(keys)
         out["neg"] = st.query_many(counter_keys(80 + rank, 5000))
@@ -61,11 +62,14 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def test_two_rank_sharded_facades(oracle):
+@pytest.mark.parametrize("peer", ["1", "0"])
+def test_two_rank_sharded_facades(oracle, peer):
+    """peer = 1: the fused peer-memory exchange (fk_shard_dispatch /
+    fk_shard_combine over CUDA IPC mappings); 0: the all-to-all router."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, peer)) for r in range(2)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=400) for _ in procs)
@@ -84,6 +88,7 @@ def test_two_rank_sharded_facades(oracle):
         n0 = int((own[0] == s).sum())
         assert np.array_equal(res[0]["codes"][own[0] == s], codes[:n0])
         assert np.array_equal(res[1]["codes"][own[1] == s], codes[n0:])
+    assert res[0]["router"] == ("_PeerRouter" if peer == "1" else "_Router")
     for r in range(2):
         assert res[r]["found"].all() and res[r]["removed"].all()
         assert res[r]["neg"].mean() < 0.01
