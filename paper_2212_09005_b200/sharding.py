@@ -202,6 +202,7 @@ class _PeerBuffers:
             handles[name] = h.raw
         everyone = [None] * self.world
         dist.all_gather_object(everyone, handles, group=self.group)
+        ok = True
         for name in self.NAMES:
             ptrs = []
             for r in range(self.world):
@@ -210,10 +211,17 @@ class _PeerBuffers:
                     continue
                 out = ctypes.c_void_p()
                 h = ctypes.create_string_buffer(everyone[r][name], 64)
-                _lib.check(self.lib.fk_ipc_open(h, ctypes.byref(out)), "ipc open")
-                ptrs.append(out.value)
+                if self.lib.fk_ipc_open(h, ctypes.byref(out)) != 0:
+                    ok = False
+                ptrs.append(out.value or 0)
             self.peers[name] = ptrs
             self.tables[name] = torch.tensor(ptrs, dtype=torch.int64, device="cuda")
+        # every rank must be able to reach every other one, or nobody uses it
+        oks = [None] * self.world
+        dist.all_gather_object(oks, ok, group=self.group)
+        if not all(oks):
+            self._free()
+            raise _NoPeerAccess()
         self.cap = cap
 
     def view(self, name, n, dtype):
@@ -225,6 +233,10 @@ class _PeerBuffers:
             self._free()
         except Exception:
             pass
+
+
+class _NoPeerAccess(RuntimeError):
+    """Some rank could not map another rank's buffers (no CUDA IPC / P2P)."""
 
 
 class _DevView:
@@ -253,6 +265,7 @@ class _PeerRouter(_Router):
         import torch.distributed as dist
         self.rank = dist.get_rank(group)
         self.bufs = _PeerBuffers(torch, group, world, self.rank)
+        self.fallback = False  # set collectively if peer mappings are unavailable
 
     def _barrier(self):
         import torch.distributed as dist
@@ -263,6 +276,8 @@ class _PeerRouter(_Router):
         torch = self.torch
         if self.world == 1:
             return keys, vals, None
+        if self.fallback:
+            return super().route(keys, vals)
         import torch.distributed as dist
         perm, counts = self.ops.partition_perm(keys, self.seed, self.shift, self.log2g)
         c = counts.to(self._coll_device())
@@ -271,7 +286,11 @@ class _PeerRouter(_Router):
         C = np.array([a.tolist() for a in allc], dtype=np.int64)  # C[source][owner]
         me = self.rank
         recv_n = int(C[:, me].sum())
-        self.bufs.ensure(max(recv_n, keys.numel()))
+        try:
+            self.bufs.ensure(max(recv_n, keys.numel()))
+        except _NoPeerAccess:  # collective decision: every rank falls back together
+            self.fallback = True
+            return super().route(keys, vals)
         seg_start = np.concatenate(([0], np.cumsum(C[me])[:-1]))
         dst_off = np.cumsum(C, axis=0) - C  # rows above: earlier source ranks
         dev = keys.device
@@ -292,6 +311,8 @@ class _PeerRouter(_Router):
     def unroute(self, res, plan):
         if plan is None:
             return res
+        if self.fallback:
+            return super().unroute(res, plan)
         torch = self.torch
         n, recv_n = plan
         res = res.contiguous()
