@@ -14,7 +14,9 @@ input / output, alternating), so nothing is freed across streams.
 
 from __future__ import annotations
 
-PIPE_CHUNK = 1 << 23  # keys per chunk (64 MiB of keys)
+import os
+
+PIPE_CHUNK = int(os.environ.get("FK_PIPE_CHUNK", 1 << 23))  # keys per chunk (64 MiB of keys)
 
 
 class HostPipeline:
