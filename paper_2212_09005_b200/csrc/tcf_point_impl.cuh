@@ -1043,7 +1043,8 @@ static int launch_ordered(const TcfDev &P, const uint64_t *keys, const uint64_t 
     // one-barrier kernel when the window gives every thread a key (its
     // window is about grid * 256 * slots); small windows keep the carry-list
     // kernel, whose window is exact
-    if (X.res2 && X.window >= thr) {
+    // (its 32-bit frontier may overshoot n by a round's grabs: keep clear of 2^32)
+    if (X.res2 && X.window >= thr && n < (int64_t)0xFFFFFFFFLL - 4 * thr * kOrdKB<1>) {
       int slots = (int)((X.window + thr - 1) / thr);
       X.slots = slots < 1 ? 1 : (slots > kOrdKB<1> ? kOrdKB<1> : slots);
       void *args[] = {(void *)&P, (void *)&keys, (void *)&values, (void *)&n, (void *)&out, (void *)&counters,
