@@ -126,6 +126,15 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+def max_over_ranks(torch, value, dev):
+    """Max of a float over the ranks (device tensor on NCCL, host on gloo)."""
+    import torch.distributed as dist
+    on = dev if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([float(value)], device=on, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def counter_stream(seed, tag, n):
     from paper_2212_09005_b200.workloads import counter_stream as cs
     return cs(seed, tag, n)
@@ -261,6 +270,7 @@ def run_ours(args, rank, world, local_rank):
     import torch
     from paper_2212_09005_b200 import Tcf
 
+    local_rank %= torch.cuda.device_count()
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     log_slots = args.log_slots
@@ -326,9 +336,7 @@ def run_ours(args, rank, world, local_rank):
     per_op_ms = {op: float(np.mean([evs[s][i].elapsed_time(evs[s][i + 1]) for s in range(args.steps)]))
                  for i, op in enumerate(ops)}
     if dist:
-        t = torch.tensor([ms_total], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_total = float(t.item())
+        ms_total = max_over_ranks(torch, ms_total, dev)
     ms_step = ms_total / args.steps
     total_ops = 4 * n * world
     value = total_ops / (ms_step / 1e3)
@@ -359,9 +367,7 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
         te = (time.perf_counter() - ts) / e2e_steps
         if dist:
-            t = torch.tensor([te], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            te = float(t.item())
+            te = max_over_ranks(torch, te, dev)
         e2e = {"value": total_ops / te, "unit": UNIT, "h2d_bytes_per_step": 4 * 8 * n,
                "d2h_bytes_per_step": 4 * n, "ms_per_step": te * 1e3}
         del hk, hn
@@ -534,6 +540,7 @@ def kmer_zipf_workload(torch, q, alpha, seed, dev, s=1.5, cmax=100, r=8):
 
 def run_workload(args, rank, world, local_rank):
     import torch
+    local_rank %= torch.cuda.device_count()
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     dist = None
@@ -569,9 +576,7 @@ def run_workload(args, rank, world, local_rank):
         torch.cuda.synchronize()
     ms_total = t0.elapsed_time(t1)
     if dist:
-        t = torch.tensor([ms_total], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_total = float(t.item())
+        ms_total = max_over_ranks(torch, ms_total, dev)
     ms_step = ms_total / args.steps
     items = sum(n for _, _, n in ops)
     per_op = {}
@@ -589,9 +594,7 @@ def run_workload(args, rank, world, local_rank):
         torch.cuda.synchronize()
         te = (time.perf_counter() - tsum) / max(1, min(args.steps, 3))
         if dist:
-            t = torch.tensor([te], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            te = float(t.item())
+            te = max_over_ranks(torch, te, dev)
         e2e = {"value": items * world / te, "unit": UNIT, "ms_per_step": te * 1e3,
                "h2d_bytes_per_step": 8 * items, "d2h_bytes_per_step": None}
     launches = count_launches(torch, step) if not args.no_launch_count else None
@@ -768,8 +771,15 @@ def main():
         if world > 1:
             import torch
             import torch.distributed as dist
-            torch.cuda.set_device(local_rank)
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+            # FK_BENCH_BACKEND=gloo: test hook for several ranks on one GPU
+            # (NCCL refuses that); the driver's runs use NCCL
+            backend = os.environ.get("FK_BENCH_BACKEND", "nccl")
+            dev_idx = local_rank % torch.cuda.device_count()
+            torch.cuda.set_device(dev_idx)
+            if backend == "nccl":
+                dist.init_process_group("nccl", device_id=torch.device("cuda", dev_idx))
+            else:
+                dist.init_process_group(backend)
         res = (run_ours if args.workload == "tcf" else run_workload)(args, rank, world, local_rank)
         if world > 1:
             import torch.distributed as dist
