@@ -400,10 +400,14 @@ def run_ours(args, rank, world, local_rank):
                                "uniform 64-bit keys, insert+pos query+neg query+delete at %.2f load"
                                % (log_slots, log_slots - 4, args.load),
                    "keys_per_op_per_gpu": n, "mode": args.mode, "group_width": args.group_width,
-                   "l2": "inputs (%.1f GB keys) and table (%d MiB) exceed the 126 MB L2; no flush"
-                         % (8 * n / 1e9, (1 << log_slots) * 2 >> 20),
-                   "parallelism": ("hash-prefix shards x%d, NCCL all-to-all" % world) if world > 1
-                   else "single GPU"},
+                   "l2": (("inputs (%.1f GB keys) and table (%d MiB) exceed the 126 MB L2; no flush"
+                           if (1 << log_slots) * 2 > (126 << 20) else
+                           "inputs %.1f GB; the %d MiB table is L2-resident (an L2-resident configuration, "
+                           "not the headline)") % (8 * n / 1e9, (1 << log_slots) * 2 >> 20)),
+                   "parallelism": ("hash-prefix shards x%d, %s" % (
+                       world, "peer-memory exchange (fk_shard_dispatch/combine)"
+                       if type(filt._router).__name__ == "_PeerRouter" and not filt._router.fallback
+                       else "all-to-all exchange")) if world > 1 else "single GPU"},
         "per_op": per_op,
         "roofline": {"bound": "hbm", "kernel": KERNEL_OF[(args.mode, dom)], "op": dom, "achieved": achieved,
                      "peak": peak, "unit": "GB/s", "frac": achieved / peak, "peak_kind": peak_kind,
