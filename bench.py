@@ -229,6 +229,31 @@ def count_launches(torch, step):
         return None
 
 
+def zipf_queries(torch, filt, keys, stream, s=1.5, reps=3):
+    """Skewed lookups on the filled table (secondary numbers, not in `value`):
+    positive queries whose key ranks follow the reference's bounded Zipf(s)
+    sampler (fk/workloads.py:81-118) over the inserted keys, 2^24 host draws
+    tiled to one query per inserted key.  Hot keys' blocks stay in L2."""
+    from paper_2212_09005_b200.workloads import zipf_bounded
+    n = keys.numel()
+    rng = np.random.default_rng(12345)
+    ranks = zipf_bounded(rng, s, n, 1 << 24) - 1
+    perm = torch.from_numpy(ranks).to(keys.device)
+    idx = perm.repeat((n + perm.numel() - 1) // perm.numel())[:n]
+    q = keys[idx]
+    filt.query_many(q)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(reps):
+        found = filt.query_many(q)
+    b.record(stream)
+    b.synchronize()
+    ms = a.elapsed_time(b) / reps
+    return {"ops_per_s": n / (ms / 1e3), "ms": ms, "zipf_s": s, "all_found": bool(found.all()),
+            "how": "query_many of %d keys with Zipf(%.1f) ranks over the inserted keys" % (n, s)}
+
+
 def concurrent_mode(torch, nb, args, keys, negs, stream, ceiling=None, steps=2):
     """The paper's free-threaded CAS mode on the same workload (secondary
     numbers; not bit-identical to the sequential reference)."""
@@ -390,6 +415,11 @@ def run_ours(args, rank, world, local_rank):
     traffic = ncu_traffic(args.mode, dom, n)
     launches = count_launches(torch, step) if not args.no_launch_count else None
     conc = None
+    zq = None
+    if world == 1 and not args.no_concurrent:
+        filt._reset()
+        filt.insert_many(keys)
+        zq = zipf_queries(torch, filt, keys, stream)
     if args.mode == "ordered" and not args.no_concurrent and world == 1:
         conc = concurrent_mode(torch, nb, args, keys, negs, stream, ceiling)
     result = {
@@ -423,6 +453,8 @@ def run_ours(args, rank, world, local_rank):
     }
     if conc:
         result["concurrent_mode"] = conc
+    if zq:
+        result["zipf_queries"] = zq
     if rank == 0 and world == 1 and not args.no_cpu:
         result["cpu_baseline"] = cpu_baseline(args.cpu_budget_s)
     return result if rank == 0 else None
