@@ -63,6 +63,10 @@ SECTORS_PER_OP = {"insert": 1.260, "query_pos": 1.1437, "query_neg": 2.0, "delet
 # plain random reads.  (rmw, extra reads) per op:
 RMW_PER_OP = {"insert": (1.0, 0.260), "delete": (1.0, 0.1437), "query_pos": (0.0, 1.1437), "query_neg": (0.0, 2.0)}
 
+# bytes each secondary-workload op returns to the host per item (e2e D2H):
+# counts 8 B, found / removed flags 1 B; inserts return only failed keys
+RESULT_BYTES = {"count": 8, "bulk_delete": 1, "query_pos": 1, "query_neg": 1, "delete": 1}
+
 KERNEL_OF = {
     ("ordered", "insert"): "k_tcf_ordered1<KB=2,OP=insert> (one-barrier, u16, B=16, G=1)",
     ("ordered", "delete"): "k_tcf_ordered1<KB=2,OP=delete> (one-barrier, u16, B=16, G=1)",
@@ -632,7 +636,8 @@ def run_workload(args, rank, world, local_rank):
         if dist:
             te = max_over_ranks(torch, te, dev)
         e2e = {"value": items * world / te, "unit": UNIT, "ms_per_step": te * 1e3,
-               "h2d_bytes_per_step": 8 * items, "d2h_bytes_per_step": None}
+               "h2d_bytes_per_step": 8 * items,
+               "d2h_bytes_per_step": sum(RESULT_BYTES.get(name, 0) * m for name, _, m in ops)}
     launches = count_launches(torch, step) if not args.no_launch_count else None
     res = {"metric": METRIC, "value": items * world / (ms_step / 1e3), "unit": UNIT, "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
