@@ -40,6 +40,8 @@ def _worker(rank, world, port, q, peer="1"):
         out["found"] = st.query_many(keys)
         out["neg"] = st.query_many(counter_keys(80 + rank, 5000))
         out["blocks"] = st._local._blocks.copy()
+        # uneven batches, one of them empty: the exchange is still collective
+        out["uneven"] = st.query_many(keys[:0] if rank == 0 else keys[:100])
         out["removed"] = st.delete_many(keys[::2])
         out["counters"] = st.counters
         sb = ShardedBulkTcf(num_blocks=512)
@@ -89,6 +91,7 @@ def test_two_rank_sharded_facades(oracle, peer):
         assert np.array_equal(res[0]["codes"][own[0] == s], codes[:n0])
         assert np.array_equal(res[1]["codes"][own[1] == s], codes[n0:])
     assert res[0]["router"] == ("_PeerRouter" if peer == "1" else "_Router")
+    assert len(res[0]["uneven"]) == 0 and len(res[1]["uneven"]) == 100 and res[1]["uneven"].all()
     for r in range(2):
         assert res[r]["found"].all() and res[r]["removed"].all()
         assert res[r]["neg"].mean() < 0.01
