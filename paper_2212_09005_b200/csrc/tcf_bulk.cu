@@ -1,3 +1,4 @@
+#include <stdlib.h>
 // tcf_bulk.cu -- bulk two-choice filter on sm_100a.
 //
 // Replaces the bulk half of the reference kernel contract together with the
@@ -396,6 +397,109 @@ __global__ void __launch_bounds__(32) k_btcf_route_seq(const uint32_t *__restric
   }
 }
 
+// Block-parallel form of the same walk for large tables (bit-identical
+// decisions).  One 1024-thread CTA takes the next 1024 leftovers; a leftover
+// whose b2 (or b1) meets an earlier leftover's other block inside the window
+// ends the window's conflict-free prefix (found with a shared-memory table of
+// first touches); inside the prefix the only dependencies left are the b1
+// groups (leftovers are sorted by b1), so every b2 counter is read once in
+// parallel and each group's head runs the group's one-register scan
+// x <- x + [x <= min(y, B - 1)].  Prefixes are ~sqrt(blocks) long, so this
+// pays off on large tables only (the caller keeps the warp walk below 2^16
+// blocks).
+constexpr int kRouteW = 1024, kRouteHT = 4096;
+constexpr size_t kRouteSmem = (size_t)kRouteHT * 12 + (size_t)kRouteW * 12;
+
+__global__ void __launch_bounds__(kRouteW, 1) k_btcf_route_prefix(const uint32_t *__restrict__ lb1,
+                                                                  const uint32_t *__restrict__ lb2, int64_t m,
+                                                                  uint32_t *__restrict__ load, uint32_t B,
+                                                                  int32_t *__restrict__ dest) {
+  extern __shared__ uint32_t route_smem[];  // kRouteSmem bytes (dynamic: > 48 KB)
+  uint32_t *ht_key = route_smem;
+  int *ht_a = reinterpret_cast<int *>(ht_key + kRouteHT), *ht_b = ht_a + kRouteHT;
+  uint32_t *s_y = reinterpret_cast<uint32_t *>(ht_b + kRouteHT), *s_a = s_y + kRouteW;
+  int32_t *s_d = reinterpret_cast<int32_t *>(s_a + kRouteW);
+  __shared__ int s_first;
+  const int k = threadIdx.x;
+  auto slot = [&](uint32_t blk) {  // insert-or-find in the open-addressed table
+    uint32_t h = (blk * 2654435761u) & (kRouteHT - 1);
+    for (;;) {
+      uint32_t prev = atomicCAS(&ht_key[h], 0xFFFFFFFFu, blk);
+      if (prev == 0xFFFFFFFFu || prev == blk) return h;
+      h = (h + 1) & (kRouteHT - 1);
+    }
+  };
+  for (int64_t base = 0; base < m;) {
+    const int cnt = m - base < kRouteW ? (int)(m - base) : kRouteW;
+    for (int i = k; i < kRouteHT; i += kRouteW) {
+      ht_key[i] = 0xFFFFFFFFu;
+      ht_a[i] = ht_b[i] = kRouteW;
+    }
+    if (k == 0) s_first = cnt;
+    __syncthreads();
+    const bool live = k < cnt;
+    uint32_t a = 0, b = 0, ha = 0, hb = 0;
+    if (live) {
+      a = lb1[base + k];
+      b = lb2[base + k];
+      ha = slot(a);
+      hb = slot(b);
+      atomicMin(&ht_a[ha], k);
+      atomicMin(&ht_b[hb], k);
+    }
+    __syncthreads();
+    // conflict: b = an earlier a or b, a = an earlier b, or b = own a
+    if (live && (b == a || ht_a[hb] < k || ht_b[hb] < k || ht_b[ha] < k)) atomicMin(&s_first, k);
+    __syncthreads();
+    const int first = s_first;
+    if (first == 0) {  // leftover 0 alone (b1 == b2): the plain rule
+      if (k == 0) {
+        const uint32_t la = load[a], lbv = load[b];
+        const bool pa = la <= lbv;
+        const uint32_t lp = pa ? la : lbv, d = pa ? a : b;
+        if (lp < B) load[d] = lp + 1;
+        dest[base] = lp < B ? (int32_t)d : -1;
+      }
+      __syncthreads();
+      base += 1;
+      continue;
+    }
+    const bool act = k < first;
+    if (act) {
+      s_y[k] = load[b];
+      s_a[k] = a;
+    }
+    __syncthreads();
+    // group heads scan their group in order
+    if (act && (k == 0 || s_a[k - 1] != a)) {
+      uint32_t x = load[a];
+      int j = k;
+      for (; j < first && s_a[j] == a; j++) {
+        const uint32_t y = s_y[j];
+        const uint32_t t = y < B - 1 ? y : B - 1;
+        if (x <= t) {
+          s_d[j] = (int32_t)a;
+          x++;
+        } else {
+          s_d[j] = y < B ? -2 : -1;  // -2: takes its b2 (x > y)
+        }
+      }
+      load[a] = x;
+    }
+    __syncthreads();
+    if (act) {
+      int32_t d = s_d[k];
+      if (d == -2) {
+        load[b] = s_y[k] + 1;  // b is touched by no other leftover of the prefix
+        d = (int32_t)b;
+      }
+      dest[base + k] = d;
+    }
+    __syncthreads();
+    base += first;
+  }
+}
+
 // leftover positions -> (b1, b2) of each leftover and the words
 __global__ void k_left_blocks(BDev P, const uint64_t *__restrict__ keys, const uint32_t *__restrict__ sval,
                               const uint32_t *__restrict__ lpos, int64_t m, uint32_t *__restrict__ lb1,
@@ -717,7 +821,13 @@ int btcf_insert(const BDev &P, const uint64_t *keys, int64_t n, uint64_t *failed
     FK_CHECK_LAUNCH();
     uint32_t Bu = (uint32_t)P.B;
     size_t sm = (size_t)P.nb * 4;
-    if (sm <= 200 * 1024) {
+    if ((P.nb >= (1u << 16) && !getenv("FK_ROUTE_WARP")) || getenv("FK_ROUTE_PREFIX")) {
+      // large tables: block-parallel conflict-free prefixes (FK_ROUTE_WARP
+      // forces the single-warp walk, FK_ROUTE_PREFIX this one)
+      FK_S(cudaMemcpyAsync(load, P.fill, P.nb * 4, cudaMemcpyDeviceToDevice, st));
+      FK_S(cudaFuncSetAttribute(k_btcf_route_prefix, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRouteSmem));
+      k_btcf_route_prefix<<<1, kRouteW, kRouteSmem, st>>>(lb1, lb2, m, load, Bu, dest);
+    } else if (sm <= 200 * 1024) {
       if (sm > 48 * 1024)
         FK_S(cudaFuncSetAttribute(k_btcf_route_seq<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
       k_btcf_route_seq<true><<<1, 32, sm, st>>>(lb1, lb2, m, P.fill, P.nb, load, Bu, dest);
