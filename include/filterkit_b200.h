@@ -217,6 +217,14 @@ int fk_gqf_count(const fk_gqf_geom *g, const fk_gqf_tables *t, const uint64_t *k
 int fk_gqf_find_run(const fk_gqf_geom *g, const fk_gqf_tables *t, const int64_t *quotients, int64_t n,
                     int64_t *se, void *stream);
 
+/* Device enumeration (replaces the host decode loop of
+ * Gqf.enumerate_items, gqf.py:403-409): every stored (fingerprint, count)
+ * pair in fingerprint order into device arrays of capacity cap.  Synchronous;
+ * *count_out (HOST) = number of items; nothing is written when it exceeds
+ * cap (call again with a larger buffer). */
+int fk_gqf_enumerate(const fk_gqf_geom *g, const fk_gqf_tables *t, uint64_t *fp_out, uint64_t *cnt_out,
+                     int64_t cap, int64_t *count_out, void *stream);
+
 /* Structure validation on the device (replaces the host checks of
  * Gqf.validate, gqf.py:430-492, which decode every run in Python), derived
  * from the bit vectors alone by global rank/select.  Synchronous; out (HOST

@@ -90,6 +90,8 @@ _SIGS = {
     "fk_gqf_find_run": (c_i32, [ctypes.POINTER(GqfGeom), ctypes.POINTER(GqfTables), c_vp, c_i64, c_vp, c_vp]),
     "fk_gqf_rebuild_index": (c_i32, [ctypes.POINTER(GqfGeom), ctypes.POINTER(GqfTables), c_vp]),
     "fk_gqf_validate": (c_i32, [ctypes.POINTER(GqfGeom), ctypes.POINTER(GqfTables), c_vp, c_vp]),
+    "fk_gqf_enumerate": (c_i32, [ctypes.POINTER(GqfGeom), ctypes.POINTER(GqfTables), c_vp, c_vp, c_i64,
+                                 ctypes.POINTER(c_i64), c_vp]),
     "fk_gqf_apply": (c_i32, [ctypes.POINTER(GqfGeom), ctypes.POINTER(GqfTables), ctypes.POINTER(GqfTables),
                              c_vp, c_i32, c_vp, c_i64, c_i32, c_i32, c_vp, ctypes.POINTER(GqfResult), c_vp]),
 }

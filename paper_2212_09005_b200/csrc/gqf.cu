@@ -199,7 +199,7 @@ int rebuild_index(const fk_gqf_geom *g, const fk_gqf_tables *t, cudaStream_t st)
   k_word_popc<<<blocks_for(nw), 256, 0, st>>>(t->runends, nw, pr);
   FK_CU(cub_excl_sum_i64(S, po, ro, nw));
   FK_CU(cub_excl_sum_i64(S, pr, rr, nw));
-  k_spill_from_ranks<<<blocks_for(nqw), 256, 0, st>>>(t->runends, ro, rr, nqw, t->spill);
+  k_spill_from_ranks<<<blocks_for(nqw), 256, 0, st>>>(t->runends, ro, rr, nqw, nw, t->spill);
   FK_CHECK_LAUNCH();
   return 0;
 }
@@ -347,6 +347,37 @@ int apply_small_delete_t(const fk_gqf_geom *g, const fk_gqf_tables *cur, const u
   if (rc) return rc;
   FK_CU(cudaStreamSynchronize(st));
   res->shifted = (int64_t)hm;
+  return 0;
+}
+
+// (fingerprint, count) items of the whole table in fingerprint order, by
+// the decode pass the rebuild uses (two passes: per-word group counts, then
+// writes at the scanned offsets).  *count_out = the number of items; nothing
+// is written when it exceeds cap.
+template <typename S_t>
+int enumerate_t(const fk_gqf_geom *g, const fk_gqf_tables *t, uint64_t *fp_out, uint64_t *cnt_out, int64_t cap,
+                int64_t *count_out, cudaStream_t st) {
+  Scratch S(st);
+  GqfDev T = make_dev(g, t);
+  const int64_t nqw = ((1LL << g->q) + 63) >> 6;
+  int64_t *gcount = S.get<int64_t>(nqw), *goff = S.get<int64_t>(nqw);
+  int *d_err = S.get<int>(4);
+  if (S.err) return -(int)S.err;
+  FK_CU(cudaMemsetAsync(d_err, 0, 4 * sizeof(int), st));
+  k_decode_words<S_t><<<blocks_for(nqw), 256, 0, st>>>(T, nqw, 0, gcount, nullptr, nullptr, nullptr, d_err);
+  FK_CU(cub_excl_sum_i64(S, gcount, goff, nqw));
+  int64_t tail[2];
+  int h_err = 0;
+  FK_CU(cudaMemcpyAsync(&tail[0], goff + nqw - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  FK_CU(cudaMemcpyAsync(&tail[1], gcount + nqw - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  FK_CU(cudaMemcpyAsync(&h_err, d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  FK_CU(cudaStreamSynchronize(st));
+  if (h_err) return FK_E_INVARIANT;
+  *count_out = tail[0] + tail[1];
+  if (*count_out > cap) return 0;
+  k_decode_words<S_t><<<blocks_for(nqw), 256, 0, st>>>(T, nqw, 1, nullptr, goff, fp_out, cnt_out, d_err);
+  FK_CHECK_LAUNCH();
+  FK_CU(cudaStreamSynchronize(st));
   return 0;
 }
 
@@ -740,6 +771,17 @@ int fk_gqf_find_run(const fk_gqf_geom *g, const fk_gqf_tables *t, const int64_t 
   k_gqf_find_run<<<blocks_for(n), 256, 0, (cudaStream_t)stream>>>(T, quotients, n, se);
   FK_CHECK_LAUNCH();
   return 0;
+}
+
+int fk_gqf_enumerate(const fk_gqf_geom *g, const fk_gqf_tables *t, uint64_t *fp_out, uint64_t *cnt_out, int64_t cap,
+                     int64_t *count_out, void *stream) {
+  if (!geom_ok(g) || !t || !count_out || cap < 0) return FK_E_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (g->r) {
+    case 8: return enumerate_t<uint8_t>(g, t, fp_out, cnt_out, cap, count_out, st);
+    case 16: return enumerate_t<uint16_t>(g, t, fp_out, cnt_out, cap, count_out, st);
+    default: return enumerate_t<uint32_t>(g, t, fp_out, cnt_out, cap, count_out, st);
+  }
 }
 
 int fk_gqf_validate(const fk_gqf_geom *g, const fk_gqf_tables *t, int64_t *out, void *stream) {

@@ -183,14 +183,17 @@ __global__ void k_word_popc(const uint64_t *__restrict__ bv, int64_t nw, int64_t
 }
 
 // rank_occ/rank_run: exclusive prefix sums of per-word popcounts (int64).
+// nw: quotient words (spill entries); nrun: runend words over the whole
+// physical table -- a run of a quotient near the end can end in the padding
 __global__ void k_spill_from_ranks(const uint64_t *__restrict__ run, const int64_t *__restrict__ rank_occ,
-                                   const int64_t *__restrict__ rank_run, int64_t nw, uint32_t *__restrict__ spill) {
+                                   const int64_t *__restrict__ rank_run, int64_t nw, int64_t nrun,
+                                   uint32_t *__restrict__ spill) {
   for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += (int64_t)gridDim.x * blockDim.x) {
     int64_t K = rank_occ[w];  // occupied quotients < 64w
     uint32_t s = 0;
     if (K > 0) {
       // word v holding the K-th runend: last v with rank_run[v] < K
-      int64_t lo = 0, hi = nw - 1;
+      int64_t lo = 0, hi = nrun - 1;
       while (lo < hi) {
         int64_t mid = (lo + hi + 1) >> 1;
         if (rank_run[mid] < K) lo = mid; else hi = mid - 1;

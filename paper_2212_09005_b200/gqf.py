@@ -328,6 +328,35 @@ class Gqf:
         return list(self.enumerate_items())
 
     def enumerate_items(self):
+        """Stored (fingerprint, count) pairs in fingerprint order, decoded on
+        the device (fk_gqf_enumerate) and yielded from host arrays."""
+        fps, cnts = self.device_items()
+        for f, c in zip(fps.tolist(), cnts.tolist()):
+            yield f, c
+
+    def device_items(self):
+        """(fingerprints, counts) as numpy uint64 arrays, fingerprint order."""
+        torch = self._torch
+        n = ctypes.c_int64(0)
+        with self._op_lock:
+            self._sync_in()
+            cap = max(1, self.distinct_items)
+            for _ in range(2):
+                fp = torch.empty(cap, dtype=torch.int64, device=self._device)
+                cn = torch.empty(cap, dtype=torch.int64, device=self._device)
+                rc = self._lib.fk_gqf_enumerate(ctypes.byref(self._geom), ctypes.byref(self._tables(self._cur)),
+                                                _lib.dptr(fp), _lib.dptr(cn), cap, ctypes.byref(n),
+                                                _lib.stream_ptr(torch))
+                if rc == _lib.FK_E_INVARIANT:
+                    raise ValidationError("table does not decode")
+                _lib.check(rc, "gqf enumerate")
+                if n.value <= cap:
+                    break
+                cap = n.value  # the distinct counter disagreed with the table
+        k = n.value
+        return (fp[:k].cpu().numpy().view(np.uint64), cn[:k].cpu().numpy().view(np.uint64))
+
+    def _enumerate_host(self):
         r = self.params.r
         slots = self._slots
         quotients, starts, ends = self._derive_structure()
