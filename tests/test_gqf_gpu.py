@@ -496,3 +496,54 @@ def test_runs_spilling_into_padding(oracle, r):
         assert g.find_run(qt) == o.find_run(qt)
     assert list(g.enumerate_items()) == list(g._enumerate_host())
     g.validate()
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_churn_fuzz_vs_oracle(oracle, monkeypatch, seed):
+    """Random churn at high load (the reference's dict-oracle fuzz, here
+    against the oracle image): point and bulk inserts/deletes with counts,
+    small batches (region-local paths) and large ones (rebuild), capacity
+    errors included; image, counts and found flags after every step."""
+    from paper_2212_09005_b200 import CapacityError, Gqf
+    rng = np.random.default_rng(500 + seed)
+    q = 11
+    g = Gqf(q=q, r=8, seed=seed)
+    o = _oracle(g, oracle)
+    pool = rng.integers(0, 2 ** 62, 1500, dtype=np.uint64)
+    # a third of the pool packed against the end of the table (runs into the padding)
+    tail = craft(g, [(int(x), int(y)) for x, y in zip(rng.integers((1 << q) - 200, 1 << q, 500),
+                                                       rng.integers(0, 256, 500))])
+    pool = np.concatenate([pool, tail])
+    raised = 0
+    for step in range(80):
+        size = int(rng.choice([1, 5, 40, 400]))
+        keys = pool[rng.integers(0, len(pool), size)]
+        cnt = rng.integers(1, 20, size).astype(np.uint64) if rng.random() < 0.5 else None
+        small = rng.random() < 0.5
+        monkeypatch.setenv("FK_GQF_SMALL", "100000" if small else "0")
+        op = rng.integers(0, 4)
+        if op == 0:
+            try:
+                g.insert_many(keys, cnt)
+            except CapacityError:
+                raised += 1
+            o.insert_many(keys, cnt)
+        elif op == 1:
+            try:
+                g.bulk_insert(keys, cnt)
+            except CapacityError:
+                pass
+            try:
+                o.bulk_insert(keys, cnt)
+            except Exception:
+                pass
+        elif op == 2:
+            assert np.array_equal(np.asarray(g.delete_many(keys, cnt)), o.delete_many(keys, cnt).astype(bool))
+        else:
+            assert np.array_equal(np.asarray(g.bulk_delete(keys, cnt)),
+                                  np.asarray(o.bulk_delete(keys, cnt)).astype(bool))
+        same_image(g, o)
+        assert np.array_equal(g.count_many(pool), o.count_many(pool))
+    assert raised > 0  # the capacity paths ran
+    g.validate()
+    assert list(g.enumerate_items()) == list(g._enumerate_host())
