@@ -273,3 +273,30 @@ def test_ordered_kernels_bit_exact(oracle, monkeypatch, onebar, nb, res_shift, c
     _same_tables(f, o)
     assert f.counters == o.counters
     f.validate()
+
+
+@pytest.mark.parametrize("geom,onebar", [("u16", "1"), ("u16", "0"), ("u32v", "1")])
+def test_ordered_churn_fuzz_vs_oracle(oracle, monkeypatch, geom, onebar):
+    """Interleaved ordered insert / delete batches (duplicates, tombstone
+    reuse, overfill into the backing table and FULL codes) through both
+    ordered kernels: codes, removed flags and the image equal the oracle's
+    after every batch."""
+    from paper_2212_09005_b200 import Tcf
+    monkeypatch.setenv("FK_ORD_ONEBAR", onebar)
+    monkeypatch.setenv("FK_ORD_WINDOW", str(1 << 20))
+    kw = dict(tag_bits=16, slot_bits=32) if geom == "u32v" else {}
+    f = Tcf(num_blocks=1 << 14, **kw)
+    o = _oracle(f, oracle)
+    rng = np.random.default_rng(7 + len(geom) + int(onebar))
+    pool = counter_keys(4242, 400_000)
+    for step in range(12):
+        keys = pool[rng.integers(0, len(pool), int(rng.integers(1000, 120_000)))]
+        if rng.random() < 0.6:
+            vals = None
+            if geom == "u32v":
+                vals = rng.integers(0, 1 << 16, len(keys)).astype(np.uint64)
+            assert np.array_equal(f.insert_many(keys, vals), o.insert_many(keys, vals)), step
+        else:
+            assert np.array_equal(f.delete_many(keys), o.delete_many(keys).astype(bool)), step
+        _same_tables(f, o)
+    assert f.counters == o.counters
