@@ -77,3 +77,21 @@ def test_c4_q26_counting_properties():
     g.bulk_delete(w["uniq"])
     assert g.occupied_slots == 0 and g.total_items == 0
     g.validate()
+
+
+def test_bulk_tcf_2p23_block_parallel_route_bit_exact(oracle):
+    """2^23 slots (2^16 blocks: the block-parallel routing path) at 0.9 load
+    in two batches: failed keys, image, fill, backing and deletes equal the
+    oracle's."""
+    from paper_2212_09005_b200 import BulkTcf
+    f = BulkTcf(num_blocks=1 << 16)
+    p = f.params
+    o = oracle.OracleBulkTcf(p.num_blocks, 128, 16, np.uint16, p.backing_slots, p.cut_slots, p.probe_limit, 0)
+    keys = counter_keys(2323, int(0.9 * (1 << 23)))
+    for part in np.array_split(keys, 2):
+        assert np.array_equal(np.asarray(f.insert_batch(part)), np.asarray(o.insert_batch(part)))
+    assert np.array_equal(f._blocks, o.blocks) and np.array_equal(f._fill, o.fill)
+    assert np.array_equal(f._backing, o.backing)
+    d = keys[::3]
+    assert np.array_equal(np.asarray(f.delete_batch(d)), np.asarray(o.delete_batch(d)).astype(bool))
+    assert np.array_equal(f._blocks, o.blocks) and np.array_equal(f._fill, o.fill)
