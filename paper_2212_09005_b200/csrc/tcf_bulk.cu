@@ -408,7 +408,14 @@ __global__ void __launch_bounds__(32) k_btcf_route_seq(const uint32_t *__restric
 // pays off on large tables only (the caller keeps the warp walk below 2^16
 // blocks).
 constexpr int kRouteW = 1024, kRouteHT = 4096;
-constexpr size_t kRouteSmem = (size_t)kRouteHT * 12 + (size_t)kRouteW * 12;
+constexpr size_t kRouteSmem = (size_t)kRouteHT * 12 + (size_t)kRouteW * 12 + (size_t)kRouteW * 16;
+
+__device__ __forceinline__ void cp_async4(void *smem, const void *gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
 __global__ void __launch_bounds__(kRouteW, 1) k_btcf_route_prefix(const uint32_t *__restrict__ lb1,
                                                                   const uint32_t *__restrict__ lb2, int64_t m,
@@ -419,8 +426,12 @@ __global__ void __launch_bounds__(kRouteW, 1) k_btcf_route_prefix(const uint32_t
   int *ht_a = reinterpret_cast<int *>(ht_key + kRouteHT), *ht_b = ht_a + kRouteHT;
   uint32_t *s_y = reinterpret_cast<uint32_t *>(ht_b + kRouteHT), *s_a = s_y + kRouteW;
   int32_t *s_d = reinterpret_cast<int32_t *>(s_a + kRouteW);
+  // ring of the next 2W leftovers (b1, b2): slot i % 2W holds leftover i;
+  // refilled with cp.async a window ahead of use
+  uint32_t *ring_a = reinterpret_cast<uint32_t *>(s_d + kRouteW), *ring_b = ring_a + 2 * kRouteW;
   __shared__ int s_first;
   const int k = threadIdx.x;
+  constexpr int RM = 2 * kRouteW - 1;
   auto slot = [&](uint32_t blk) {  // insert-or-find in the open-addressed table
     uint32_t h = (blk * 2654435761u) & (kRouteHT - 1);
     for (;;) {
@@ -429,8 +440,15 @@ __global__ void __launch_bounds__(kRouteW, 1) k_btcf_route_prefix(const uint32_t
       h = (h + 1) & (kRouteHT - 1);
     }
   };
+  for (int i = k; i < 2 * kRouteW && i < m; i += kRouteW) {
+    cp_async4(&ring_a[i], lb1 + i);
+    cp_async4(&ring_b[i], lb2 + i);
+  }
+  cp_async_commit();
+  cp_async_commit();  // (an empty group: the loop waits for all but the newest)
   for (int64_t base = 0; base < m;) {
     const int cnt = m - base < kRouteW ? (int)(m - base) : kRouteW;
+    cp_async_wait1();
     for (int i = k; i < kRouteHT; i += kRouteW) {
       ht_key[i] = 0xFFFFFFFFu;
       ht_a[i] = ht_b[i] = kRouteW;
@@ -438,10 +456,12 @@ __global__ void __launch_bounds__(kRouteW, 1) k_btcf_route_prefix(const uint32_t
     if (k == 0) s_first = cnt;
     __syncthreads();
     const bool live = k < cnt;
-    uint32_t a = 0, b = 0, ha = 0, hb = 0;
+    uint32_t a = 0, b = 0, ha = 0, hb = 0, y = 0, x0 = 0;
     if (live) {
-      a = lb1[base + k];
-      b = lb2[base + k];
+      a = ring_a[(base + k) & RM];
+      b = ring_b[(base + k) & RM];
+      y = load[b];   // issued before the conflict test; valid for prefix members
+      x0 = load[a];  // (no prefix leftover but its own group touches either)
       ha = slot(a);
       hb = slot(b);
       atomicMin(&ht_a[ha], k);
@@ -452,6 +472,7 @@ __global__ void __launch_bounds__(kRouteW, 1) k_btcf_route_prefix(const uint32_t
     if (live && (b == a || ht_a[hb] < k || ht_b[hb] < k || ht_b[ha] < k)) atomicMin(&s_first, k);
     __syncthreads();
     const int first = s_first;
+    int adv;
     if (first == 0) {  // leftover 0 alone (b1 == b2): the plain rule
       if (k == 0) {
         const uint32_t la = load[a], lbv = load[b];
@@ -460,43 +481,49 @@ __global__ void __launch_bounds__(kRouteW, 1) k_btcf_route_prefix(const uint32_t
         if (lp < B) load[d] = lp + 1;
         dest[base] = lp < B ? (int32_t)d : -1;
       }
+      adv = 1;
+    } else {
+      const bool act = k < first;
+      if (act) {
+        s_y[k] = y;
+        s_a[k] = a;
+      }
       __syncthreads();
-      base += 1;
-      continue;
-    }
-    const bool act = k < first;
-    if (act) {
-      s_y[k] = load[b];
-      s_a[k] = a;
-    }
-    __syncthreads();
-    // group heads scan their group in order
-    if (act && (k == 0 || s_a[k - 1] != a)) {
-      uint32_t x = load[a];
-      int j = k;
-      for (; j < first && s_a[j] == a; j++) {
-        const uint32_t y = s_y[j];
-        const uint32_t t = y < B - 1 ? y : B - 1;
-        if (x <= t) {
-          s_d[j] = (int32_t)a;
-          x++;
-        } else {
-          s_d[j] = y < B ? -2 : -1;  // -2: takes its b2 (x > y)
+      // group heads scan their group in order
+      if (act && (k == 0 || s_a[k - 1] != a)) {
+        uint32_t x = x0;
+        for (int j = k; j < first && s_a[j] == a; j++) {
+          const uint32_t yj = s_y[j];
+          const uint32_t t = yj < B - 1 ? yj : B - 1;
+          if (x <= t) {
+            s_d[j] = (int32_t)a;
+            x++;
+          } else {
+            s_d[j] = yj < B ? -2 : -1;  // -2: takes its b2 (x > y)
+          }
         }
+        load[a] = x;
       }
-      load[a] = x;
-    }
-    __syncthreads();
-    if (act) {
-      int32_t d = s_d[k];
-      if (d == -2) {
-        load[b] = s_y[k] + 1;  // b is touched by no other leftover of the prefix
-        d = (int32_t)b;
+      __syncthreads();
+      if (act) {
+        int32_t d = s_d[k];
+        if (d == -2) {
+          load[b] = y + 1;  // b is touched by no other leftover of the prefix
+          d = (int32_t)b;
+        }
+        dest[base + k] = d;
       }
-      dest[base + k] = d;
+      adv = first;
     }
+    // refill the consumed ring slots with leftovers [base + 2W, base + 2W + adv)
+    if (k < adv && base + 2 * kRouteW + k < m) {
+      const int64_t i = base + 2 * kRouteW + k;
+      cp_async4(&ring_a[i & RM], lb1 + i);
+      cp_async4(&ring_b[i & RM], lb2 + i);
+    }
+    cp_async_commit();
     __syncthreads();
-    base += first;
+    base += adv;
   }
 }
 
