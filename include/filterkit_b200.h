@@ -118,6 +118,11 @@ int fk_tcf_delete(const fk_tcf_geom *g, void *blocks, void *backing, const uint6
                   int keys_are_fps, int64_t n, uint8_t *removed, int64_t *counters, int mode,
                   void *workspace, size_t ws_bytes, void *stream);
 
+/* Census for Tcf.validate / load_factor (tcf.py:196-249) without copying the
+ * table to the host.  Synchronous; out4 (HOST) = live main slots, main slots
+ * with a reserved tag, live backing slots, backing slots with a reserved tag. */
+int fk_tcf_census(const fk_tcf_geom *g, const void *blocks, const void *backing, int64_t *out4, void *stream);
+
 /* ---- bulk TCF (sorted, front-packed blocks) ----------------------------- */
 
 /* Geometry, derived on the host exactly as BulkTcfParams (tcf_bulk.py:43-77).

@@ -66,6 +66,7 @@ _SIGS = {
     "fk_tcf_workspace_bytes": (c_sz, [ctypes.POINTER(TcfGeom), c_i64, c_i32]),
     "fk_tcf_insert": (c_i32, [ctypes.POINTER(TcfGeom), c_vp, c_vp, c_vp, c_i32, c_vp, c_i64, c_vp,
                               c_vp, c_i32, c_vp, c_sz, c_vp]),
+    "fk_tcf_census": (c_i32, [ctypes.POINTER(TcfGeom), c_vp, c_vp, c_vp, c_vp]),
     "fk_tcf_query": (c_i32, [ctypes.POINTER(TcfGeom), c_vp, c_vp, c_vp, c_i32, c_i64, c_vp, c_vp, c_vp]),
     "fk_tcf_delete": (c_i32, [ctypes.POINTER(TcfGeom), c_vp, c_vp, c_vp, c_i32, c_i64, c_vp, c_vp,
                               c_i32, c_vp, c_sz, c_vp]),

@@ -143,6 +143,49 @@ static int prep_ordered(const fk_tcf_geom *g, int64_t n, void *ws, size_t ws_byt
   return 0;
 }
 
+// Census of a slot array for validate() / load_factor() (tcf.py:196-249):
+// live slots (word > TOMBSTONE) and live slots whose tag bits are reserved
+// (tag < 2).  Grid-stride, warp-reduced, one atomic per warp.
+template <typename S>
+__global__ void k_tcf_census(const S *__restrict__ slots, int64_t n, uint64_t fmask,
+                             unsigned long long *__restrict__ out) {
+  unsigned long long live = 0, bad = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t w = slots[i];
+    if (w > 1) {
+      live++;
+      bad += (w & fmask) < 2;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    live += __shfl_xor_sync(0xFFFFFFFFu, live, o);
+    bad += __shfl_xor_sync(0xFFFFFFFFu, bad, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (live) atomicAdd(&out[0], live);
+    if (bad) atomicAdd(&out[1], bad);
+  }
+}
+
+template <typename S>
+static int census_t(const void *p, int64_t n, uint64_t fmask, unsigned long long *d, cudaStream_t st) {
+  if (n <= 0) return 0;
+  int64_t blocks = (n + 255) / 256;
+  int64_t cap = (int64_t)num_sms() * 8;
+  k_tcf_census<S><<<(int)(blocks < cap ? blocks : cap), 256, 0, st>>>((const S *)p, n, fmask, d);
+  FK_CHECK_LAUNCH();
+  return 0;
+}
+
+static int census(int wbytes, const void *p, int64_t n, uint64_t fmask, unsigned long long *d, cudaStream_t st) {
+  switch (wbytes) {
+    case 1: return census_t<uint8_t>(p, n, fmask, d, st);
+    case 4: return census_t<uint32_t>(p, n, fmask, d, st);
+    case 8: return census_t<uint64_t>(p, n, fmask, d, st);
+    default: return census_t<uint16_t>(p, n, fmask, d, st);
+  }
+}
+
 }  // namespace fk
 
 using namespace fk;
@@ -190,6 +233,26 @@ int fk_tcf_delete(const fk_tcf_geom *g, void *blocks, void *backing, const uint6
   if (n > 0xFFFFFFF0LL) return FK_E_ARG;
   int rc = prep_ordered(g, n, ws, ws_bytes, &c.X, st);
   return rc ? rc : run(g, kOpDelOrd, P, c, st);
+}
+
+int fk_tcf_census(const fk_tcf_geom *g, const void *blocks, const void *backing, int64_t *out4, void *stream) {
+  if (!geom_ok(g) || !out4) return FK_E_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  unsigned long long *d = nullptr;
+  FK_TRY(cudaMallocAsync((void **)&d, 4 * sizeof(unsigned long long), st));
+  FK_TRY(cudaMemsetAsync(d, 0, 4 * sizeof(unsigned long long), st));
+  const uint64_t fm = g->tag_bits >= 64 ? ~0ULL : ((1ULL << g->tag_bits) - 1);
+  int rc = census(g->slot_bytes, blocks, g->num_blocks * (int64_t)g->block_slots, fm, d, st);
+  if (!rc) rc = census(g->slot_bytes, backing, g->backing_slots, fm, d + 2, st);
+  unsigned long long h[4] = {0, 0, 0, 0};
+  if (!rc) {
+    cudaError_t e = cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) rc = -(int)e;
+  }
+  cudaFreeAsync(d, st);
+  for (int i = 0; i < 4; i++) out4[i] = (int64_t)h[i];
+  return rc;
 }
 
 }  // extern "C"

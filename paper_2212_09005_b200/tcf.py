@@ -381,8 +381,19 @@ class Tcf:
         blk = self._blocks[block_index * p.block_slots:(block_index + 1) * p.block_slots]
         return int((blk > TOMBSTONE).sum())
 
+    def _census(self):
+        """(live main, reserved-tag main, live backing, reserved-tag backing),
+        counted on the device (fk_tcf_census)."""
+        out = np.zeros(4, dtype=np.int64)
+        with self._op_lock:
+            self._t.before_device_op()
+            _lib.check(self._lib.fk_tcf_census(ctypes_byref(self._geom), self._t.ptr("blocks"),
+                                               self._t.ptr("backing"), out.ctypes.data_as(_ctypes_vp()),
+                                               _lib.stream_ptr(self._torch)), "tcf census")
+        return [int(x) for x in out]
+
     def load_factor(self):
-        return float((self._blocks > TOMBSTONE).sum()) / self.params.main_slots
+        return self._census()[0] / self.params.main_slots
 
     def size_bits(self):
         p = self.params
@@ -394,15 +405,13 @@ class Tcf:
         return {"inserts_ok": int(c[0]), "inserts_backing": int(c[1]), "deletes_ok": int(c[2])}
 
     def validate(self):
-        """Structural invariants (tcf.py:232-249); raises ValidationError."""
-        p = self.params
-        fmask = np.uint64((1 << p.tag_bits) - 1 if p.tag_bits < 64 else (1 << 64) - 1)
-        used_total = 0
-        for name, arr in (("main", self._blocks), ("backing", self._backing)):
-            used = arr[arr > TOMBSTONE].astype(np.uint64)
-            if len(used) and int((used & fmask).min()) < 2:
+        """Structural invariants (tcf.py:232-249) from a device census;
+        raises ValidationError."""
+        live_m, bad_m, live_b, bad_b = self._census()
+        for name, bad in (("main", bad_m), ("backing", bad_b)):
+            if bad:
                 raise ValidationError("%s table holds a used slot with a reserved tag" % name)
-            used_total += len(used)
+        used_total = live_m + live_b
         c = self.counters
         expect = c["inserts_ok"] - c["deletes_ok"]
         if used_total != expect:
@@ -413,3 +422,8 @@ class Tcf:
 def ctypes_byref(x):
     import ctypes
     return ctypes.byref(x)
+
+
+def _ctypes_vp():
+    import ctypes
+    return ctypes.c_void_p

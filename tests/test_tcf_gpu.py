@@ -300,3 +300,31 @@ def test_ordered_churn_fuzz_vs_oracle(oracle, monkeypatch, geom, onebar):
             assert np.array_equal(f.delete_many(keys), o.delete_many(keys).astype(bool)), step
         _same_tables(f, o)
     assert f.counters == o.counters
+
+
+@pytest.mark.parametrize("kw", [{}, dict(tag_bits=8, slot_bits=8), dict(tag_bits=16, slot_bits=32)])
+def test_device_census_validate_and_load_factor(kw):
+    """validate() / load_factor() count on the device (fk_tcf_census): they
+    match the host mirror and catch reserved tags in either table."""
+    from paper_2212_09005_b200 import Tcf, ValidationError
+    f = Tcf(num_blocks=2048, **kw)
+    keys = counter_keys(61, 30_000)
+    f.insert_many(keys)
+    f.delete_many(keys[::4])
+    blocks, backing = f._blocks, f._backing
+    assert f.load_factor() == float((blocks > 1).sum()) / len(blocks)
+    f.validate()
+    i = int(np.flatnonzero(blocks > 1)[0])
+    old = blocks[i]
+    blocks[i] = (int(blocks[i]) >> f.params.tag_bits << f.params.tag_bits) | 1 if f.params.slot_bits > 8 else 1
+    if blocks[i] > 1:  # a live word whose tag is reserved
+        with pytest.raises(ValidationError):
+            f.validate()
+    blocks[i] = old
+    f.validate()
+    if len(backing):
+        j = int(np.flatnonzero(backing <= 1)[0])
+        backing[j] = 1 << f.params.tag_bits if f.params.slot_bits > f.params.tag_bits else 0
+        if backing[j] > 1:
+            with pytest.raises(ValidationError):
+                f.validate()
