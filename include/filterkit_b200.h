@@ -140,6 +140,14 @@ typedef struct fk_btcf_geom {
     uint64_t seed;
 } fk_btcf_geom;
 
+/* Sorted-block invariants of BulkTcf.validate (tcf_bulk.py:354-374) on the
+ * device.  Synchronous; out8 (HOST): [0] bitmask (1 fill over capacity,
+ * 2 reserved word in a live prefix, 4 unsorted prefix, 8 non-empty tail),
+ * [1..4] first offending block per check, [5] sum of fill, [6] live backing
+ * slots. */
+int fk_btcf_validate(const fk_btcf_geom *g, const void *blocks, const uint32_t *fill, const void *backing,
+                     int64_t *out8, void *stream);
+
 /* replaces BulkTcf.insert_batch's kernel sequence (tcf_bulk.py:179-257):
  * _partition_fps + btcf_merge_lists (shortcut) + btcf_route + btcf_merge_lists
  * (dest-grouped) + backing_insert_batch.  `fill` is the device u32[nb] fill

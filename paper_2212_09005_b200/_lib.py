@@ -72,6 +72,7 @@ _SIGS = {
                               c_i32, c_vp, c_sz, c_vp]),
     "fk_btcf_insert": (c_i32, [ctypes.POINTER(BtcfGeom), c_vp, c_vp, c_vp, c_vp, c_i32, c_i64, c_vp, c_vp,
                                c_vp, c_vp, c_vp]),
+    "fk_btcf_validate": (c_i32, [ctypes.POINTER(BtcfGeom), c_vp, c_vp, c_vp, c_vp, c_vp]),
     "fk_btcf_query": (c_i32, [ctypes.POINTER(BtcfGeom), c_vp, c_vp, c_vp, c_vp, c_i32, c_i64, c_vp, c_vp]),
     "fk_btcf_delete": (c_i32, [ctypes.POINTER(BtcfGeom), c_vp, c_vp, c_vp, c_vp, c_i32, c_i64, c_vp, c_vp,
                                c_vp]),

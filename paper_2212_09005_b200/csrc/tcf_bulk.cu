@@ -1017,7 +1017,83 @@ BDev make_dev(const fk_btcf_geom *g, void *blocks, uint32_t *fill, void *backing
 
 using namespace fk;
 
+namespace fk {
+namespace {
+// Sorted-block invariants of BulkTcf.validate (tcf_bulk.py:354-374), one
+// thread per block: v[0] |= 1 fill over capacity, 2 a reserved word in the
+// live prefix, 4 an unsorted prefix, 8 a non-empty tail; v[1 + c] = first
+// such block (atomicMin); v[5] = sum of fill; v[6] = live backing slots.
+template <typename S>
+__global__ void k_btcf_validate(const S *__restrict__ blocks, const uint32_t *__restrict__ fill, int64_t nb, int B,
+                                const S *__restrict__ backing, int64_t bsize,
+                                unsigned long long *__restrict__ v) {
+  unsigned long long sumf = 0, liveb = 0;
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t f = fill[b];
+    sumf += f;
+    unsigned bad = 0;
+    if ((int64_t)f > B) bad |= 1;
+    const S *blk = blocks + b * (int64_t)B;
+    uint64_t prev = 0;
+    for (int j = 0; j < B; j++) {
+      const uint64_t w = blk[j];
+      if ((uint32_t)j < f) {
+        if (w < 2) bad |= 2;
+        if (j > 0 && w < prev) bad |= 4;
+        prev = w;
+      } else if (w != 0) {
+        bad |= 8;
+      }
+    }
+    for (int c = 0; c < 4; c++)
+      if (bad >> c & 1) {
+        atomicOr(&v[0], 1ull << c);
+        atomicMin(&v[1 + c], (unsigned long long)b);
+      }
+  }
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < bsize; i += (int64_t)gridDim.x * blockDim.x)
+    liveb += (uint64_t)backing[i] > 1;
+  if (sumf) atomicAdd(&v[5], sumf);
+  if (liveb) atomicAdd(&v[6], liveb);
+}
+
+template <typename S>
+int btcf_validate_t(const fk_btcf_geom *g, const void *blocks, const uint32_t *fill, const void *backing,
+                    int64_t *out8, cudaStream_t st) {
+  unsigned long long *d = nullptr;
+  FK_TRY(cudaMallocAsync((void **)&d, 8 * sizeof(unsigned long long), st));
+  unsigned long long init[8] = {0, ~0ull, ~0ull, ~0ull, ~0ull, 0, 0, 0};
+  int rc = 0;
+  cudaError_t e = cudaMemcpyAsync(d, init, sizeof(init), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) {
+    k_btcf_validate<S><<<grid_for(g->num_blocks), 256, 0, st>>>((const S *)blocks, fill, g->num_blocks,
+                                                              g->block_slots, (const S *)backing, g->backing_slots,
+                                                              d);
+    e = cudaGetLastError();
+  }
+  unsigned long long h[8];
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaFreeAsync(d, st);
+  if (e != cudaSuccess) return -(int)e;
+  for (int i = 0; i < 8; i++) out8[i] = (int64_t)h[i];
+  return rc;
+}
+}  // namespace
+}  // namespace fk
+
 extern "C" {
+
+int fk_btcf_validate(const fk_btcf_geom *g, const void *blocks, const uint32_t *fill, const void *backing,
+                     int64_t *out8, void *stream) {
+  if (!geom_ok(g) || !out8) return FK_E_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (g->slot_bytes) {
+    case 1: return btcf_validate_t<uint8_t>(g, blocks, fill, backing, out8, st);
+    case 4: return btcf_validate_t<uint32_t>(g, blocks, fill, backing, out8, st);
+    default: return btcf_validate_t<uint16_t>(g, blocks, fill, backing, out8, st);
+  }
+}
 
 int fk_btcf_insert(const fk_btcf_geom *g, void *blocks, uint32_t *fill, void *backing, const uint64_t *keys,
                    int keys_are_fps, int64_t n, uint64_t *failed_keys, int64_t *n_failed, int64_t *counters,

@@ -287,8 +287,38 @@ class BulkTcf:
         out.extend((-1, int(w)) for w in backing[(backing != EMPTY) & (backing != TOMBSTONE)].tolist())
         return out
 
+    _VMSG = ((1, "block %d fill over capacity"), (2, "block %d stores a reserved word"),
+             (4, "block %d prefix not sorted"), (8, "block %d tail not empty"))
+
     def validate(self):
-        """Sorted-block invariants (tcf_bulk.py:354-374); raises ValidationError."""
+        """Sorted-block invariants (tcf_bulk.py:354-374), checked on the
+        device (fk_btcf_validate); raises ValidationError.  On a violation,
+        tables small enough for the host re-run the host checks so the
+        message names the same first failure."""
+        out = np.zeros(8, dtype=np.int64)
+        with self._op_lock:
+            self._t.before_device_op()
+            b, f, bk = self._ptrs()
+            _lib.check(self._lib.fk_btcf_validate(ctypes.byref(self._geom), b, f, bk,
+                                                  out.ctypes.data_as(ctypes.c_void_p),
+                                                  _lib.stream_ptr(self._torch)), "btcf validate")
+        first = None
+        for bit, msg in self._VMSG:
+            if int(out[0]) & bit:
+                first = msg % int(out[1 + bit.bit_length() - 1])
+                break
+        c = self.counters
+        used = int(out[5]) + int(out[6])
+        if first is None and used != c["inserts_ok"] - c["deletes_ok"]:
+            first = "stored words (%d) do not match inserts-deletes (%d)" % (used, c["inserts_ok"] - c["deletes_ok"])
+        if first is None:
+            return
+        if self.params.main_slots <= (1 << 22):
+            self._validate_host()
+        raise ValidationError(first)
+
+    def _validate_host(self):
+        """The reference's host checks over the mirrored image."""
         p = self.params
         B = p.block_slots
         blocks = self._blocks.reshape(p.num_blocks, B)

@@ -163,3 +163,33 @@ def test_device_tensors_and_validate():
     blk[b * 128], blk[b * 128 + 1] = 0xFFFF, 2
     with pytest.raises(ValidationError):
         f.validate()
+
+
+def test_device_validate_agrees_with_host_checks():
+    """BulkTcf.validate runs on the device (fk_btcf_validate); every kind of
+    corruption the reference's host checks reject is rejected, and a clean
+    table passes."""
+    from paper_2212_09005_b200 import BulkTcf, ValidationError
+    f = BulkTcf(num_blocks=256)
+    f.insert_batch(counter_keys(71, 25_000))
+    f.validate()
+    B = f.params.block_slots
+    fill = f._fill
+    blk = int(np.flatnonzero(fill > 3)[0])
+    base = blk * B
+
+    def corrupt(fn):
+        blocks, fl = f._blocks, f._fill
+        saved = (blocks.copy(), fl.copy())
+        fn(blocks, fl)
+        with pytest.raises(ValidationError):
+            f.validate()
+        blocks[:] = saved[0]
+        fl[:] = saved[1]
+        f.validate()
+
+    corrupt(lambda b, fl: fl.__setitem__(blk, B + 1))                      # fill over capacity
+    corrupt(lambda b, fl: b.__setitem__(base + 1, 1))                      # reserved word in the prefix
+    corrupt(lambda b, fl: b.__setitem__(base, b[base + 2] + 1))            # unsorted prefix
+    corrupt(lambda b, fl: b.__setitem__(base + int(fl[blk]), 77))          # tail not empty
+    corrupt(lambda b, fl: fl.__setitem__(blk, fl[blk] - 1) or b.__setitem__(base + int(fl[blk]), 0))  # count mismatch
