@@ -1026,8 +1026,197 @@ __global__ void __launch_bounds__(256, 4)
 // (B=16); BF=32 the CG-32 sweep point (B=32, u16); everything else BF=0.
 // keys per tile per round in the ordered kernel: 2 on the register-resident
 // G=1 path (4 spills at the 64-register cap of 4 CTAs/SM), 4 otherwise
+// ---------------------------------------------------------------------------
+// Multi-pass ordered kernel for cooperative groups of G >= 2 lanes.  Same
+// rounds and reservations as k_tcf_ordered, but the reserve and commit passes
+// each stream the window in chunks of KB keys per tile and the commit pass
+// re-derives the key's blocks and tag from the (L2-resident) window keys, so
+// the window is not capped at one chunk per tile.  Measured at 2^28 slots
+// (profiles/r1g_cg_ordered.txt): G = 2 6.6 G inserts/s vs 4.0 for the
+// register-held kernel, G = 8 3.7 vs 2.0; G = 1 is the other way round.
+template <typename S, int G, int BF, int KB, int OP>
+__global__ void __launch_bounds__(256, 4)
+    k_tcf_ordered_mp(TcfDev P, const uint64_t *__restrict__ keys, const uint64_t *__restrict__ values, int64_t n,
+                     uint8_t *__restrict__ out, int64_t *__restrict__ counters, OrdScratch X) {
+  cg::grid_group grid = cg::this_grid();
+  Tile<G> t;
+  const int64_t tiles = (int64_t)gridDim.x * (blockDim.x / G);
+  const int64_t tid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+  const int64_t Wn = X.window;
+  long long n_a = 0;  // insert: placed in a block; delete: removed
+  int64_t F = 0;
+  int64_t nc = 0;
+  int cur = 0;
+  unsigned round = 0;
+  const uint64_t pol_keep = l2_evict_last(), pol_stream = l2_evict_first();
+
+  for (;;) {
+    int64_t room = Wn - nc;
+    if (room < 0) room = 0;
+    int64_t Fend = F + room < n ? F + room : n;
+    int64_t total = (Fend - F) + nc;
+    const uint32_t *cin = X.carry[cur];
+    uint32_t *cout = X.carry[cur ^ 1];
+
+    // ---- reserve --------------------------------------------------------
+    for (int64_t base = tid; base < total; base += tiles * KB) {
+      uint32_t idx[KB], b1[KB], b2[KB];
+      bool ok[KB];
+#pragma unroll
+      for (int j = 0; j < KB; j++) {
+        int64_t e = base + (int64_t)j * tiles;
+        ok[j] = e < total;
+        idx[j] = ok[j] ? (e < nc ? __ldcg(cin + e) : (uint32_t)(F + e - nc)) : 0u;
+      }
+#pragma unroll
+      for (int j = 0; j < KB; j++) {
+        if (!ok[j]) continue;
+        KeyInfo ki = key_info(P, X.hints ? ld_stream_u64(keys + idx[j], pol_stream) : keys[idx[j]]);
+        b1[j] = (uint32_t)ki.b1;
+        b2[j] = (uint32_t)ki.b2;
+      }
+      if (t.lane == 0) {
+#pragma unroll
+        for (int j = 0; j < KB; j++) {
+          if (!ok[j]) continue;
+          uint32_t g1 = b1[j] >> X.res_shift, g2 = b2[j] >> X.res_shift;
+          if (X.hints) {
+            red_min_u32(&X.res[g1], idx[j], pol_keep);
+            if (g2 != g1) red_min_u32(&X.res[g2], idx[j], pol_keep);
+          } else {
+            atomicMin(&X.res[g1], idx[j]);
+            if (g2 != g1) atomicMin(&X.res[g2], idx[j]);
+          }
+        }
+      }
+    }
+    grid.sync();
+
+    // ---- commit ---------------------------------------------------------
+    if (blockIdx.x == 0 && threadIdx.x == 0) X.ctl[cur] = 0;  // list `cur` is consumed this round
+    for (int64_t base = tid;; base += tiles * KB) {
+      // warp-uniform trip count: lanes past the end still join the shuffles
+      if (!__any_sync(0xFFFFFFFFu, base < total)) break;
+      uint32_t idx[KB], b1[KB], b2[KB];
+      uint64_t word[KB];
+      bool ok[KB], hold[KB];
+#pragma unroll
+      for (int j = 0; j < KB; j++) {
+        int64_t e = base + (int64_t)j * tiles;
+        ok[j] = e < total;
+        idx[j] = ok[j] ? (e < nc ? __ldcg(cin + e) : (uint32_t)(F + e - nc)) : 0u;
+      }
+#pragma unroll
+      for (int j = 0; j < KB; j++) {
+        if (!ok[j]) continue;
+        KeyInfo ki = key_info(P, X.hints ? ld_stream_u64(keys + idx[j], pol_stream) : keys[idx[j]]);
+        b1[j] = (uint32_t)ki.b1;
+        b2[j] = (uint32_t)ki.b2;
+        word[j] = OP == 0 ? ((P.f >= 64 ? 0 : ((values ? values[idx[j]] : 0) << P.f)) | ki.tag) : ki.tag;
+      }
+#pragma unroll
+      for (int j = 0; j < KB; j++)
+        hold[j] = ok[j] && (X.hints ? ld_cg_u32(&X.res[b1[j] >> X.res_shift], pol_keep)
+                                    : __ldcg(&X.res[b1[j] >> X.res_shift])) == idx[j] &&
+                  (X.hints ? ld_cg_u32(&X.res[b2[j] >> X.res_shift], pol_keep)
+                           : __ldcg(&X.res[b2[j] >> X.res_shift])) == idx[j];
+      Chunk<S, G, BF> c1[KB];
+      S *blocks = reinterpret_cast<S *>(P.blocks);
+#pragma unroll
+      for (int j = 0; j < KB; j++)
+        if (hold[j]) c1[j].template load<true>(blocks + (uint64_t)b1[j] * P.B, P.B, t.lane);
+      // carry the losers: one warp-aggregated atomicAdd per pass
+      {
+        unsigned mine = 0;
+#pragma unroll
+        for (int j = 0; j < KB; j++) mine += (ok[j] && !hold[j] && t.lane == 0) ? 1u : 0u;
+        unsigned lane = threadIdx.x & 31;
+        unsigned incl = mine;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          unsigned v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+          if ((int)lane >= o) incl += v;
+        }
+        unsigned total_w = __shfl_sync(0xFFFFFFFFu, incl, 31);
+        unsigned basepos = 0;
+        if (lane == 31 && total_w) basepos = atomicAdd(&X.ctl[cur ^ 1], total_w);
+        basepos = __shfl_sync(0xFFFFFFFFu, basepos, 31);
+        unsigned pos = basepos + incl - mine;
+#pragma unroll
+        for (int j = 0; j < KB; j++)
+          if (ok[j] && !hold[j] && t.lane == 0) cout[pos++] = idx[j];
+      }
+#pragma unroll
+      for (int j = 0; j < KB; j++) {
+        if (!ok[j] || !hold[j]) continue;
+        bool defer;
+        if (OP == 0) {
+          uint8_t code = commit_insert<S, G, BF>(P, t, b1[j], b2[j], word[j], c1[j]);
+          defer = code == 4;
+          if (!defer && t.lane == 0) {
+            out[idx[j]] = code;
+            n_a++;
+          }
+        } else {
+          int done = commit_delete<S, G, BF>(P, t, b1[j], b2[j], word[j], c1[j]);
+          defer = !done && P.bsize;
+          if (!defer && t.lane == 0) {
+            out[idx[j]] = done ? 1 : 0;
+            n_a += done;
+          }
+        }
+        if (t.lane == 0) {
+          if (defer) {
+            unsigned slot = atomicAdd(&X.ctl[2], 1u);
+            if (slot < X.defer_cap) {
+              X.defer_idx[slot] = idx[j];
+              X.defer_pend[slot] = 1;
+            }
+          }
+          // only the holder writes these words now
+          if (X.hints) {
+            st_u32(&X.res[b1[j] >> X.res_shift], kNoRes, pol_keep);
+            st_u32(&X.res[b2[j] >> X.res_shift], kNoRes, pol_keep);
+          } else {
+            X.res[b1[j] >> X.res_shift] = kNoRes;
+            X.res[b2[j] >> X.res_shift] = kNoRes;
+          }
+        }
+      }
+    }
+    grid.sync();
+    nc = (int64_t)__ldcg(&X.ctl[cur ^ 1]);
+    cur ^= 1;
+    F = Fend;
+    round++;
+    if (F >= n && nc == 0) break;
+  }
+
+  if (blockIdx.x == 0 && threadIdx.x == 0) X.ctl[5] = round;
+  const unsigned main_rounds = round;
+
+  long long n_b = 0;
+  round = ordered_backing_phase<S, G, OP>(P, keys, values, out, X, t, tiles, tid, grid, round, &n_a, &n_b);
+  if (blockIdx.x == 0 && threadIdx.x == 0) X.ctl[6] = round - main_rounds;
+  if (t.lane == 0) {
+    if (OP == 0) {
+      if (n_a) atomicAdd((unsigned long long *)&counters[0], (unsigned long long)n_a);
+      if (n_b) atomicAdd((unsigned long long *)&counters[1], (unsigned long long)n_b);
+    } else if (n_a) {
+      atomicAdd((unsigned long long *)&counters[2], (unsigned long long)n_a);
+    }
+  }
+}
+
+
 template <int G>
 constexpr int kOrdKB = G == 1 ? 2 : 4;
+
+template <typename S, int G, int BF, int OP>
+constexpr auto ord_kernel() {
+  if constexpr (G > 1) return k_tcf_ordered_mp<S, G, BF, kOrdKB<G>, OP>;
+  else return k_tcf_ordered<S, G, BF, kOrdKB<G>, OP>;
+}
 
 template <typename S, int G, int BF, int OP>
 static int launch_ordered(const TcfDev &P, const uint64_t *keys, const uint64_t *values, int64_t n, uint8_t *out,
@@ -1053,16 +1242,17 @@ static int launch_ordered(const TcfDev &P, const uint64_t *keys, const uint64_t 
       return 0;
     }
   }
-  auto kern = k_tcf_ordered<S, G, BF, kOrdKB<G>, OP>;
+  // G >= 2: the multi-pass kernel; G = 1: the register-held kernel, whose
+  // window is one chunk of kOrdKB<1> keys per tile and round
+  constexpr bool mp = G > 1;
+  auto kern = ord_kernel<S, G, BF, OP>();
   int per_sm = 0;
   FK_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
   if (per_sm < 1) return FK_E_ARG;
   if (X.ctas_per_sm > 0 && X.ctas_per_sm < per_sm) per_sm = X.ctas_per_sm;
   int grid = per_sm * num_sms();
-  // one chunk of kOrdKB<G> keys per tile and round (the kernel keeps them in
-  // registers between its reserve and commit passes)
   int64_t cap = (int64_t)grid * (256 / G) * kOrdKB<G>;
-  if (X.window > cap) X.window = cap;
+  if (!mp && X.window > cap) X.window = cap;
   void *args[] = {(void *)&P, (void *)&keys, (void *)&values, (void *)&n, (void *)&out, (void *)&counters, (void *)&X};
   FK_TRY(cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(256), args, 0, st));
   return 0;

@@ -43,6 +43,7 @@ def main():
     ap.add_argument("--log-slots", type=int, nargs="+", default=[20, 22, 24, 28])
     ap.add_argument("--cfg", nargs="+", default=["default"])
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--group-width", type=int, default=1)
     a = ap.parse_args()
     import torch
     from paper_2212_09005_b200 import Tcf, _lib
@@ -52,15 +53,15 @@ def main():
         nb = (1 << ls) // 16
         n = int(0.9 * (1 << ls))
         keys = bench.device_keys(torch, 1, bench.TAG_UNIFORM, n, dev)
-        filt = Tcf(num_blocks=nb, mode="ordered")
+        filt = Tcf(num_blocks=nb, group_width=a.group_width, mode="ordered")
         for cfg in a.cfg:
             env = {}
             if cfg != "default":
                 for kv in cfg.split(","):
                     k, v = kv.split("=")
                     env[{"W": "FK_ORD_WINDOW", "RS": "FK_ORD_RES_SHIFT", "CTAS": "FK_ORD_CTAS_PER_SM",
-                         "H": "FK_ORD_HINTS"}[k]] = v
-            for k in ("FK_ORD_WINDOW", "FK_ORD_RES_SHIFT", "FK_ORD_CTAS_PER_SM", "FK_ORD_HINTS"):
+                         "H": "FK_ORD_HINTS", "OB": "FK_ORD_ONEBAR"}[k]] = v
+            for k in ("FK_ORD_WINDOW", "FK_ORD_RES_SHIFT", "FK_ORD_CTAS_PER_SM", "FK_ORD_HINTS", "FK_ORD_ONEBAR"):
                 os.environ.pop(k, None)
             os.environ.update(env)
             rs = int(env.get("FK_ORD_RES_SHIFT", default_rs(nb)))
@@ -99,7 +100,7 @@ def main():
                 res[op]["ms"] = ms
                 res[op]["g_ops_per_s"] = n / ms / 1e6
                 res[op]["us_per_round"] = 1e3 * ms / max(1, res[op]["rounds"] + res[op]["backing_rounds"])
-            print(json.dumps({"log_slots": ls, "cfg": cfg, "rs": rs, **res}), flush=True)
+            print(json.dumps({"log_slots": ls, "G": a.group_width, "cfg": cfg, "rs": rs, **res}), flush=True)
         del keys, filt
         torch.cuda.empty_cache()
 
