@@ -875,46 +875,53 @@ __global__ void __launch_bounds__(256, 4)
   __shared__ unsigned s_warp[32];
   __shared__ unsigned s_base;
 
+  // this lane's first new input index for `need` slots: one frontier atomic
+  // per CTA (a single L2 address takes every grab), so the introduced keys
+  // always form a prefix of the input
+  auto grab = [&](unsigned need) -> unsigned {
+    unsigned incl = need;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      unsigned v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if ((int)lane >= o) incl += v;
+    }
+    __syncthreads();  // s_warp / s_base are reused
+    if (lane == 31) s_warp[threadIdx.x >> 5] = incl;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned acc = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); w++) {
+        unsigned v = s_warp[w];
+        s_warp[w] = acc;
+        acc += v;
+      }
+      s_base = acc ? atomicAdd(&X.ctl[11], acc) : 0u;
+    }
+    __syncthreads();
+    return s_base + s_warp[threadIdx.x >> 5] + incl - need;
+  };
+
+  // round 0's keys
+  {
+    unsigned nx = grab((unsigned)X.slots);
+#pragma unroll
+    for (int j = 0; j < KB; j++) {
+      if (j < X.slots && (int64_t)nx < n) {
+        idx[j] = nx;
+        pend[j] = true;
+        KeyInfo ki = key_info(P, ld_stream_u64(keys + nx, pol_stream));
+        b1[j] = (uint32_t)ki.b1;
+        b2[j] = (uint32_t)ki.b2;
+        tg[j] = (uint32_t)ki.tag;
+      }
+      nx += j < X.slots ? 1u : 0u;
+    }
+  }
+
   for (;;) {
-    // ---- reserve round r: fill free slots from the frontier, bid ---------
+    // ---- bid for round r ----------------------------------------------------
     {
       uint32_t *R = (r & 1) ? X.res2 : X.res;
-      unsigned need = 0;
-#pragma unroll
-      for (int j = 0; j < KB; j++) need += (j < X.slots && !pend[j]) ? 1u : 0u;
-      // one frontier atomic per CTA (a single L2 address takes every grab)
-      unsigned incl = need;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        unsigned v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-        if ((int)lane >= o) incl += v;
-      }
-      if (lane == 31) s_warp[threadIdx.x >> 5] = incl;
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        unsigned acc = 0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); w++) {
-          unsigned v = s_warp[w];
-          s_warp[w] = acc;
-          acc += v;
-        }
-        s_base = acc ? atomicAdd(&X.ctl[11], acc) : 0u;
-      }
-      __syncthreads();
-      unsigned nx = s_base + s_warp[threadIdx.x >> 5] + incl - need;  // this lane's first new index
-#pragma unroll
-      for (int j = 0; j < KB; j++) {
-        if (j >= X.slots || pend[j]) continue;
-        if ((int64_t)nx < n) {
-          idx[j] = nx;
-          pend[j] = true;
-          KeyInfo ki = key_info(P, ld_stream_u64(keys + nx, pol_stream));
-          b1[j] = (uint32_t)ki.b1;
-          b2[j] = (uint32_t)ki.b2;
-          tg[j] = (uint32_t)ki.tag;
-        }
-        nx++;
-      }
       unsigned mine = 0;
 #pragma unroll
       for (int j = 0; j < KB; j++) {
@@ -937,10 +944,8 @@ __global__ void __launch_bounds__(256, 4)
     }
     grid.sync();
     const unsigned total = __ldcg(&X.ctl[8 + r % 3]);
-    if (blockIdx.x == 0 && threadIdx.x == 0) X.ctl[8 + (r + 2) % 3] = 0;
-    if (total == 0) break;
 
-    // ---- commit round r ----------------------------------------------------
+    // ---- commit round r, refill from the frontier for round r+1 -------------
     {
       uint32_t *R = (r & 1) ? X.res2 : X.res;
       bool hold[KB];
@@ -961,6 +966,31 @@ __global__ void __launch_bounds__(256, 4)
           hold[j] = pend[j] && ld_cg_u32(&R[b1[j] >> rs], pol_keep) == idx[j] &&
                     ld_cg_u32(&R[b2[j] >> rs], pol_keep) == idx[j];
           if (hold[j]) load16<true>(blocks + (uint64_t)b1[j] * 16, rb[j]);
+        }
+      }
+      // (no thread has a pending key when total == 0, so nothing was loaded)
+      if (total == 0) break;
+      if (blockIdx.x == 0 && threadIdx.x == 0) X.ctl[8 + (r + 2) % 3] = 0;
+      // Refill early: the slots of this round's holders and the empty slots
+      // take the next input indices now, so the frontier atomic and the key
+      // loads overlap the block loads and commits below.
+      bool refill[KB];
+      unsigned need = 0;
+#pragma unroll
+      for (int j = 0; j < KB; j++) {
+        refill[j] = j < X.slots && (!pend[j] || hold[j]);
+        need += refill[j] ? 1u : 0u;
+      }
+      unsigned nx = grab(need);
+      uint64_t nk[KB];
+      {
+        unsigned k = 0;
+#pragma unroll
+        for (int j = 0; j < KB; j++) {
+          nk[j] = 0;
+          if (!refill[j]) continue;
+          if ((int64_t)(nx + k) < n) nk[j] = ld_stream_u64(keys + nx + k, pol_stream);
+          k++;
         }
       }
 #pragma unroll
@@ -1000,6 +1030,21 @@ __global__ void __launch_bounds__(256, 4)
         st_u32(&R[g1], kNoRes, pol_keep);
         st_u32(&R[g2], kNoRes, pol_keep);
         pend[j] = false;
+      }
+      // install the new keys (slot order = input order within this lane)
+      unsigned k = 0;
+#pragma unroll
+      for (int j = 0; j < KB; j++) {
+        if (!refill[j]) continue;
+        unsigned i = nx + k;
+        k++;
+        if ((int64_t)i >= n) continue;
+        idx[j] = i;
+        pend[j] = true;
+        KeyInfo ki = key_info(P, nk[j]);
+        b1[j] = (uint32_t)ki.b1;
+        b2[j] = (uint32_t)ki.b2;
+        tg[j] = (uint32_t)ki.tag;
       }
     }
     r++;
