@@ -1274,12 +1274,15 @@ static int launch_ordered(const TcfDev &P, const uint64_t *keys, const uint64_t 
     if (X.ctas_per_sm > 0 && X.ctas_per_sm < per_sm) per_sm = X.ctas_per_sm;
     int grid = per_sm * num_sms();
     int64_t thr = (int64_t)grid * 256;
-    // one-barrier kernel when the window gives every thread a key (its
-    // window is about grid * 256 * slots); small windows keep the carry-list
-    // kernel, whose window is exact
+    // one-barrier kernel when the window gives at least every fourth thread
+    // a key (its window is grid * 256 * slots, slots = the nearest whole
+    // number, >= 1); smaller windows keep the carry-list kernel, whose window
+    // is exact (measured, profiles/r1g_ord_tune_small.jsonl: 2^22 slots,
+    // window 65 K for 76 K threads, 3.5 vs 2.7 G inserts/s; 2^20, 16 K for
+    // 38 K, 1.1-1.3 vs 0.9-1.0)
     // (its 32-bit frontier may overshoot n by a round's grabs: keep clear of 2^32)
-    if (X.res2 && X.window >= thr && n < (int64_t)0xFFFFFFFFLL - 4 * thr * kOrdKB<1>) {
-      int slots = (int)((X.window + thr - 1) / thr);
+    if (X.res2 && 4 * X.window >= thr && n < (int64_t)0xFFFFFFFFLL - 4 * thr * kOrdKB<1>) {
+      int slots = (int)((X.window + thr / 2) / thr);  // (clamped to >= 1 below)
       X.slots = slots < 1 ? 1 : (slots > kOrdKB<1> ? kOrdKB<1> : slots);
       void *args[] = {(void *)&P, (void *)&keys, (void *)&values, (void *)&n, (void *)&out, (void *)&counters,
                       (void *)&X};

@@ -60,8 +60,8 @@ def main():
                 for kv in cfg.split(","):
                     k, v = kv.split("=")
                     env[{"W": "FK_ORD_WINDOW", "RS": "FK_ORD_RES_SHIFT", "CTAS": "FK_ORD_CTAS_PER_SM",
-                         "H": "FK_ORD_HINTS", "OB": "FK_ORD_ONEBAR"}[k]] = v
-            for k in ("FK_ORD_WINDOW", "FK_ORD_RES_SHIFT", "FK_ORD_CTAS_PER_SM", "FK_ORD_HINTS", "FK_ORD_ONEBAR"):
+                         "H": "FK_ORD_HINTS", "OB": "FK_ORD_ONEBAR", "KB3": "FK_ORD_KB3"}[k]] = v
+            for k in ("FK_ORD_WINDOW", "FK_ORD_RES_SHIFT", "FK_ORD_CTAS_PER_SM", "FK_ORD_HINTS", "FK_ORD_ONEBAR", "FK_ORD_KB3"):
                 os.environ.pop(k, None)
             os.environ.update(env)
             rs = int(env.get("FK_ORD_RES_SHIFT", default_rs(nb)))
