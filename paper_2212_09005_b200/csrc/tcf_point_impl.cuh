@@ -946,39 +946,41 @@ __global__ void __launch_bounds__(256, 4)
     const unsigned total = __ldcg(&X.ctl[8 + r % 3]);
 
     // ---- commit round r, refill from the frontier for round r+1 -------------
+    // A key holding its b1 word commits when it also holds its b2 word, or
+    // when its b1 block alone decides the op (insert: b1 below the cut line;
+    // delete: the tag is live in b1) -- the op then touches b1 only, and no
+    // earlier pending key touches b1 (it would hold a smaller bid there).
     {
       uint32_t *R = (r & 1) ? X.res2 : X.res;
-      bool hold[KB];
+      bool hold[KB], hold2[KB];
       uint32_t rb[KB][8];
-      if (X.spec) {
-        // speculative: the b1 block load overlaps the reservation-word
-        // loads (losers, ~13 %, fetch their block for nothing)
 #pragma unroll
-        for (int j = 0; j < KB; j++)
-          if (pend[j]) load16<true>(blocks + (uint64_t)b1[j] * 16, rb[j]);
-#pragma unroll
-        for (int j = 0; j < KB; j++)
-          hold[j] = pend[j] && ld_cg_u32(&R[b1[j] >> rs], pol_keep) == idx[j] &&
-                    ld_cg_u32(&R[b2[j] >> rs], pol_keep) == idx[j];
-      } else {
-#pragma unroll
-        for (int j = 0; j < KB; j++) {
-          hold[j] = pend[j] && ld_cg_u32(&R[b1[j] >> rs], pol_keep) == idx[j] &&
-                    ld_cg_u32(&R[b2[j] >> rs], pol_keep) == idx[j];
-          if (hold[j]) load16<true>(blocks + (uint64_t)b1[j] * 16, rb[j]);
-        }
+      for (int j = 0; j < KB; j++) {
+        hold[j] = pend[j] && ld_cg_u32(&R[b1[j] >> rs], pol_keep) == idx[j];
+        hold2[j] = pend[j] && ld_cg_u32(&R[b2[j] >> rs], pol_keep) == idx[j];
+        if (hold[j]) load16<true>(blocks + (uint64_t)b1[j] * 16, rb[j]);
       }
       // (no thread has a pending key when total == 0, so nothing was loaded)
       if (total == 0) break;
       if (blockIdx.x == 0 && threadIdx.x == 0) X.ctl[8 + (r + 2) % 3] = 0;
-      // Refill early: the slots of this round's holders and the empty slots
-      // take the next input indices now, so the frontier atomic and the key
-      // loads overlap the block loads and commits below.
+      bool go[KB];
+#pragma unroll
+      for (int j = 0; j < KB; j++) {
+        bool b1_decides = false;
+        if (hold[j] && !hold2[j]) {
+          if (OP == 0) b1_decides = __popc(live16(rb[j])) < P.cut;
+          else b1_decides = match16(rb[j], tg[j], (uint32_t)(P.fmask & 0xFFFFu)) != 0;
+        }
+        go[j] = hold[j] && (hold2[j] || b1_decides);
+      }
+      // Refill early: the slots of this round's committers and the empty
+      // slots take the next input indices now, so the frontier atomic and the
+      // key loads overlap the commits below.
       bool refill[KB];
       unsigned need = 0;
 #pragma unroll
       for (int j = 0; j < KB; j++) {
-        refill[j] = j < X.slots && (!pend[j] || hold[j]);
+        refill[j] = j < X.slots && (!pend[j] || go[j]);
         need += refill[j] ? 1u : 0u;
       }
       unsigned nx = grab(need);
@@ -997,7 +999,7 @@ __global__ void __launch_bounds__(256, 4)
       for (int j = 0; j < KB; j++) {
         if (!pend[j]) continue;
         uint32_t g1 = b1[j] >> rs, g2 = b2[j] >> rs;
-        if (!hold[j]) {  // lost: retract our own bids so the array is clean
+        if (!go[j]) {  // lost: retract our own bids so the array is clean
           atomicCAS(&R[g1], idx[j], kNoRes);
           if (g2 != g1) atomicCAS(&R[g2], idx[j], kNoRes);
           losses++;
@@ -1027,8 +1029,13 @@ __global__ void __launch_bounds__(256, 4)
             X.defer_pend[slot] = 1;
           }
         }
+        // release the b1 word; the b2 word only if we hold it, else retract
+        // our bid there (an earlier key holds it)
         st_u32(&R[g1], kNoRes, pol_keep);
-        st_u32(&R[g2], kNoRes, pol_keep);
+        if (g2 != g1) {
+          if (hold2[j]) st_u32(&R[g2], kNoRes, pol_keep);
+          else atomicCAS(&R[g2], idx[j], kNoRes);
+        }
         pend[j] = false;
       }
       // install the new keys (slot order = input order within this lane)
