@@ -486,6 +486,17 @@ __device__ __forceinline__ int tile_first_free(const Tile<G> &t, const Chunk<S, 
   return 1;
 }
 
+// True when the b1 block alone decides a key's op (insert: b1 below the cut
+// line; delete: the tag is live in b1): the op then touches b1 only, so a key
+// holding its b1 reservation may commit without its b2 one -- no earlier
+// pending key touches b1 (it would hold a smaller bid there).  Tile-collective.
+template <typename S, int G, int BF, int OP>
+__device__ __forceinline__ bool b1_decides(const TcfDev &P, const Tile<G> &t, const Chunk<S, G, BF> &c1,
+                                           uint64_t tag) {
+  if (OP == 0) return t.sum(c1.used()) < P.cut;
+  return t.ballot(c1.first_match(0, tag, P.fmask) >= 0) != 0;
+}
+
 // The sequential insert policy (pk:126-148) on exclusively reserved blocks.
 // Returns the placement code, or 4 = "both blocks full, defer to backing".
 template <typename S, int G, int BF>
@@ -726,12 +737,14 @@ __global__ void __launch_bounds__(256, 4)
     // ---- commit ---------------------------------------------------------
     if (blockIdx.x == 0 && threadIdx.x == 0) X.ctl[cur] = 0;  // list `cur` is consumed this round
     {
+      bool hold2[KB];
 #pragma unroll
-      for (int j = 0; j < KB; j++)
+      for (int j = 0; j < KB; j++) {
         hold[j] = ok[j] && (X.hints ? ld_cg_u32(&X.res[b1[j] >> X.res_shift], pol_keep)
-                                    : __ldcg(&X.res[b1[j] >> X.res_shift])) == idx[j] &&
-                  (X.hints ? ld_cg_u32(&X.res[b2[j] >> X.res_shift], pol_keep)
-                           : __ldcg(&X.res[b2[j] >> X.res_shift])) == idx[j];
+                                    : __ldcg(&X.res[b1[j] >> X.res_shift])) == idx[j];
+        hold2[j] = ok[j] && (X.hints ? ld_cg_u32(&X.res[b2[j] >> X.res_shift], pol_keep)
+                                     : __ldcg(&X.res[b2[j] >> X.res_shift])) == idx[j];
+      }
       constexpr bool fast = kFast16<S, G, BF>;
       constexpr int KC = fast ? 1 : KB;      // generic path: one Chunk per key
       constexpr int KR = fast ? KB : 1;      // fast path: 8 registers per key
@@ -744,6 +757,18 @@ __global__ void __launch_bounds__(256, 4)
         if constexpr (fast) load16<true>(reinterpret_cast<uint16_t *>(blocks) + (uint64_t)b1[j] * 16, r1[j]);
         else c1[j].template load<true>(blocks + (uint64_t)b1[j] * P.B, P.B, t.lane);
       }
+      // commit with both words, or with the b1 word when b1 decides the op
+#pragma unroll
+      for (int j = 0; j < KB; j++) {
+        if (!hold[j] || hold2[j]) continue;
+        bool d;
+        if constexpr (fast) d = OP == 0 ? __popc(live16(r1[j])) < P.cut
+                                        : match16(r1[j], (uint32_t)tg[j], (uint32_t)(P.fmask & 0xFFFFu)) != 0;
+        else d = b1_decides<S, G, BF, OP>(P, t, c1[j], tg[j]);
+        hold[j] = d;
+        hold2[j] = false;  // (not ours: leave the b2 word to its holder)
+      }
+
       // carry the losers: one warp-aggregated atomicAdd (every lane joins)
       {
         unsigned mine = 0;
@@ -800,10 +825,10 @@ __global__ void __launch_bounds__(256, 4)
           // only the holder writes these words now
           if (X.hints) {
             st_u32(&X.res[b1[j] >> X.res_shift], kNoRes, pol_keep);
-            st_u32(&X.res[b2[j] >> X.res_shift], kNoRes, pol_keep);
+            if (hold2[j]) st_u32(&X.res[b2[j] >> X.res_shift], kNoRes, pol_keep);
           } else {
             X.res[b1[j] >> X.res_shift] = kNoRes;
-            X.res[b2[j] >> X.res_shift] = kNoRes;
+            if (hold2[j]) X.res[b2[j] >> X.res_shift] = kNoRes;
           }
         }
       }
@@ -1151,7 +1176,7 @@ __global__ void __launch_bounds__(256, 4)
       if (!__any_sync(0xFFFFFFFFu, base < total)) break;
       uint32_t idx[KB], b1[KB], b2[KB];
       uint64_t word[KB];
-      bool ok[KB], hold[KB];
+      bool ok[KB], hold[KB], hold2[KB];
 #pragma unroll
       for (int j = 0; j < KB; j++) {
         int64_t e = base + (int64_t)j * tiles;
@@ -1167,16 +1192,24 @@ __global__ void __launch_bounds__(256, 4)
         word[j] = OP == 0 ? ((P.f >= 64 ? 0 : ((values ? values[idx[j]] : 0) << P.f)) | ki.tag) : ki.tag;
       }
 #pragma unroll
-      for (int j = 0; j < KB; j++)
+      for (int j = 0; j < KB; j++) {
         hold[j] = ok[j] && (X.hints ? ld_cg_u32(&X.res[b1[j] >> X.res_shift], pol_keep)
-                                    : __ldcg(&X.res[b1[j] >> X.res_shift])) == idx[j] &&
-                  (X.hints ? ld_cg_u32(&X.res[b2[j] >> X.res_shift], pol_keep)
-                           : __ldcg(&X.res[b2[j] >> X.res_shift])) == idx[j];
+                                    : __ldcg(&X.res[b1[j] >> X.res_shift])) == idx[j];
+        hold2[j] = ok[j] && (X.hints ? ld_cg_u32(&X.res[b2[j] >> X.res_shift], pol_keep)
+                                     : __ldcg(&X.res[b2[j] >> X.res_shift])) == idx[j];
+      }
       Chunk<S, G, BF> c1[KB];
       S *blocks = reinterpret_cast<S *>(P.blocks);
 #pragma unroll
       for (int j = 0; j < KB; j++)
         if (hold[j]) c1[j].template load<true>(blocks + (uint64_t)b1[j] * P.B, P.B, t.lane);
+      // commit with both words, or with the b1 word when b1 decides the op
+      // (the tag bits of word[] are the tag for either op)
+#pragma unroll
+      for (int j = 0; j < KB; j++) {
+        if (!hold[j] || hold2[j]) continue;
+        hold[j] = b1_decides<S, G, BF, OP>(P, t, c1[j], word[j] & P.fmask);
+      }
       // carry the losers: one warp-aggregated atomicAdd per pass
       {
         unsigned mine = 0;
@@ -1228,10 +1261,10 @@ __global__ void __launch_bounds__(256, 4)
           // only the holder writes these words now
           if (X.hints) {
             st_u32(&X.res[b1[j] >> X.res_shift], kNoRes, pol_keep);
-            st_u32(&X.res[b2[j] >> X.res_shift], kNoRes, pol_keep);
+            if (hold2[j]) st_u32(&X.res[b2[j] >> X.res_shift], kNoRes, pol_keep);
           } else {
             X.res[b1[j] >> X.res_shift] = kNoRes;
-            X.res[b2[j] >> X.res_shift] = kNoRes;
+            if (hold2[j]) X.res[b2[j] >> X.res_shift] = kNoRes;
           }
         }
       }
