@@ -488,7 +488,8 @@ __device__ __forceinline__ int tile_first_free(const Tile<G> &t, const Chunk<S, 
 
 // True when the b1 block alone decides a key's op (insert: b1 below the cut
 // line; delete: the tag is live in b1): the op then touches b1 only, so a key
-// holding its b1 reservation may commit without its b2 one -- no earlier
+// holding its b1 reservation may commit without its b2 one (pk:132-134,
+// pk:213-218) -- no earlier
 // pending key touches b1 (it would hold a smaller bid there).  Tile-collective.
 template <typename S, int G, int BF, int OP>
 __device__ __forceinline__ bool b1_decides(const TcfDev &P, const Tile<G> &t, const Chunk<S, G, BF> &c1,
