@@ -470,7 +470,6 @@ struct OrdScratch {
   int prefetch;         // 1: the reserve pass prefetches each key's b1 block into L2
   uint32_t *res2;       // one-barrier kernel: reservation words of odd rounds
   int slots;            // one-barrier kernel: keys held per thread (<= KB)
-  int spec;             // one-barrier kernel: load b1 blocks before the reservation check
 };
 
 // CTA-wide OR of a predicate (all threads of the CTA must call).
