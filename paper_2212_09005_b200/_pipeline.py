@@ -35,11 +35,17 @@ class HostPipeline:
 
     def run(self, inputs, out_dtypes, launch):
         """inputs: CPU tensors of equal length (pinned for asynchronous H2D);
-        launch(dev_inputs, dev_outputs) enqueues the op on the current stream.
+        launch(dev_inputs, dev_outputs) enqueues the op on the current stream
+        (a torch.bool output is a uint8 0/1 buffer on the device).
         Returns pinned CPU output tensors after everything has landed."""
         torch = self.torch
         n = inputs[0].numel()
+        # bool results are produced as 0/1 bytes on the device and land in a
+        # bool host tensor through its uint8 view (a plain copy, no host-side
+        # conversion pass over the batch)
         outs = [torch.empty(n, dtype=dt, pin_memory=True) for dt in out_dtypes]
+        outs_raw = [o.view(torch.uint8) if o.dtype == torch.bool else o for o in outs]
+        out_dtypes = [torch.uint8 if dt == torch.bool else dt for dt in out_dtypes]
         main = torch.cuda.current_stream(self.device)
         self.h2d.wait_stream(main)  # the table state the op starts from
         ev_in = [torch.cuda.Event() for _ in range(2)]
@@ -63,7 +69,7 @@ class HostPipeline:
             ev_k[b].record(main)
             self.d2h.wait_event(ev_k[b])
             with torch.cuda.stream(self.d2h):
-                for o, d in zip(outs, dout):
+                for o, d in zip(outs_raw, dout):
                     o[lo:lo + m].copy_(d[:m], non_blocking=True)
             ev_out[b].record(self.d2h)
             used[b] = True

@@ -282,9 +282,11 @@ class Gqf:
         return self._flags(found, kind)
 
     def _flags(self, found, kind):
+        # (0/1 bytes -> bool on the device: no host-side pass over the batch)
+        found = found.bool()
         if kind == "numpy":
-            return found.cpu().numpy().astype(bool)
-        return ret(self._torch, found, kind).bool()
+            return found.cpu().numpy()
+        return ret(self._torch, found, kind)
 
     # -- bulk API ---------------------------------------------------------------------------
     def bulk_insert(self, keys, counts=None, workers=4):

@@ -222,8 +222,6 @@ class Tcf:
             out, = self._pipe.run([hk], [out_dtype], launch)
             if op != "query":
                 self._t.after_device_write()
-        if op != "insert":
-            out = out.bool()
         return out if kind == "host" else out.numpy()
 
     def _ret(self, t, kind):
@@ -310,7 +308,7 @@ class Tcf:
 
     def query_many(self, keys):
         if self._pipe_wants(keys):
-            return self._pipelined(keys, "query", self._torch.uint8)
+            return self._pipelined(keys, "query", self._torch.bool)
         return self._query(keys, False)[0]
 
     def query_values_many(self, keys):
@@ -332,8 +330,8 @@ class Tcf:
         if on_dev == "cuda":
             return found.bool(), (vals if want_values else None)
         if on_dev == "host":
-            return self._ret(found, "host").bool(), (self._ret(vals, "host") if want_values else None)
-        return found.cpu().numpy().astype(bool), (vals.cpu().numpy().view(np.uint64) if want_values else None)
+            return self._ret(found.bool(), "host"), (self._ret(vals, "host") if want_values else None)
+        return found.bool().cpu().numpy(), (vals.cpu().numpy().view(np.uint64) if want_values else None)
 
     def delete(self, key):
         return bool(self.delete_many([key])[0])
@@ -341,7 +339,7 @@ class Tcf:
     def delete_many(self, keys):
         torch = self._torch
         if self._pipe_wants(keys):
-            return self._pipelined(keys, "delete", torch.uint8)
+            return self._pipelined(keys, "delete", torch.bool)
         k, on_dev = self._keys_in(keys)
         n = k.numel()
         removed = torch.empty(n, dtype=torch.uint8, device=self._device)
@@ -359,8 +357,8 @@ class Tcf:
         if on_dev == "cuda":
             return removed.bool()
         if on_dev == "host":
-            return self._ret(removed, "host").bool()
-        return removed.cpu().numpy().astype(bool)
+            return self._ret(removed.bool(), "host")
+        return removed.bool().cpu().numpy()
 
     # -- inspection (quiescent; host mirrors) ------------------------------------
     def items(self):

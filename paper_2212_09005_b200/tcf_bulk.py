@@ -236,8 +236,8 @@ class BulkTcf:
         if kind == "cuda":
             return found.bool()
         if kind == "host":
-            return found.cpu().bool()
-        return found.cpu().numpy().astype(bool)
+            return found.bool().cpu()
+        return found.bool().cpu().numpy()
 
     def delete_batch(self, keys, workers=1):
         """Remove one stored copy per key; per-key success flags
@@ -257,8 +257,8 @@ class BulkTcf:
         if kind == "cuda":
             return removed.bool()
         if kind == "host":
-            return removed.cpu().bool()
-        return removed.cpu().numpy().astype(bool)
+            return removed.bool().cpu()
+        return removed.bool().cpu().numpy()
 
     # -- inspection (quiescent; host mirrors) -----------------------------------
     def occupancy(self, block_index):
