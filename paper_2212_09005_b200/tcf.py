@@ -112,6 +112,10 @@ class TcfParams:
         return g
 
 
+# ordered kernels index their input with 32 bits (fk_tcf_insert rejects
+# n > 0xFFFFFFF0): longer ordered batches run as consecutive launches
+_ORD_MAX_KEYS = 1 << 31
+
 _MODES = {"ordered": _lib.FK_ORDERED, "concurrent": _lib.FK_CONCURRENT}
 
 
@@ -288,14 +292,20 @@ class Tcf:
         codes = torch.empty(n, dtype=torch.uint8, device=self._device)
         if n:
             mode = _MODES[self.mode]
+            step = _ORD_MAX_KEYS if self.mode == "ordered" else n
             with self._op_lock:
                 self._t.before_device_op()
-                ws, wsb = self._workspace(n, mode)
-                rc = self._lib.fk_tcf_insert(
-                    ctypes_byref(self._geom), self._t.ptr("blocks"), self._t.ptr("backing"),
-                    _lib.dptr(k), 0, _lib.dptr(v), n, _lib.dptr(codes), _lib.dptr(self._counters_dev),
-                    mode, _lib.dptr(ws), wsb, _lib.stream_ptr(torch))
-                _lib.check(rc, "tcf insert")
+                ws, wsb = self._workspace(min(n, step), mode)
+                # ordered batches past the kernels' 32-bit input index run as
+                # consecutive launches (in order: the same sequential result)
+                for lo in range(0, n, step):
+                    m = min(step, n - lo)
+                    rc = self._lib.fk_tcf_insert(
+                        ctypes_byref(self._geom), self._t.ptr("blocks"), self._t.ptr("backing"),
+                        _lib.dptr(k[lo:lo + m]), 0, _lib.dptr(v[lo:lo + m] if v is not None else None), m,
+                        _lib.dptr(codes[lo:lo + m]), _lib.dptr(self._counters_dev), mode, _lib.dptr(ws), wsb,
+                        _lib.stream_ptr(torch))
+                    _lib.check(rc, "tcf insert")
                 self._t.after_device_write()
         return self._ret(codes, on_dev)
 
@@ -345,14 +355,17 @@ class Tcf:
         removed = torch.empty(n, dtype=torch.uint8, device=self._device)
         if n:
             mode = _MODES[self.mode]
+            step = _ORD_MAX_KEYS if self.mode == "ordered" else n
             with self._op_lock:
                 self._t.before_device_op()
-                ws, wsb = self._workspace(n, mode)
-                rc = self._lib.fk_tcf_delete(
-                    ctypes_byref(self._geom), self._t.ptr("blocks"), self._t.ptr("backing"),
-                    _lib.dptr(k), 0, n, _lib.dptr(removed), _lib.dptr(self._counters_dev), mode,
-                    _lib.dptr(ws), wsb, _lib.stream_ptr(torch))
-                _lib.check(rc, "tcf delete")
+                ws, wsb = self._workspace(min(n, step), mode)
+                for lo in range(0, n, step):
+                    m = min(step, n - lo)
+                    rc = self._lib.fk_tcf_delete(
+                        ctypes_byref(self._geom), self._t.ptr("blocks"), self._t.ptr("backing"),
+                        _lib.dptr(k[lo:lo + m]), 0, m, _lib.dptr(removed[lo:lo + m]),
+                        _lib.dptr(self._counters_dev), mode, _lib.dptr(ws), wsb, _lib.stream_ptr(torch))
+                    _lib.check(rc, "tcf delete")
                 self._t.after_device_write()
         if on_dev == "cuda":
             return removed.bool()

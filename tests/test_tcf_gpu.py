@@ -328,3 +328,26 @@ def test_device_census_validate_and_load_factor(kw):
         if backing[j] > 1:
             with pytest.raises(ValidationError):
                 f.validate()
+
+
+def test_ordered_batches_past_32bit_index_chunk_exactly(oracle, monkeypatch):
+    """Ordered batches longer than the kernels' 32-bit input index run as
+    consecutive launches; shrink the limit and check the result is still the
+    sequential reference (codes, values, image, delete flags, counters)."""
+    import torch
+    from paper_2212_09005_b200 import Tcf, tcf as tcf_mod
+    monkeypatch.setattr(tcf_mod, "_ORD_MAX_KEYS", 4093)
+    f = Tcf(num_blocks=2 ** 10, tag_bits=16, slot_bits=32)
+    o = _oracle(f, oracle)
+    keys = counter_keys(77, int(0.95 * 2 ** 14))
+    vals = (keys % 251).astype(np.uint64)
+    kd = torch.from_numpy(keys.view(np.int64)).cuda()
+    vd = torch.from_numpy(vals.view(np.int64)).cuda()
+    codes = f.insert_many(kd, vd).cpu().numpy()
+    assert np.array_equal(codes, o.insert_many(keys, vals))
+    _same_tables(f, o)
+    d = np.concatenate([keys[::3], counter_keys(78, 3000)])
+    got = f.delete_many(torch.from_numpy(d.view(np.int64)).cuda()).cpu().numpy()
+    assert np.array_equal(got, o.delete_many(d))
+    _same_tables(f, o)
+    assert f.counters == o.counters
