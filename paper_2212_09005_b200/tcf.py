@@ -328,7 +328,7 @@ class Tcf:
         torch = self._torch
         k, on_dev = self._keys_in(keys)
         n = k.numel()
-        found = torch.empty(n, dtype=torch.uint8, device=self._device)
+        found = torch.empty(n, dtype=torch.bool, device=self._device)  # the kernel writes 0/1 bytes
         vals = torch.empty(n if want_values else 0, dtype=torch.int64, device=self._device)
         if n:
             with self._op_lock:
@@ -338,10 +338,10 @@ class Tcf:
                     _lib.dptr(k), 0, n, _lib.dptr(found), _lib.dptr(vals), _lib.stream_ptr(torch))
                 _lib.check(rc, "tcf query")
         if on_dev == "cuda":
-            return found.bool(), (vals if want_values else None)
+            return found, (vals if want_values else None)
         if on_dev == "host":
-            return self._ret(found.bool(), "host"), (self._ret(vals, "host") if want_values else None)
-        return found.bool().cpu().numpy(), (vals.cpu().numpy().view(np.uint64) if want_values else None)
+            return self._ret(found, "host"), (self._ret(vals, "host") if want_values else None)
+        return found.cpu().numpy(), (vals.cpu().numpy().view(np.uint64) if want_values else None)
 
     def delete(self, key):
         return bool(self.delete_many([key])[0])
@@ -352,7 +352,7 @@ class Tcf:
             return self._pipelined(keys, "delete", torch.bool)
         k, on_dev = self._keys_in(keys)
         n = k.numel()
-        removed = torch.empty(n, dtype=torch.uint8, device=self._device)
+        removed = torch.empty(n, dtype=torch.bool, device=self._device)  # the kernels write 0/1 bytes
         if n:
             mode = _MODES[self.mode]
             step = _ORD_MAX_KEYS if self.mode == "ordered" else n
@@ -368,10 +368,10 @@ class Tcf:
                     _lib.check(rc, "tcf delete")
                 self._t.after_device_write()
         if on_dev == "cuda":
-            return removed.bool()
+            return removed
         if on_dev == "host":
-            return self._ret(removed.bool(), "host")
-        return removed.bool().cpu().numpy()
+            return self._ret(removed, "host")
+        return removed.cpu().numpy()
 
     # -- inspection (quiescent; host mirrors) ------------------------------------
     def items(self):
