@@ -218,7 +218,8 @@ class Gqf:
         k, kind = keys_in(torch, keys, self._device)
         n = k.numel()
         d = self._deltas(counts, n, kind)
-        found = torch.zeros(n, dtype=torch.uint8, device=self._device) if op == _lib.FK_GQF_DELETE else None
+        # (0/1 bytes written by the kernels)
+        found = torch.zeros(n, dtype=torch.bool, device=self._device) if op == _lib.FK_GQF_DELETE else None
         res = _lib.GqfResult()
         if n:
             with self._op_lock:
@@ -282,8 +283,6 @@ class Gqf:
         return self._flags(found, kind)
 
     def _flags(self, found, kind):
-        # (0/1 bytes -> bool on the device: no host-side pass over the batch)
-        found = found.bool()
         if kind == "numpy":
             return found.cpu().numpy()
         return ret(self._torch, found, kind)

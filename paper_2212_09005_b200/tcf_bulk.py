@@ -226,7 +226,7 @@ class BulkTcf:
         torch = self._torch
         k, kind = _keys_in(torch, keys, self._device)
         n = k.numel()
-        found = torch.empty(n, dtype=torch.uint8, device=self._device)
+        found = torch.empty(n, dtype=torch.bool, device=self._device)  # the kernel writes 0/1 bytes
         if n:
             with self._op_lock:
                 self._t.before_device_op()
@@ -234,10 +234,10 @@ class BulkTcf:
                 _lib.check(self._lib.fk_btcf_query(ctypes.byref(self._geom), b, f, bk, _lib.dptr(k), 0, n,
                                                    _lib.dptr(found), _lib.stream_ptr(torch)), "btcf query")
         if kind == "cuda":
-            return found.bool()
+            return found
         if kind == "host":
-            return found.bool().cpu()
-        return found.bool().cpu().numpy()
+            return found.cpu()
+        return found.cpu().numpy()
 
     def delete_batch(self, keys, workers=1):
         """Remove one stored copy per key; per-key success flags
@@ -245,7 +245,7 @@ class BulkTcf:
         torch = self._torch
         k, kind = _keys_in(torch, keys, self._device)
         n = k.numel()
-        removed = torch.zeros(n, dtype=torch.uint8, device=self._device)
+        removed = torch.zeros(n, dtype=torch.bool, device=self._device)  # the kernels write 0/1 bytes
         if n:
             with self._op_lock:
                 self._t.before_device_op()
@@ -255,10 +255,10 @@ class BulkTcf:
                                                     _lib.stream_ptr(torch)), "btcf delete")
                 self._t.after_device_write()
         if kind == "cuda":
-            return removed.bool()
+            return removed
         if kind == "host":
-            return removed.bool().cpu()
-        return removed.bool().cpu().numpy()
+            return removed.cpu()
+        return removed.cpu().numpy()
 
     # -- inspection (quiescent; host mirrors) -----------------------------------
     def occupancy(self, block_index):
