@@ -381,19 +381,27 @@ __global__ void __launch_bounds__(32) k_btcf_route_seq(const uint32_t *__restric
     a0 = a1; b0 = b1; l0a = l1a; l0b = l1b;
     a1 = a2; b1 = b2; l1a = l2a; l1b = l2b;
   };
-  for (int64_t base = 0; base < m; base += 32) {
+  // one chunk of 32 leftovers: j + 2 < 32 come from the chunk's registers
+  // (xa, xb), the last two from the next chunk's (ya, yb)
+  auto chunk = [&](int64_t base, uint32_t xa, uint32_t xb, uint32_t ya, uint32_t yb) {
     const int cnt = m - base < 32 ? (int)(m - base) : 32;
-    // leftovers j + 2 < 32 come from this chunk's registers, the last two
-    // from the next chunk's (loaded a full chunk earlier)
     for (int j = 0; j < 30 && j < cnt; j++)
-      step(j, __shfl_sync(0xFFFFFFFFu, ca, j + 2), __shfl_sync(0xFFFFFFFFu, cb, j + 2));
+      step(j, __shfl_sync(0xFFFFFFFFu, xa, j + 2), __shfl_sync(0xFFFFFFFFu, xb, j + 2));
     for (int j = 30; j < cnt; j++)
-      step(j, __shfl_sync(0xFFFFFFFFu, na, j - 30), __shfl_sync(0xFFFFFFFFu, nb2, j - 30));
+      step(j, __shfl_sync(0xFFFFFFFFu, ya, j - 30), __shfl_sync(0xFFFFFFFFu, yb, j - 30));
     if (base + lane < m) dest[base + lane] = mine;
-    ca = na;
-    cb = nb2;
-    na = base + 64 + lane < m ? lb1[base + 64 + lane] : 0;
-    nb2 = base + 64 + lane < m ? lb2[base + 64 + lane] : 0;
+  };
+  // Two chunks per trip with the register sets swapping roles: every
+  // leftover load lands in a register first read a whole chunk later (a
+  // rotating copy at the loop head would wait for the load just issued).
+  for (int64_t base = 0; base < m; base += 64) {
+    chunk(base, ca, cb, na, nb2);
+    ca = base + 64 + lane < m ? lb1[base + 64 + lane] : 0;
+    cb = base + 64 + lane < m ? lb2[base + 64 + lane] : 0;
+    if (base + 32 >= m) break;
+    chunk(base + 32, na, nb2, ca, cb);
+    na = base + 96 + lane < m ? lb1[base + 96 + lane] : 0;
+    nb2 = base + 96 + lane < m ? lb2[base + 96 + lane] : 0;
   }
 }
 
