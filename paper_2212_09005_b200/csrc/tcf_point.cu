@@ -129,7 +129,7 @@ static int prep_ordered(const fk_tcf_geom *g, int64_t n, void *ws, size_t ws_byt
   X->hints = ord_hints();
   // fewer grid-barrier participants when a round holds few keys (measured)
   X->prefetch = env_int("FK_ORD_PREFETCH", 0);  // measured slower (8.1 vs 8.7 G/s at C3)
-  X->ctas_per_sm = env_int("FK_ORD_CTAS_PER_SM", g->num_blocks <= (1 << 16) ? 1 : (g->num_blocks <= (1 << 20) ? 2 : 0));
+  X->ctas_per_sm = env_int("FK_ORD_CTAS_PER_SM", g->num_blocks <= (1 << 17) ? 1 : (g->num_blocks <= (1 << 20) ? 2 : 0));
   FK_TRY(cudaMemsetAsync(X->res, 0xFF, (size_t)((g->num_blocks >> X->res_shift) + 1) * 4, st));
   X->res2 = nullptr;
   if (ord_onebar(g)) {
