@@ -35,13 +35,26 @@ class DeviceTables:
         dt, c = self.spec[name]
         return _lib.dptr(self.dev[name]) if c else _lib.c_vp(0)
 
-    def host(self, name):
+    def _fetch(self, name):
         if name not in self.mirror:
             dt, c = self.spec[name]
             self.mirror[name] = _lib.host_view(self.torch, self.dev[name], dt)[:c] if c else \
                 np.zeros(0, dtype=dt)
-        self.lent.add(name)
         return self.mirror[name]
+
+    def host(self, name):
+        """The mutable mirror handed to callers (the reference's private
+        arrays); it is pushed back before every later device operation."""
+        m = self._fetch(name)
+        self.lent.add(name)
+        return m
+
+    def peek(self, name):
+        """Read-only view of the mirror for the facades' own inspection
+        methods: not lent, so it never triggers a push-back."""
+        v = self._fetch(name).view()
+        v.flags.writeable = False
+        return v
 
     def before_device_op(self):
         """Push handed-out mirrors back (they stay lent -- the caller may still

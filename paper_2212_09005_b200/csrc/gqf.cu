@@ -294,6 +294,15 @@ int apply_small_t(const fk_gqf_geom *g, const fk_gqf_tables *cur, const fk_gqf_t
     for (int32_t f : hf)
       if (f) return f < 0 ? FK_E_INVARIANT : 1;
   }
+  // The regions ran in sorted order and in parallel, each reading the shared
+  // occupancy racily, so their load checks prove nothing.  The reference
+  // checks occupancy before each insert (pk:592-593), so if the final
+  // occupancy is below max_occupied, no order could have failed.  Otherwise
+  // discard the copy and let the full path decide in input order.
+  int64_t h_occ = 0;
+  FK_CU(cudaMemcpyAsync(&h_occ, nxt->stats, sizeof(h_occ), cudaMemcpyDeviceToHost, st));
+  FK_CU(cudaStreamSynchronize(st));
+  if (h_occ >= g->max_occupied) return 1;
   unsigned long long hm = 0;
   FK_CU(cudaMemcpyAsync(&hm, moved, sizeof(hm), cudaMemcpyDeviceToHost, st));
   int rc = rebuild_index(g, nxt, st);

@@ -132,13 +132,21 @@ class Tcf:
             raise ValueError("mode must be 'ordered' or 'concurrent'")
         self.params = params
         self.mode = mode
+        p = params
+        dt = _slot_dtype(p.slot_bits)
+        if p.block_slots * dt.itemsize * 8 > 1024:
+            # The reference bounds block_slots * slot_bits (tcf.py:61-75); the
+            # kernels hold a block in at most 1024 bits of *storage* words
+            # (slot_bits=12 is stored as uint16), so reject it here, not at
+            # the first operation.
+            raise ValueError(
+                "block_slots * storage bits = %d * %d exceeds the 1024-bit block the B200 kernels hold "
+                "(slot_bits=%d is stored as %s)" % (p.block_slots, dt.itemsize * 8, p.slot_bits, dt.name))
         torch = _lib.require_cuda(device)
         self._torch = torch
         self._device = torch.device(device) if device is not None else \
             torch.device("cuda", torch.cuda.current_device())
         self._lib = _lib.load()
-        p = params
-        dt = _slot_dtype(p.slot_bits)
         self._dtype = dt
         self._t = _DeviceTables(torch, self._device, {
             "blocks": (dt, p.main_slots), "backing": (dt, p.backing_slots)})
@@ -378,7 +386,7 @@ class Tcf:
         p = self.params
         fmask = (1 << p.tag_bits) - 1
         out = []
-        blocks, backing = self._blocks, self._backing
+        blocks, backing = self._t.peek("blocks"), self._t.peek("backing")
         for i in np.flatnonzero(blocks > TOMBSTONE).tolist():
             w = int(blocks[i])
             out.append((i // p.block_slots, w & fmask, w >> p.tag_bits))
@@ -389,7 +397,7 @@ class Tcf:
 
     def occupancy(self, block_index):
         p = self.params
-        blk = self._blocks[block_index * p.block_slots:(block_index + 1) * p.block_slots]
+        blk = self._t.peek("blocks")[block_index * p.block_slots:(block_index + 1) * p.block_slots]
         return int((blk > TOMBSTONE).sum())
 
     def _census(self):

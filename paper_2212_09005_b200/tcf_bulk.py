@@ -173,7 +173,7 @@ class BulkTcf:
         torch = self._torch
         p = self.params
         w = np.sort(np.ascontiguousarray(words).astype(self._dtype))
-        if int(self._fill[block_index]) + len(w) > p.block_slots:
+        if int(self._t.peek("fill")[block_index]) + len(w) > p.block_slots:
             raise FilterFullError("block %d cannot take %d more words" % (block_index, len(w)))
         if not len(w):
             return
@@ -262,10 +262,10 @@ class BulkTcf:
 
     # -- inspection (quiescent; host mirrors) -----------------------------------
     def occupancy(self, block_index):
-        return int(self._fill[block_index])
+        return int(self._t.peek("fill")[block_index])
 
     def load_factor(self):
-        return float(self._fill.astype(np.int64).sum()) / self.params.main_slots
+        return float(self._t.peek("fill").astype(np.int64).sum()) / self.params.main_slots
 
     def size_bits(self):
         p = self.params
@@ -279,7 +279,7 @@ class BulkTcf:
     def items(self):
         """All stored (block_index, word) pairs; backing entries get -1."""
         p = self.params
-        blocks, fill, backing = self._blocks, self._fill, self._backing
+        blocks, fill, backing = self._t.peek("blocks"), self._t.peek("fill"), self._t.peek("backing")
         out = []
         for b in np.flatnonzero(fill).tolist():
             base = b * p.block_slots
@@ -321,8 +321,8 @@ class BulkTcf:
         """The reference's host checks over the mirrored image."""
         p = self.params
         B = p.block_slots
-        blocks = self._blocks.reshape(p.num_blocks, B)
-        fill = self._fill.astype(np.int64)
+        blocks = self._t.peek("blocks").reshape(p.num_blocks, B)
+        fill = self._t.peek("fill").astype(np.int64)
         if (fill > B).any():
             raise ValidationError("block %d fill over capacity" % int(np.flatnonzero(fill > B)[0]))
         idx = np.arange(B)[None, :]
@@ -337,7 +337,7 @@ class BulkTcf:
         tail = (~live) & (vals != EMPTY)
         if tail.any():
             raise ValidationError("block %d tail not empty" % int(np.flatnonzero(tail.any(1))[0]))
-        bk = self._backing
+        bk = self._t.peek("backing")
         used = int(fill.sum()) + int(((bk != EMPTY) & (bk != TOMBSTONE)).sum())
         c = self.counters
         if used != c["inserts_ok"] - c["deletes_ok"]:

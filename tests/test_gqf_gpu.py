@@ -455,6 +455,45 @@ def test_small_batches_hitting_capacity_fall_back_exactly(oracle, monkeypatch, o
     assert raised > 0
 
 
+@pytest.mark.parametrize("order", ["point", "bulk"])
+def test_small_batch_at_load_ceiling_keeps_input_order(oracle, order):
+    """Occupancy max_occupied - 1, batch [new key A, existing key B] with B's
+    increment not growing its group and fp(B) < fp(A): the reference inserts A
+    (occupancy reaches the ceiling) and raises on B (pk:592-593).  The
+    region-local small path applies in sorted order and must not succeed
+    where the reference raises.  q = 15: four quotient regions, so regions of
+    one parity run in parallel."""
+    from paper_2212_09005_b200 import CapacityError, Gqf
+    g = Gqf(q=15, r=8, seed=4)
+    o = _oracle(g, oracle)
+    p = g.params
+    rng = np.random.default_rng(123)
+    pairs = rng.choice(1 << (p.q + p.r), size=p.max_occupied + 64, replace=False)
+    pairs = [(int(x) >> p.r, int(x) & 0xFF) for x in pairs]
+    # B: (quotient 5, remainder 10) with count 1000 (4 slots; 1001 is 4 slots too)
+    pairs = [pr for pr in pairs if pr[0] not in (5, 20000)]
+    kb = craft(g, [(5, 10)])
+    g.bulk_insert(kb, np.array([1000], np.uint64))
+    o.bulk_insert(kb, np.array([1000], np.uint64))
+    fill = craft(g, pairs[: p.max_occupied - 1 - int(o.stats[0])])
+    g.bulk_insert(fill)
+    o.bulk_insert(fill)
+    assert int(o.stats[0]) == p.max_occupied - 1
+    same_image(g, o)
+    ka = craft(g, [(20000, 7)])  # another region, fingerprint above B's
+    batch = np.concatenate([ka, kb])
+    if order == "point":
+        with pytest.raises(CapacityError):
+            g.insert_many(batch)
+        assert o.insert_many(batch) == (1, 1)
+    else:
+        # bulk order is sorted (B, then A): the reference succeeds, and so must we
+        assert o.bulk_insert(batch) == []
+        g.bulk_insert(batch)
+    same_image(g, o)
+    assert int(g._stats[0]) <= p.max_occupied
+
+
 @pytest.mark.parametrize("r", [8, 16])
 def test_device_enumerate_equals_host_decode(r):
     """enumerate_items decodes on the device (fk_gqf_enumerate); it yields

@@ -58,3 +58,13 @@ def test_countgroup_codec_matches_reference(golden):
         assert countgroups.encoded_length(rem, count, r) == length
         assert countgroups.parse_group(ref, 0, length - 1, r) == (rem, count, length)
     assert countgroups.encode_group(7, 300, 8) == [7, 4, 43, 7]  # test_countgroups.py:39-43
+
+
+def test_tcf_storage_width_limit_raises_at_construction():
+    """slot_bits=12 with 80 slots passes the reference's bit check (960 bits)
+    but its uint16 storage needs 1280 bits per block: the B200 facade says so
+    in Tcf.__init__ (before touching the device), not at the first op."""
+    from paper_2212_09005_b200 import Tcf
+    TcfParams(num_blocks=4, block_slots=80, tag_bits=12, slot_bits=12)  # reference-valid
+    with pytest.raises(ValueError, match="1024-bit block"):
+        Tcf(num_blocks=4, block_slots=80, tag_bits=12, slot_bits=12)
