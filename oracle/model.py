@@ -389,8 +389,37 @@ class OracleGqf:
             raise RuntimeError("oracle invariant violation")
         return s.value, e.value
 
-    def _bulk(self, fps, deltas, op):
-        """fk/gqf.py:293-353 with workers=1: stable sort, even regions, then odd."""
+    def _region_op(self, fps, deltas, op, stats):
+        """One region's slice through the batch kernel (pk:772-801 /
+        pk:827-847) against the given stats array; -> (code, found, shifted)."""
+        sh = ctypes.c_int64(0)
+        if op == "insert":
+            fail = ctypes.c_int64(-1)
+            code = lib().orc_gqf_insert_batch(
+                *self._args(), _p(stats), ctypes.c_int64(self.phys), self.q, self.r,
+                ctypes.c_int64(self.max_occupied), _p(fps), _p(deltas), ctypes.c_int64(len(fps)),
+                ctypes.byref(sh), ctypes.byref(fail))
+            found = None
+        else:
+            found = np.zeros(len(fps), dtype=np.uint8)
+            code = lib().orc_gqf_delete_batch(
+                *self._args(), _p(stats), ctypes.c_int64(self.phys), self.q, self.r, _p(fps),
+                _p(deltas), ctypes.c_int64(len(fps)), _p(found), ctypes.byref(sh))
+        if code < 0 or (op != "insert" and code):
+            raise RuntimeError("oracle invariant violation (%d)" % code)
+        return code, found, sh.value
+
+    def _bulk(self, fps, deltas, op, workers=1):
+        """fk/gqf.py:293-353: stable sort, even regions, then odd.
+
+        workers > 1 runs the regions of one parity on threads, as the
+        reference's own worker pool does (fk/gqf.py:326-345; regions of one
+        parity never touch each other's slots, pk:758-769).  Each thread gets
+        a private copy of _stats (the reference adds to one array atomically,
+        pk:579-581) and the deltas are summed after the phase.  The load check
+        then sees a stale occupancy, so a parallel insert phase that reports
+        any capacity failure is an error here: it is only for batches that
+        stay below max_occupied (the full-size parity tests)."""
         order = np.argsort(fps, kind="stable")
         fps, deltas = fps[order], deltas[order]
         marks = np.arange(self.quotient_regions + 1, dtype=np.uint64) << np.uint64(self.r + REGION_BITS)
@@ -398,35 +427,61 @@ class OracleGqf:
         found = np.ones(len(fps), dtype=np.uint8)
         failures = []
         for parity in (0, 1):
+            jobs = []
             for g in range(parity, self.quotient_regions, 2):
                 lo, hi = int(bounds[g]), int(bounds[g + 1])
-                if lo >= hi:
-                    continue
+                if lo < hi:
+                    jobs.append((g, lo, hi))
+            if workers <= 1:
+                for g, lo, hi in jobs:
+                    if op == "insert":
+                        code, _, sh = self._region_op(fps[lo:hi], deltas[lo:hi], op, self.stats)
+                        if code:
+                            failures.append((code, g))
+                    else:
+                        _, fl, sh = self._region_op(fps[lo:hi][::-1].copy(), deltas[lo:hi][::-1].copy(), op,
+                                                    self.stats)
+                        found[lo:hi] = fl[::-1]
+                    self.shifted += sh
+                continue
+            from concurrent.futures import ThreadPoolExecutor
+            base = self.stats.copy()
+
+            def run(job):
+                g, lo, hi = job
+                st = base.copy()
                 if op == "insert":
-                    code, _ = self.insert_fps(fps[lo:hi], deltas[lo:hi])
-                    if code:
-                        failures.append((code, g))
+                    res = self._region_op(fps[lo:hi], deltas[lo:hi], op, st)
                 else:
-                    fl = self.delete_fps(fps[lo:hi][::-1].copy(), deltas[lo:hi][::-1].copy())
-                    found[lo:hi] = fl[::-1]
+                    res = self._region_op(fps[lo:hi][::-1].copy(), deltas[lo:hi][::-1].copy(), op, st)
+                return job, res, st - base
+
+            with ThreadPoolExecutor(workers) as ex:
+                for (g, lo, hi), (code, fl, sh), dst in ex.map(run, jobs):
+                    if code:
+                        raise RuntimeError("capacity failure in a parallel oracle phase (region %d)" % g)
+                    if fl is not None:
+                        found[lo:hi] = fl[::-1]
+                    self.stats += dst
+                    self.shifted += sh
         inv = np.empty_like(order)
         inv[order] = np.arange(len(order))
         return failures, found[inv].astype(bool)
 
-    def bulk_insert(self, keys, counts=None):
+    def bulk_insert(self, keys, counts=None, workers=1):
         """Returns the failure list [(code, region)] (empty on success)."""
         fps = self.fps(keys)
         if not len(fps):
             return []
         deltas = np.ones(len(fps), np.uint64) if counts is None else _u64(counts)
-        return self._bulk(fps, deltas, "insert")[0]
+        return self._bulk(fps, deltas, "insert", workers)[0]
 
-    def bulk_delete(self, keys, counts=None):
+    def bulk_delete(self, keys, counts=None, workers=1):
         fps = self.fps(keys)
         if not len(fps):
             return np.zeros(0, dtype=bool)
         deltas = np.full(len(fps), 2 ** 63, np.uint64) if counts is None else _u64(counts)
-        return self._bulk(fps, deltas, "delete")[1]
+        return self._bulk(fps, deltas, "delete", workers)[1]
 
     def image(self):
         return dict(slots=self.slots, occupieds=self.occ, runends=self.run,

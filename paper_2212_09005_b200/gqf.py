@@ -163,7 +163,7 @@ class Gqf:
 
     # -- derived views -----------------------------------------------------------
     def _stat(self, i):
-        return int(self._t.peek("stats")[i])
+        return int(self._cur.peek("stats")[i])
 
     @property
     def occupied_slots(self):
@@ -314,8 +314,8 @@ class Gqf:
     def _derive_structure(self):
         """(quotients, run starts, run ends) by global rank/select over the
         bit vectors -- independent of the device's run index."""
-        occ = np.unpackbits(self._t.peek("occupieds").view(np.uint8), bitorder="little")
-        run = np.unpackbits(self._t.peek("runends").view(np.uint8), bitorder="little")
+        occ = np.unpackbits(self._cur.peek("occupieds").view(np.uint8), bitorder="little")
+        run = np.unpackbits(self._cur.peek("runends").view(np.uint8), bitorder="little")
         quotients = np.flatnonzero(occ).astype(np.int64)
         ends = np.flatnonzero(run).astype(np.int64)
         if len(quotients) != len(ends):
@@ -359,7 +359,7 @@ class Gqf:
 
     def _enumerate_host(self):
         r = self.params.r
-        slots = self._t.peek("slots")
+        slots = self._cur.peek("slots")
         quotients, starts, ends = self._derive_structure()
         for qt, s, e in zip(quotients.tolist(), starts.tolist(), ends.tolist()):
             for rem, cnt in decode_run(slots, s, e, r):
@@ -452,7 +452,7 @@ class Gqf:
                 raise ValidationError("runs overlap")
             if np.any((ends >> REGION_BITS) > (quotients >> REGION_BITS) + 1):
                 raise ValidationError("run crossed its region hard bound")
-        offsets = self._t.peek("offsets")
+        offsets = self._cur.peek("offsets")
         bounds = np.arange(p.num_regions, dtype=np.int64) << REGION_BITS
         idx = np.searchsorted(quotients, bounds)
         derived = np.where(idx > 0, np.maximum(0, ends[np.maximum(idx - 1, 0)] - bounds + 1) if len(ends) else 0, 0)
@@ -466,7 +466,7 @@ class Gqf:
         used = np.cumsum(used[:phys]) > 0
         if int(used.sum()) != self.occupied_slots:
             raise ValidationError("used slots %d != occupied counter %d" % (int(used.sum()), self.occupied_slots))
-        slots = self._t.peek("slots")
+        slots = self._cur.peek("slots")
         if np.any(slots[~used] != 0):
             raise ValidationError("free slots hold residual data")
         total = distinct = 0
