@@ -460,7 +460,7 @@ def run_ours(args, rank, world, local_rank):
     if zq:
         result["zipf_queries"] = zq
     if rank == 0 and world == 1 and not args.no_cpu:
-        result["cpu_baseline"] = cpu_baseline(args.cpu_budget_s)
+        result["cpu_baseline"] = cpu_baseline(log_slots, args.load)
     return result if rank == 0 else None
 
 
@@ -578,6 +578,52 @@ def kmer_zipf_workload(torch, q, alpha, seed, dev, s=1.5, cmax=100, r=8):
             "s": s, "cmax": cmax, "mean_slots_per_key": mean_len}
 
 
+def _workload_bytes(args, filt, ops, world):
+    """Algorithmic bytes per item of each op of a secondary workload (the
+    figure its `roofline.achieved` is computed from):
+    * bulk TCF insert: the 8-B key read once plus the block table, fill and
+      backing arrays read and written once per batch (2 x table bytes / n);
+    * bulk TCF query: 8-B key + the 256-B b1 block (+ b2 on 14.4 %) + 1-B flag;
+    * bulk TCF delete: as the query plus the block written back;
+    * GQF bulk insert / delete (per occurrence / key): 8-B key read, one
+      8-B partition scatter + gather, and the table read and written once per
+      batch (2 x table bytes / items) -- SURVEY 8(d);
+    * GQF count: 8-B key + occupieds, runends and slot sectors + 8-B count."""
+    t = filt._local if world > 1 else filt
+    if args.workload == "bulk_tcf":
+        tab = sum(v.numel() for v in t._t.dev.values())
+        n = ops[0][2]
+        return {"insert": 8 + 2.0 * tab / n, "query_pos": 8 + 256 * 1.144 + 1, "query_neg": 8 + 512 + 1,
+                "delete": 8 + 256 * 1.144 + 256 + 1}, tab
+    tab = sum(v.numel() for v in t._cur.dev.values())
+    b = {name: (8 + 16 + 2.0 * tab / n) for name, _, n in ops if name != "count"}
+    b["count"] = 8 + 3 * 32 + 8
+    return b, tab
+
+
+def _workload_kernel(workload, op):
+    if workload == "bulk_tcf":
+        return {"insert": "fk_btcf_insert pipeline (CUB partition sort + k_btcf_merge + route + backing)",
+                "query_pos": "k_btcf_query", "query_neg": "k_btcf_query",
+                "delete": "fk_btcf_delete pipeline (sort + k_btcf_delete x2 + backing)"}[op]
+    return {"bulk_insert": "fk_gqf_apply insert pipeline (hash/split + radix sort + RLE + decode/merge/place)",
+            "count": "k_gqf_count",
+            "bulk_delete": "fk_gqf_apply delete pipeline (sort + reduce + decode/merge/place)"}[op]
+
+
+def _workload_traffic(workload, op, items):
+    """DRAM bytes (read + write) of the op's kernels per launch of the op,
+    from the newest committed ncu capture of that workload (profiles/
+    r2*_<workload>_<op>_dram.json, written by scripts/prof_workloads.py)."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_%s_%s_dram.json" % (workload, op))),
+                       reverse=True):
+        d = json.load(open(path))
+        return {"bytes_per_launch": d["dram_bytes"] * items / d["items"], "bytes_per_op": d["dram_bytes"] / d["items"],
+                "source": os.path.relpath(path, ROOT)}
+    return None
+
+
 def run_workload(args, rank, world, local_rank):
     import torch
     local_rank %= torch.cuda.device_count()
@@ -603,47 +649,79 @@ def run_workload(args, rank, world, local_rank):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(len(ops) + 1)] for _ in range(args.steps)]
+    # at least ~1.5 s of timed steps, so the clock sampler sees the load
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    step()
+    t1.record(stream)
+    t1.synchronize()
+    one = t0.elapsed_time(t1)
+    steps = args.steps
+    if not args.exact_steps:
+        steps = max(steps, min(400, int(1500.0 / max(one, 1e-3)) + 1))
+    if dist:
+        t = torch.tensor([steps], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        steps = int(t.item())
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(len(ops) + 1)] for _ in range(steps)]
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local_rank) as clk:
         t0.record(stream)
-        for s in range(args.steps):
+        for s in range(steps):
             step(evs[s])
         t1.record(stream)
         torch.cuda.synchronize()
     ms_total = t0.elapsed_time(t1)
     if dist:
         ms_total = max_over_ranks(torch, ms_total, dev)
-    ms_step = ms_total / args.steps
+    ms_step = ms_total / steps
     items = sum(n for _, _, n in ops)
     per_op = {}
     for i, (name, _, n) in enumerate(ops):
-        ms = float(np.mean([evs[s][i].elapsed_time(evs[s][i + 1]) for s in range(args.steps)]))
+        ms = float(np.mean([evs[s][i].elapsed_time(evs[s][i + 1]) for s in range(steps)]))
         per_op[name] = {"ops_per_s": n / (ms / 1e3), "ms": ms, "items": n}
     e2e = None
     if not args.no_e2e:
         hx = {k: v.cpu().pin_memory() for k, v in x.items()}
         step(inp=hx)
         torch.cuda.synchronize()
+        ne = max(1, min(steps, 3))
         tsum = time.perf_counter()
-        for _ in range(max(1, min(args.steps, 3))):
+        for _ in range(ne):
             step(inp=hx)
         torch.cuda.synchronize()
-        te = (time.perf_counter() - tsum) / max(1, min(args.steps, 3))
+        te = (time.perf_counter() - tsum) / ne
         if dist:
             te = max_over_ranks(torch, te, dev)
         e2e = {"value": items * world / te, "unit": UNIT, "ms_per_step": te * 1e3,
                "h2d_bytes_per_step": 8 * items,
                "d2h_bytes_per_step": sum(RESULT_BYTES.get(name, 0) * m for name, _, m in ops)}
     launches = count_launches(torch, step) if not args.no_launch_count else None
+    peak, peak_kind = peaks()
+    bpo, tab = _workload_bytes(args, filt, ops, world)
+    dom = max(per_op, key=lambda k: per_op[k]["ms"])
+    for name in per_op:
+        gbs = bpo[name] * per_op[name]["ops_per_s"] / 1e9
+        per_op[name].update({"bytes_per_op": bpo[name], "achieved_gbs": gbs, "frac_of_%s_hbm" % peak_kind: gbs / peak})
+    traffic = _workload_traffic(args.workload, dom, per_op[dom]["items"])
+    achieved = per_op[dom]["achieved_gbs"]
     res = {"metric": METRIC, "value": items * world / (ms_step / 1e3), "unit": UNIT, "n_gpus": world,
-           "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+           "steps": steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "u16" if args.workload == "bulk_tcf" else "u8",
-           "data": "synthetic", "config": {"workload": desc, "l2": "no flush: inputs + tables rewritten per step"},
-           "per_op": per_op, "e2e": e2e, "gpu_launches": launches * args.steps if launches is not None else None,
+           "data": "synthetic",
+           "config": {"workload": desc, "table_bytes": tab,
+                      "l2": "no flush: inputs + tables rewritten per step (table %s the 126 MB L2)"
+                            % ("inside" if tab < (126 << 20) else "larger than")},
+           "per_op": per_op,
+           "roofline": {"bound": "hbm", "kernel": _workload_kernel(args.workload, dom), "op": dom,
+                        "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                        "peak_kind": peak_kind, "bytes_per_op": bpo[dom],
+                        "traffic": traffic["bytes_per_launch"] if traffic else None,
+                        "traffic_bytes_per_op": traffic["bytes_per_op"] if traffic else None,
+                        "traffic_source": traffic["source"] if traffic else None},
+           "e2e": e2e, "gpu_launches": launches * steps if launches is not None else None,
            "gpu_launches_per_step": launches, "clocks": clk.summary()}
     if rank == 0 and world == 1 and not args.no_cpu:
         res["cpu_baseline"] = cpu_baseline_workload(cpu_key)
@@ -651,11 +729,66 @@ def run_workload(args, rank, world, local_rank):
 
 
 def cpu_baseline_workload(key):
-    """The reference's compiled kernels + restated facade glue (oracle/
-    ref_model.py) on all host cores, on the same workload."""
+    """The unmodified reference package (baseline/_ref) on all host cores on
+    the same workload through its public bulk API with workers = cores
+    (fk/bench.py:156-268); GQF C4 on a bounded q=22 sample of the same
+    spectrum.  Median of 3 where one run takes under 5 s."""
+    fk = ref_package()
+    if fk is None:
+        return _cpu_baseline_workload_kernels(key)
+    threads = os.cpu_count() or 1
+    kind, log_slots, load = key
+    w = fk.workloads
+    if kind == "bulk_tcf":
+        nb = (1 << log_slots) // 128
+        n = int(load * (1 << log_slots))
+        keys = w.counter_stream(1, TAG_UNIFORM, n)
+        negs = w.counter_stream(2, TAG_FPR, n)
+
+        def run():
+            f = fk.BulkTcf(fk.BulkTcfParams(num_blocks=nb))
+            t = time.perf_counter()
+            f.insert_batch(keys, workers=threads)
+            f.query_batch(keys, workers=threads)
+            f.query_batch(negs, workers=threads)
+            f.delete_batch(keys, workers=threads)
+            return 4 * n, time.perf_counter() - t
+        what = "bulk TCF 2^%d slots, insert_batch + 2x query_batch + delete_batch" % log_slots
+    else:
+        if kind == "gqf_kmer":
+            qs = min(log_slots, 22)
+            occ, uniq = kmer_zipf_host(qs, load, 1)
+            what = ("GQF q=%d (bounded sample of the q=%d run) k-mer Zipf spectrum at load %.2f, naive "
+                    "bulk_insert + count_many + bulk_delete" % (qs, log_slots, load))
+        else:
+            qs = log_slots
+            occ = w.gen_keys(w.WorkloadSpec("ur_count", n=int(load * (1 << qs)) // 4, seed=1))
+            uniq = np.unique(occ)
+            what = "GQF q=%d ur_count (full size), naive bulk_insert + count_many + bulk_delete" % qs
+
+        def run():
+            f = fk.Gqf(fk.GqfParams(q=qs))
+            t = time.perf_counter()
+            f.bulk_insert(occ, workers=threads)
+            f.count_many(uniq, workers=threads)
+            f.bulk_delete(uniq, workers=threads)
+            return len(occ) + 2 * len(uniq), time.perf_counter() - t
+    ops, dt = run()
+    rates = [ops / dt]
+    if dt < 5.0:
+        rates += [o / d for o, d in (run(), run())]
+    return {"value": float(np.median(rates)), "unit": UNIT, "cores": threads, "kind": "reference",
+            "cpu_model": cpu_model(), "repeats": len(rates),
+            "sample": "unmodified reference package (baseline/_ref) public API, workers=%d: %s (%d ops, %.1f s "
+                      "per run, median of %d)" % (threads, what, ops, dt, len(rates))}
+
+
+def _cpu_baseline_workload_kernels(key):
+    """Fallback without baseline/_ref: the reference's compiled kernels +
+    restated facade glue (oracle/ref_model.py)."""
     from oracle import ref_model
     if not ref_model.available():
-        return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": "oracle/_ref not built"}
+        return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": "reference not built"}
     threads = os.cpu_count() or 1
     kind, log_slots, load = key
     if kind == "bulk_tcf":
@@ -671,11 +804,14 @@ def cpu_baseline_workload(key):
         f.delete_batch(keys, threads)
         dt = time.perf_counter() - t
         ops = 4 * n
-        what = "bulk TCF 2^%d, insert_batch+2x query_batch+delete_batch, workers=%d" % (log_slots, threads)
-    elif kind == "gqf_kmer":
-        # bounded sample: the same spectrum and load factor on a q=22 table
+    else:
+        from paper_2212_09005_b200.workloads import WorkloadSpec, gen_keys
         qs = min(log_slots, 22)
-        occ, uniq = kmer_zipf_host(qs, load, 1)
+        if kind == "gqf_kmer":
+            occ, uniq = kmer_zipf_host(qs, load, 1)
+        else:
+            occ = gen_keys(WorkloadSpec("ur_count", n=int(load * (1 << qs)) // 4, seed=1))
+            uniq = np.unique(occ)
         f = ref_model.RefGqf(qs)
         t = time.perf_counter()
         f.bulk_insert(occ, workers=threads)
@@ -683,101 +819,221 @@ def cpu_baseline_workload(key):
         f.bulk_delete(uniq, workers=threads)
         dt = time.perf_counter() - t
         ops = len(occ) + 2 * len(uniq)
-        what = ("GQF q=%d (scaled from q=%d) k-mer Zipf spectrum at load %.2f, naive bulk_insert + count_many + "
-                "bulk_delete, workers=%d" % (qs, log_slots, load, threads))
-    else:
-        from paper_2212_09005_b200.workloads import WorkloadSpec, gen_keys
-        occ = gen_keys(WorkloadSpec("ur_count", n=int(load * (1 << log_slots)) // 4, seed=1))
-        uniq = np.unique(occ)
-        f = ref_model.RefGqf(log_slots)
-        t = time.perf_counter()
-        f.bulk_insert(occ, workers=threads)
-        f.count_many(uniq, threads)
-        f.bulk_delete(uniq, workers=threads)
-        dt = time.perf_counter() - t
-        ops = len(occ) + 2 * len(uniq)
-        what = "GQF q=%d ur_count naive bulk_insert + count_many + bulk_delete, workers=%d" % (log_slots, threads)
-    return {"value": ops / dt, "unit": UNIT, "cores": threads, "kind": "reference",
-            "sample": "reference _ckernels (oracle/_ref) + facade glue: %s (%d ops, %.1f s)" % (what, ops, dt)}
+    return {"value": ops / dt, "unit": UNIT, "cores": threads, "kind": "reference", "cpu_model": cpu_model(),
+            "sample": "reference _ckernels (oracle/_ref) + restated facade glue: %s (%d ops, %.1f s)"
+                      % (kind, ops, dt)}
+
+
+def secondary_lines(args, rank, world, local_rank):
+    """configs[0] (bulk TCF 2^20), configs[1] (C2: GQF q=22 ur_count) and
+    configs[3] (C4: GQF q=28 k-mer Zipf at load 0.9), each a full line of its
+    own (value, per-op, roofline, e2e, clocks, cpu_baseline), carried under
+    the headline line's "secondary" key so the driver's single run records
+    them."""
+    import copy
+    import torch
+    out = {}
+    for wl in ("bulk_tcf", "gqf", "gqf_kmer"):
+        a = copy.copy(args)
+        a.workload = wl
+        a.log_slots_set = False
+        a.load = 0.9
+        a.steps = 3
+        a.exact_steps = False
+        out[wl] = run_workload(a, rank, world, local_rank)
+        torch.cuda.empty_cache()
+    return out
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline / reference arm: the reference's own compiled kernels
+# CPU baseline / reference arm: the UNMODIFIED reference package
 # ---------------------------------------------------------------------------
+#
+# oracle/install_ref.sh pip-installs /root/reference/pkg (its Cython
+# _ckernels built with the reference's own setup.py) into baseline/_ref,
+# which travels to the GPU box.  The reference arm and the cpu_baseline legs
+# drive that package through its public API and its own bench drivers
+# (fk/bench.py:101-268: key-range slices on OS threads over the point API,
+# workers= on the bulk API).  When baseline/_ref is absent, the compiled
+# kernels in oracle/_ref with restated facade glue (oracle/ref_model.py)
+# stand in.
 
-def _ref_step(log_slots, load, threads, seed=1):
-    from oracle import ref_model
-    nb = (1 << log_slots) // 16
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def ref_package():
+    """The reference `filterkit` from baseline/_ref with its compiled backend,
+    or None."""
+    if not os.path.isdir(os.path.join(REF_DIR, "filterkit")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    try:
+        import filterkit
+        import filterkit.bench  # noqa: F401
+    except ImportError:
+        return None
+    if "c" not in filterkit.available_backends():
+        return None
+    return filterkit
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _ref_c3_driver(fk, log_slots, threads):
+    cfg = fk.bench.BenchConfig(filter_id="tcf", op="insert", log_slots=log_slots, threads=threads)
+    return fk.bench._PointTcfDriver(cfg)
+
+
+def _ref_c3_step(fk, log_slots, keys, negs, threads):
+    """One C3 step through the reference's own point-TCF driver
+    (fk/bench.py:101-148; Tcf.insert_many/query_many/delete_many, fk/tcf.py:
+    142-192, on key-range slices across OS threads): seconds per op."""
+    d = _ref_c3_driver(fk, log_slots, threads)
+    d.build()
+    t = [time.perf_counter()]
+    d.insert(keys, threads, 1)
+    t.append(time.perf_counter())
+    d.query(keys, threads)
+    t.append(time.perf_counter())
+    d.query(negs, threads)
+    t.append(time.perf_counter())
+    d.delete(keys, threads)
+    t.append(time.perf_counter())
+    return {op: t[i + 1] - t[i] for i, op in enumerate(("insert", "query_pos", "query_neg", "delete"))}
+
+
+def _ref_c3_one_thread(fk, log_slots, keys, negs, threads, parts=8):
+    """The single-thread figure on a bounded sample of the same
+    step: the keys are cut into 8*parts pieces and every 8th piece is inserted
+    (later deleted) by ONE thread, timed, the others by `threads` threads,
+    untimed, in key order -- so the timed inserts see every load level; 1/8
+    of the positives and of the negatives are queried by one thread.
+    -> (ops, seconds)."""
+    d = _ref_c3_driver(fk, log_slots, threads)
+    d.build()
+    f = d.filt
+    pk = np.array_split(keys, 8 * parts)
+    pn = np.array_split(negs, 8 * parts)
+    ops, sec = 0, 0.0
+
+    def phase(pieces, fn_one, fn_many, timed_every=8):
+        nonlocal ops, sec
+        for i, piece in enumerate(pieces):
+            if i % timed_every == 0:
+                t = time.perf_counter()
+                fn_one(piece)
+                sec += time.perf_counter() - t
+                ops += len(piece)
+            elif fn_many is not None:
+                fn_many(piece)
+
+    phase(pk, f.insert_many, lambda x: d.insert(x, threads, 1))
+    phase(pk, f.query_many, None)
+    phase(pn, f.query_many, None)
+    phase(pk, f.delete_many, lambda x: d.delete(x, threads))
+    return ops, sec
+
+
+def _c3_keys_host(log_slots, load, fk=None):
     n = int(load * (1 << log_slots))
-    bs = int(round(nb * 16 * 0.01))
-    keys = counter_stream(seed, TAG_UNIFORM, n)
-    negs = counter_stream(seed + 1, TAG_FPR, n)
-    f = ref_model.RefTcf(nb, backing_slots=bs)
+    gen = fk.workloads.counter_stream if fk is not None else counter_stream
+    return gen(1, TAG_UNIFORM, n), gen(2, TAG_FPR, n)
+
+
+def cpu_baseline(log_slots=28, load=0.9, repeats=3):
+    """The reference package on all host cores, C3 at full size (2^28 slots,
+    the same keys as the GPU run): median of `repeats` steps (fk/bench.py:
+    77, :488)."""
+    threads = os.cpu_count() or 1
+    fk = ref_package()
+    if fk is None:
+        return _cpu_baseline_kernels(log_slots, load, threads)
+    keys, negs = _c3_keys_host(log_slots, load, fk)
+    rates = []
+    for _ in range(repeats):
+        tt = _ref_c3_step(fk, log_slots, keys, negs, threads)
+        rates.append(4 * len(keys) / sum(tt.values()))
+    return {"value": float(np.median(rates)), "unit": UNIT, "cores": threads, "kind": "reference",
+            "cpu_model": cpu_model(), "repeats": repeats, "steps_ops_per_s": rates,
+            "sample": "unmodified reference package (baseline/_ref, pip-installed from /root/reference/pkg, "
+                      "compiled backend) through its own point-TCF bench driver (fk/bench.py:101-148): C3 at full "
+                      "size, 2^%d slots at %.2f load, insert+pos+neg+delete of the same keys as the GPU run, "
+                      "%d threads slicing the keys (fk/bench.py:86-97), median of %d steps"
+                      % (log_slots, load, threads, repeats)}
+
+
+def _cpu_baseline_kernels(log_slots, load, threads):
+    """Fallback without baseline/_ref: the reference's compiled kernels
+    (oracle/_ref) under restated facade glue (oracle/ref_model.py)."""
+    from oracle import ref_model
+    if not ref_model.available():
+        return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                "sample": "unavailable: neither baseline/_ref nor oracle/_ref is built"}
+    nb = (1 << log_slots) // 16
+    keys, negs = _c3_keys_host(log_slots, load)
+    f = ref_model.RefTcf(nb, backing_slots=int(round(nb * 16 * 0.01)))
     t = time.perf_counter()
     f.insert_many(keys, threads)
     f.query_many(keys, threads)
     f.query_many(negs, threads)
     f.delete_many(keys, threads)
     dt = time.perf_counter() - t
-    return 4 * n, dt
-
-
-def _ref_kind():
-    from oracle import ref_model
-    return "reference" if ref_model.available() else None
-
-
-def cpu_baseline(budget_s=15.0):
-    """The reference's compiled _ckernels on all host cores, on a bounded
-    sample: the same workload shape with the table scaled down so the run
-    takes about budget_s."""
-    if _ref_kind() is None:
-        return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
-                "sample": "unavailable: oracle/_ref not built"}
-    threads = os.cpu_count() or 1
-    ops, dt = _ref_step(20, 0.9, threads)
-    rate = ops / dt
-    log_slots = 20
-    while log_slots < 28 and 4 * 0.9 * (1 << (log_slots + 1)) / rate < budget_s:
-        log_slots += 1
-    ops, dt = _ref_step(log_slots, 0.9, threads)
-    return {"value": ops / dt, "unit": UNIT, "cores": threads, "kind": "reference",
-            "sample": "reference _ckernels (oracle/_ref), point TCF 2^%d slots at 0.9 load, insert+pos+neg+delete "
-                      "(%d ops, %.1f s), %d threads slicing keys like fk/bench.py:86-97"
-                      % (log_slots, ops, dt, threads)}
+    return {"value": 4 * len(keys) / dt, "unit": UNIT, "cores": threads, "kind": "reference",
+            "cpu_model": cpu_model(),
+            "sample": "reference _ckernels (oracle/_ref) + restated facade glue, point TCF 2^%d slots at %.2f "
+                      "load, insert+pos+neg+delete, %d threads" % (log_slots, load, threads)}
 
 
 def run_reference(args, rank, world):
+    """--impl reference: the unmodified reference package on the host cores,
+    on our arm's config (C3: 2^28 slots, 0.9 load, the same keys), every
+    step at full size."""
     if rank != 0:
         return None
-    if _ref_kind() is None:
-        return {"impl": "reference", "unavailable": "oracle/_ref (reference _ckernels build) not present"}
+    fk = ref_package()
     threads = os.cpu_count() or 1
-    # size the per-step sample so that W+K steps finish in a few minutes
-    ops, dt = _ref_step(20, args.load, threads)
-    rate = ops / dt
-    log_slots = 20
-    per_step_budget = max(2.0, 150.0 / max(1, args.steps + args.warmup))
-    while log_slots < args.log_slots and 4 * args.load * (1 << (log_slots + 1)) / rate < per_step_budget:
-        log_slots += 1
+    if fk is None:
+        return {"impl": "reference", "unavailable": "baseline/_ref (reference package install) not present"}
+    log_slots = args.log_slots
+    keys, negs = _c3_keys_host(log_slots, args.load, fk)
     for _ in range(args.warmup):
-        _ref_step(log_slots, args.load, threads)
-    tot_ops, tot_t = 0, 0.0
-    for s in range(args.steps):
-        o, t = _ref_step(log_slots, args.load, threads, seed=1 + s)
-        tot_ops += o
-        tot_t += t
-    value = tot_ops / tot_t
-    sample = ("reference _ckernels (oracle/_ref), point TCF 2^%d slots at %.2f load, insert+pos+neg+delete per step, "
-              "%d threads" % (log_slots, args.load, threads))
+        _ref_c3_step(fk, log_slots, keys, negs, threads)
+    steps = [_ref_c3_step(fk, log_slots, keys, negs, threads) for _ in range(args.steps)]
+    tot_t = sum(sum(st.values()) for st in steps)
+    ops_step = 4 * len(keys)
+    value = ops_step * args.steps / tot_t
+    rates = [ops_step / sum(st.values()) for st in steps]
+    per_op = {op: {"ops_per_s": len(keys) / float(np.mean([st[op] for st in steps])),
+                   "ms": 1e3 * float(np.mean([st[op] for st in steps]))} for op in steps[0]}
+    one_ops, one_s = _ref_c3_one_thread(fk, log_slots, keys, negs, threads)
+    sample = ("unmodified reference package (baseline/_ref, pip-installed from /root/reference/pkg, compiled "
+              "backend) through its own point-TCF bench driver (fk/bench.py:101-148): 2^%d slots at %.2f load, "
+              "insert+pos+neg+delete of the GPU run's keys each step, %d threads slicing the keys "
+              "(fk/bench.py:86-97)" % (log_slots, args.load, threads))
     return {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u16",
             "data": "synthetic",
-            "config": {"workload": "C3 (scaled sample): point TCF, 2^%d slots, uniform keys, insert+query+delete"
-                                   % log_slots},
+            "config": {"workload": "C3: point TCF, 2^%d slots/GPU (nb=2^%d x B=16, 16-bit tags, 1%% backing), "
+                                   "uniform 64-bit keys, insert+pos query+neg query+delete at %.2f load"
+                                   % (log_slots, log_slots - 4, args.load),
+                       "keys_per_op_per_gpu": len(keys), "same_config_as_gpu_arm": True},
+            "per_op": per_op, "median_step_ops_per_s": float(np.median(rates)),
+            "one_thread": {"ops_per_s": one_ops / one_s, "ops": one_ops, "seconds": one_s,
+                           "sample": "same table and keys; every 8th of 64 key pieces inserted/deleted by one "
+                                     "thread (timed) between multi-thread pieces (untimed), 1/8 of the "
+                                     "positive and negative queries by one thread"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
-                             "sample": sample},
+                             "cpu_model": cpu_model(), "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
@@ -796,7 +1052,10 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-concurrent", action="store_true")
     ap.add_argument("--no-launch-count", action="store_true")
-    ap.add_argument("--cpu-budget-s", type=float, default=15.0)
+    ap.add_argument("--no-secondary", action="store_true",
+                    help="skip the configs[0]/C2/C4 lines carried under 'secondary'")
+    ap.add_argument("--exact-steps", action="store_true",
+                    help="secondary workloads: time exactly --steps steps (default: at least ~1.5 s)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     args.log_slots_set = args.log_slots is not None
@@ -822,6 +1081,10 @@ def main():
             else:
                 dist.init_process_group(backend)
         res = (run_ours if args.workload == "tcf" else run_workload)(args, rank, world, local_rank)
+        if args.workload == "tcf" and not args.no_secondary and not args.log_slots_set:
+            sec = secondary_lines(args, rank, world, local_rank)
+            if res is not None:
+                res["secondary"] = sec
         if world > 1:
             import torch.distributed as dist
             dist.destroy_process_group()

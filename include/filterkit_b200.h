@@ -182,6 +182,46 @@ int fk_btcf_partition(const fk_btcf_geom *g, const uint64_t *keys, int keys_are_
 int fk_btcf_merge_lists(const fk_btcf_geom *g, void *blocks, uint32_t *fill, const uint64_t *sorted_keys,
                         const uint32_t *seg_lo, const uint32_t *seg_hi, uint32_t *status, void *stream);
 
+/* ---- bulk-TCF kernel contract, one entry per reference function --------
+ * The reference's facade (fk/tcf_bulk.py:145-325) calls these on raw arrays;
+ * the fused fk_btcf_insert / fk_btcf_delete above run the same steps without
+ * the host round trips.  All synchronous (each returns a host count). */
+
+/* replaces btcf_route (_ckernels.pyx:408-444, _pykernels.py:266-287): the
+ * sequential two-choice routing of n items in input order against the
+ * committed fill (u32[num_blocks], unchanged); dest (device int64[n]) gets
+ * the chosen block or -1.  b1s/b2s are device int64[n]. */
+int fk_btcf_route(const uint32_t *fill, int64_t num_blocks, int block_slots, const int64_t *b1s, const int64_t *b2s,
+                  int64_t n, int64_t *dest, void *stream);
+
+/* replaces btcf_merge_lists (_ckernels.pyx:379-405, _pykernels.py:244-263):
+ * for blocks b in [b_lo, b_hi) in ascending order, merge words[starts[b]:
+ * ends[b]] (slot_t, sorted) into the sorted prefix; stops at the first block
+ * that would overflow.  *status_out (HOST) = 0, or 1 + that block. */
+int fk_btcf_merge_words(const fk_btcf_geom *g, void *blocks, uint32_t *fill, const void *words, int64_t n_words,
+                        const int64_t *starts, const int64_t *ends, int64_t b_lo, int64_t b_hi, int64_t *status_out,
+                        void *stream);
+
+/* replaces btcf_delete_blocklocal (_ckernels.pyx:482-512, _pykernels.py:
+ * 315-337): each sorted item k of block b's segment (b in [b_lo, b_hi))
+ * removes one stored copy of words[k] from block b; removed[k] (device u8)
+ * flags it; *n_removed (HOST) = the number removed. */
+int fk_btcf_delete_blocklocal(const fk_btcf_geom *g, void *blocks, uint32_t *fill, const void *words,
+                              int64_t n_words, const int64_t *starts, const int64_t *ends, int64_t b_lo, int64_t b_hi,
+                              uint8_t *removed, int64_t *n_removed, void *stream);
+
+/* replaces backing_insert_batch (_ckernels.pyx:447-466, _pykernels.py:
+ * 290-301): fingerprints in input order into the backing table; codes
+ * (device u8[n]) = P_BACKING (2) or P_FULL (3); *n_fail (HOST) = FULL count. */
+int fk_backing_insert_batch(const fk_btcf_geom *g, void *backing, const uint64_t *fps, int64_t n, uint8_t *codes,
+                            int64_t *n_fail, void *stream);
+
+/* replaces backing_delete_batch (_ckernels.pyx:515-549, _pykernels.py:
+ * 340-363): removed (device u8[n]) per fingerprint, input order;
+ * *n_removed (HOST) = the number removed. */
+int fk_backing_delete_batch(const fk_btcf_geom *g, void *backing, const uint64_t *fps, int64_t n, uint8_t *removed,
+                            int64_t *n_removed, void *stream);
+
 /* ---- GQF (counting quotient filter) ------------------------------------- */
 
 /* Geometry, derived on the host exactly as GqfParams (gqf.py:52-95). */
@@ -265,6 +305,20 @@ int fk_gqf_rebuild_index(const fk_gqf_geom *g, const fk_gqf_tables *t, void *str
 int fk_gqf_apply(const fk_gqf_geom *g, const fk_gqf_tables *cur, const fk_gqf_tables *next,
                  const uint64_t *keys, int keys_are_fps, const uint64_t *deltas, int64_t n, int op, int order,
                  uint8_t *found, fk_gqf_result *result, void *stream);
+
+/* replaces gqf_insert_batch (_ckernels.pyx:1147-1202, _pykernels.py:772-801)
+ * exactly: fingerprints (device u64[n]) with deltas (device u64[n]) applied
+ * in input order to the image `t` IN PLACE, stopping at the first capacity
+ * failure: *code (HOST) = 0 / GQF_LOAD_CAPACITY / GQF_SHIFT_BOUND,
+ * *fail_idx (HOST) = the failing item or -1, *shift_out (HOST) += slots
+ * moved.  t->spill is rebuilt from the bit vectors first.  Synchronous. */
+int fk_gqf_insert_batch(const fk_gqf_geom *g, const fk_gqf_tables *t, const uint64_t *fps, const uint64_t *deltas,
+                        int64_t n, int32_t *code, int64_t *fail_idx, int64_t *shift_out, void *stream);
+
+/* replaces gqf_delete_batch (_ckernels.pyx:1253-1296, _pykernels.py:827-847):
+ * input order, in place; found (device u8[n]); *shift_out (HOST) += moved. */
+int fk_gqf_delete_batch(const fk_gqf_geom *g, const fk_gqf_tables *t, const uint64_t *fps, const uint64_t *deltas,
+                        int64_t n, uint8_t *found, int64_t *shift_out, void *stream);
 
 /* ---- hash-prefix sharding (new in this build) -------------- */
 

@@ -78,6 +78,15 @@ _SIGS = {
                                c_vp]),
     "fk_btcf_partition": (c_i32, [ctypes.POINTER(BtcfGeom), c_vp, c_i32, c_i64, c_vp, c_vp, c_vp]),
     "fk_btcf_merge_lists": (c_i32, [ctypes.POINTER(BtcfGeom), c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "fk_btcf_route": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp, c_i64, c_vp, c_vp]),
+    "fk_btcf_merge_words": (c_i32, [ctypes.POINTER(BtcfGeom), c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_i64,
+                                    ctypes.POINTER(c_i64), c_vp]),
+    "fk_btcf_delete_blocklocal": (c_i32, [ctypes.POINTER(BtcfGeom), c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_i64,
+                                          c_i64, c_vp, ctypes.POINTER(c_i64), c_vp]),
+    "fk_backing_insert_batch": (c_i32, [ctypes.POINTER(BtcfGeom), c_vp, c_vp, c_i64, c_vp, ctypes.POINTER(c_i64),
+                                        c_vp]),
+    "fk_backing_delete_batch": (c_i32, [ctypes.POINTER(BtcfGeom), c_vp, c_vp, c_i64, c_vp, ctypes.POINTER(c_i64),
+                                        c_vp]),
     "fk_shard_partition": (c_i32, [c_vp, c_vp, c_i64, c_u64, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "fk_shard_unpermute": (c_i32, [c_vp, c_vp, c_i64, c_i32, c_vp, c_vp]),
     "fk_shard_dispatch": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_u64, c_i32, c_i32, ctypes.c_uint32, c_vp, c_vp, c_vp,
@@ -94,6 +103,10 @@ _SIGS = {
     "fk_gqf_validate": (c_i32, [ctypes.POINTER(GqfGeom), ctypes.POINTER(GqfTables), c_vp, c_vp]),
     "fk_gqf_enumerate": (c_i32, [ctypes.POINTER(GqfGeom), ctypes.POINTER(GqfTables), c_vp, c_vp, c_i64,
                                  ctypes.POINTER(c_i64), c_vp]),
+    "fk_gqf_insert_batch": (c_i32, [ctypes.POINTER(GqfGeom), ctypes.POINTER(GqfTables), c_vp, c_vp, c_i64,
+                                    ctypes.POINTER(c_i32), ctypes.POINTER(c_i64), ctypes.POINTER(c_i64), c_vp]),
+    "fk_gqf_delete_batch": (c_i32, [ctypes.POINTER(GqfGeom), ctypes.POINTER(GqfTables), c_vp, c_vp, c_i64, c_vp,
+                                    ctypes.POINTER(c_i64), c_vp]),
     "fk_gqf_apply": (c_i32, [ctypes.POINTER(GqfGeom), ctypes.POINTER(GqfTables), ctypes.POINTER(GqfTables),
                              c_vp, c_i32, c_vp, c_i64, c_i32, c_i32, c_vp, ctypes.POINTER(GqfResult), c_vp]),
 }

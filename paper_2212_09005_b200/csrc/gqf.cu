@@ -827,4 +827,70 @@ int fk_gqf_apply(const fk_gqf_geom *g, const fk_gqf_tables *cur, const fk_gqf_ta
   }
 }
 
+// ---- contract-shaped entries (the reference's raw-array kernel contract) ----
+//
+// gqf_insert_batch / gqf_delete_batch (_ckernels.pyx:1147-1202, :1253-1296)
+// mutate ONE table image in place and process the fingerprints in input
+// order.  fk_gqf_apply may leave its result in a second image (canonical
+// rebuild); these wrappers give it stream-ordered scratch for that image and
+// copy the result back, so the caller sees the contract's in-place update.
+// The derived run index (t->spill) is rebuilt from the bit vectors first:
+// a contract caller hands in raw arrays it may have written itself.
+static int contract_apply(const fk_gqf_geom *g, const fk_gqf_tables *t, const uint64_t *fps, const uint64_t *deltas,
+                          int64_t n, int op, uint8_t *found, fk_gqf_result *res, cudaStream_t st) {
+  int rc = rebuild_index(g, t, st);
+  if (rc) return rc;
+  const size_t sb = g->r / 8;
+  const size_t words = (size_t)(g->phys >> 6);
+  const size_t spill = (size_t)((1LL << g->q) >> 6) > 0 ? (size_t)((1LL << g->q) >> 6) : 1;
+  Scratch S(st);
+  fk_gqf_tables nx;
+  nx.slots = S.get<char>((size_t)g->phys * sb);
+  nx.occupieds = S.get<uint64_t>(words);
+  nx.runends = S.get<uint64_t>(words);
+  nx.offsets = S.get<int32_t>((size_t)g->num_regions);
+  nx.stats = S.get<int64_t>(3);
+  nx.spill = S.get<uint32_t>(spill);
+  if (S.err) return -(int)S.err;
+  rc = fk_gqf_apply(g, t, &nx, fps, 1, deltas, n, op, FK_ORDER_POINT, found, res, st);
+  if (rc) return rc;
+  if (res->swapped) {
+    FK_CU(cudaMemcpyAsync(t->slots, nx.slots, (size_t)g->phys * sb, cudaMemcpyDeviceToDevice, st));
+    FK_CU(cudaMemcpyAsync(t->occupieds, nx.occupieds, words * 8, cudaMemcpyDeviceToDevice, st));
+    FK_CU(cudaMemcpyAsync(t->runends, nx.runends, words * 8, cudaMemcpyDeviceToDevice, st));
+    FK_CU(cudaMemcpyAsync(t->offsets, nx.offsets, (size_t)g->num_regions * 4, cudaMemcpyDeviceToDevice, st));
+    FK_CU(cudaMemcpyAsync(t->stats, nx.stats, 3 * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+    FK_CU(cudaMemcpyAsync(t->spill, nx.spill, spill * 4, cudaMemcpyDeviceToDevice, st));
+    res->swapped = 0;
+  }
+  FK_CU(cudaStreamSynchronize(st));
+  return 0;
+}
+
+int fk_gqf_insert_batch(const fk_gqf_geom *g, const fk_gqf_tables *t, const uint64_t *fps, const uint64_t *deltas,
+                        int64_t n, int32_t *code, int64_t *fail_idx, int64_t *shift_out, void *stream) {
+  if (!geom_ok(g) || !t || !code || !fail_idx || !deltas || n < 0 || n > 0xFFFFFFF0LL) return FK_E_ARG;
+  *code = 0;
+  *fail_idx = -1;
+  if (n == 0) return 0;
+  fk_gqf_result res{};
+  int rc = contract_apply(g, t, fps, deltas, n, FK_GQF_INSERT, nullptr, &res, (cudaStream_t)stream);
+  if (rc) return rc;
+  *code = res.code;
+  *fail_idx = res.code ? res.fail_index : -1;
+  if (shift_out) *shift_out += res.shifted;
+  return 0;
+}
+
+int fk_gqf_delete_batch(const fk_gqf_geom *g, const fk_gqf_tables *t, const uint64_t *fps, const uint64_t *deltas,
+                        int64_t n, uint8_t *found, int64_t *shift_out, void *stream) {
+  if (!geom_ok(g) || !t || !found || !deltas || n < 0 || n > 0xFFFFFFF0LL) return FK_E_ARG;
+  if (n == 0) return 0;
+  fk_gqf_result res{};
+  int rc = contract_apply(g, t, fps, deltas, n, FK_GQF_DELETE, found, &res, (cudaStream_t)stream);
+  if (rc) return rc;
+  if (shift_out) *shift_out += res.shifted;
+  return 0;
+}
+
 }  // extern "C"

@@ -1,4 +1,6 @@
+#include <stdio.h>
 #include <stdlib.h>
+#include <string.h>
 // tcf_bulk.cu -- bulk two-choice filter on sm_100a.
 //
 // Replaces the bulk half of the reference kernel contract together with the
@@ -535,6 +537,184 @@ __global__ void __launch_bounds__(kRouteW, 1) k_btcf_route_prefix(const uint32_t
   }
 }
 
+// ---------------------------------------------------------------------------
+// parallel two-choice routing by fixpoint iteration (btcf_route, ck:408-444)
+// ---------------------------------------------------------------------------
+// Item k (in the walk's order) decides d_k = rule(L(a_k, k), L(b_k, k)) with
+// L(X, k) = fill[X] + #{j < k : d_j = X} and rule = the smaller load (tie ->
+// a) unless it is >= B (-> -1).  d_0 depends on fill alone and d_k on
+// d_0..d_{k-1} only, so the system has exactly one solution: the sequential
+// walk's decisions.  Jacobi sweeps (recompute every d_k from the previous
+// iterate's counts) reach it -- after t sweeps at least the first t decisions
+// are final -- and in practice the iterate stops changing after ~50 sweeps at
+// every table size measured (2^20..2^24 slots): a decision flips only while
+// its two loads are within the perturbation of the counts.  A sweep is two
+// exclusive prefix sums and one elementwise pass:
+//   P1 over the (a, index)-sorted order of c1_j = [d_j == a_j]
+//   P2 over the (b, index)-sorted order of c2_j = [d_j == b_j != a_j]
+//   L(a_k, k) = fill[a_k] + P1[pos1_k] - P1[s1[a_k]] + P2[qA_k] - P2[s2[a_k]]
+//   L(b_k, k) = fill[b_k] + P1[qB_k] - P1[s1[b_k]] + P2[pos2_k] - P2[s2[b_k]]
+// where pos1/pos2 place item k in the two orders, s1/s2 start each block's
+// segment there, qA_k is the first position of b-order segment a_k holding
+// an index >= k, and qB_k likewise in a-order segment b_k.  Stopping rule:
+// a sweep that changes no decision has found the fixpoint.  One cooperative
+// kernel runs the sweeps (two grid barriers each); if it has not converged
+// after kJacobiMax sweeps the caller runs the sequential walk instead.
+constexpr int kJT = 256, kJItems = 4, kJTile = kJT * kJItems, kJacobiMax = 4096;
+
+struct RouteJ {
+  const uint32_t *a, *b, *fill;
+  const uint32_t *perm1, *perm2, *pos1, *pos2, *qA, *qB, *s1, *s2;
+  int32_t *d;
+  uint32_t *P1, *P2;     // [m + 1] exclusive prefix sums
+  uint32_t *ts;          // [2 parities][2 orders][T] tile sums
+  unsigned *ctl;         // [0..2] changed counts (sweep % 3), [3] sweeps run, [4] converged
+  int64_t m;
+  int T;
+  uint32_t B;
+};
+
+__device__ __forceinline__ int32_t route_rule(uint32_t l1, uint32_t l2, uint32_t a, uint32_t b, uint32_t B) {
+  const bool pa = l1 <= l2;
+  const uint32_t lp = pa ? l1 : l2;
+  return lp < B ? (int32_t)(pa ? a : b) : -1;
+}
+
+__global__ void __launch_bounds__(kJT) k_btcf_route_jacobi(RouteJ R) {
+  cg::grid_group grid = cg::this_grid();
+  typedef cub::BlockScan<unsigned long long, kJT> Scan;
+  typedef cub::BlockReduce<unsigned long long, kJT> Red;
+  __shared__ union {
+    typename Scan::TempStorage scan;
+    typename Red::TempStorage red;
+  } tmp;
+  __shared__ unsigned long long s_off;
+  const int64_t m = R.m;
+  const int T = R.T;
+  const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // sweep 0's iterate: the rule on the committed fills alone, with its tile sums
+  for (int64_t k = tid; k < m; k += nth) {
+    const uint32_t a = R.a[k], b = R.b[k];
+    const int32_t d = route_rule(R.fill[a], R.fill[b], a, b, R.B);
+    R.d[k] = d;
+    if (d == (int32_t)a) atomicAdd(&R.ts[R.pos1[k] / kJTile], 1u);
+    else if (d == (int32_t)b) atomicAdd(&R.ts[T + R.pos2[k] / kJTile], 1u);
+  }
+  grid.sync();
+  unsigned sweep = 0;
+  for (;; sweep++) {
+    const int par = sweep & 1;
+    uint32_t *ts = R.ts + (size_t)par * 2 * T, *tsn = R.ts + (size_t)(par ^ 1) * 2 * T;
+    // ---- phase S: P1, P2 of the current iterate (tile scans + tile offsets)
+    for (int64_t i = tid; i < 2 * (int64_t)T; i += nth) tsn[i] = 0;
+    if (tid == 0) R.ctl[(sweep + 1) % 3] = 0;
+    for (int t = blockIdx.x; t < T; t += gridDim.x) {
+      // offsets: sums of the tile sums before t, both orders packed (P1 << 32 | P2)
+      unsigned long long part = 0;
+      for (int u = threadIdx.x; u < t; u += kJT)
+        part += ((unsigned long long)ts[u] << 32) | ts[T + u];
+      unsigned long long off = Red(tmp.red).Sum(part);
+      if (threadIdx.x == 0) s_off = off;
+      __syncthreads();
+      off = s_off;
+      unsigned long long v[kJItems];
+      const int64_t p0 = (int64_t)t * kJTile + (int64_t)threadIdx.x * kJItems;
+#pragma unroll
+      for (int j = 0; j < kJItems; j++) {
+        const int64_t p = p0 + j;
+        unsigned long long c = 0;
+        if (p < m) {
+          const uint32_t i1 = R.perm1[p], i2 = R.perm2[p];
+          const int32_t d1 = __ldcg(&R.d[i1]), d2 = __ldcg(&R.d[i2]);
+          const uint32_t a2 = R.a[i2], b2 = R.b[i2];
+          c = ((unsigned long long)(d1 == (int32_t)R.a[i1]) << 32) | (unsigned long long)(d2 == (int32_t)b2 && a2 != b2);
+        }
+        v[j] = c;
+      }
+      Scan(tmp.scan).ExclusiveSum(v, v);
+#pragma unroll
+      for (int j = 0; j < kJItems; j++) {
+        const int64_t p = p0 + j;
+        if (p <= m) {
+          const unsigned long long x = v[j] + off;
+          R.P1[p] = (uint32_t)(x >> 32);
+          R.P2[p] = (uint32_t)x;
+        }
+      }
+      __syncthreads();
+      // P[m] (the totals) when m is a multiple of the tile
+      if (t == T - 1 && threadIdx.x == kJT - 1 && p0 + kJItems == m) {
+        // v holds exclusive sums; the last item's own flags are re-read
+        const uint32_t i1 = R.perm1[m - 1], i2 = R.perm2[m - 1];
+        const int32_t d1 = __ldcg(&R.d[i1]), d2 = __ldcg(&R.d[i2]);
+        const uint32_t a2 = R.a[i2], b2 = R.b[i2];
+        R.P1[m] = R.P1[m - 1] + (d1 == (int32_t)R.a[i1]);
+        R.P2[m] = R.P2[m - 1] + (d2 == (int32_t)b2 && a2 != b2);
+      }
+    }
+    grid.sync();
+    // ---- phase D: every decision from the counts of the current iterate
+    unsigned changed = 0;
+    for (int64_t k = tid; k < m; k += nth) {
+      const uint32_t a = R.a[k], b = R.b[k];
+      const uint32_t l1 = R.fill[a] + (R.P1[R.pos1[k]] - R.P1[R.s1[a]]) + (R.P2[R.qA[k]] - R.P2[R.s2[a]]);
+      const uint32_t l2 = R.fill[b] + (R.P1[R.qB[k]] - R.P1[R.s1[b]]) + (R.P2[R.pos2[k]] - R.P2[R.s2[b]]);
+      const int32_t d = route_rule(l1, l2, a, b, R.B);
+      if (d != R.d[k]) {
+        R.d[k] = d;
+        changed++;
+      }
+      if (d == (int32_t)a) atomicAdd(&tsn[R.pos1[k] / kJTile], 1u);
+      else if (d == (int32_t)b) atomicAdd(&tsn[T + R.pos2[k] / kJTile], 1u);
+    }
+    changed = __reduce_add_sync(0xFFFFFFFFu, changed);
+    if ((threadIdx.x & 31) == 0 && changed) atomicAdd(&R.ctl[sweep % 3], changed);
+    grid.sync();
+    const unsigned c = __ldcg(&R.ctl[sweep % 3]);
+    if (c == 0 || sweep + 1 >= (unsigned)kJacobiMax) {
+      if (tid == 0) {
+        R.ctl[3] = sweep + 1;
+        R.ctl[4] = c == 0 ? 1u : 0u;
+      }
+      return;
+    }
+  }
+}
+
+// segment bounds of a sorted u32 array: s[v] = first position of value v,
+// e[v] = one past its last (arrays pre-zeroed: absent values stay empty)
+__global__ void k_seg_bounds_u32(const uint32_t *__restrict__ v, int64_t n, uint32_t *__restrict__ s,
+                                 uint32_t *__restrict__ e) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t x = v[p];
+    if (p == 0 || v[p - 1] != x) s[x] = (uint32_t)p;
+    if (p == n - 1 || v[p + 1] != x) e[x] = (uint32_t)(p + 1);
+  }
+}
+
+// pos[perm[p]] = p
+__global__ void k_invert_perm(const uint32_t *__restrict__ perm, int64_t n, uint32_t *__restrict__ pos) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x)
+    pos[perm[p]] = (uint32_t)p;
+}
+
+// q[k] = first position p in [s[x_k], e[x_k]) with perm[p] >= k (perm is
+// ascending inside a segment), i.e. s[x_k] + #{j < k in segment x_k}
+__global__ void k_seg_rank(const uint32_t *__restrict__ x, const uint32_t *__restrict__ perm,
+                           const uint32_t *__restrict__ s, const uint32_t *__restrict__ e, int64_t n,
+                           uint32_t *__restrict__ q) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t v = x[k];
+    uint32_t lo = s[v], hi = e[v];
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (perm[mid] < (uint32_t)k) lo = mid + 1; else hi = mid;
+    }
+    q[k] = lo;
+  }
+}
+
 // leftover positions -> (b1, b2) of each leftover and the words
 __global__ void k_left_blocks(BDev P, const uint64_t *__restrict__ keys, const uint32_t *__restrict__ sval,
                               const uint32_t *__restrict__ lpos, int64_t m, uint32_t *__restrict__ lb1,
@@ -704,6 +884,88 @@ __global__ void k_seg0_len(const uint32_t *__restrict__ seg_lo, const uint32_t *
 }
 
 // ---------------------------------------------------------------------------
+// contract-shape adapters (the reference's raw-array entry points)
+// ---------------------------------------------------------------------------
+__global__ void k_i64_to_u32(const int64_t *__restrict__ a, int64_t n, uint32_t *__restrict__ b) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    b[i] = (uint32_t)a[i];
+}
+
+__global__ void k_i32_to_i64(const int32_t *__restrict__ a, int64_t n, int64_t *__restrict__ b) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    b[i] = a[i];
+}
+
+// per-block segments of the contract's (starts, ends) restricted to
+// [b_lo, b_hi); every other block gets an empty segment
+__global__ void k_contract_segs(const int64_t *__restrict__ starts, const int64_t *__restrict__ ends, int64_t b_lo,
+                                int64_t b_hi, uint64_t nb, uint32_t *__restrict__ lo, uint32_t *__restrict__ hi) {
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < (int64_t)nb;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    const bool in = b >= b_lo && b < b_hi && ends[b] > starts[b];
+    lo[b] = in ? (uint32_t)starts[b] : 0u;
+    hi[b] = in ? (uint32_t)ends[b] : 0u;
+  }
+}
+
+// skey[k] = (b << f) | word for every item k of block b's segment
+template <typename S>
+__global__ void k_contract_keys(const S *__restrict__ words, const uint32_t *__restrict__ lo,
+                                const uint32_t *__restrict__ hi, uint64_t nb, int f, uint64_t *__restrict__ skey) {
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < (int64_t)nb;
+       b += (int64_t)gridDim.x * blockDim.x)
+    for (uint32_t k = lo[b]; k < hi[b]; k++) skey[k] = ((uint64_t)b << f) | (uint64_t)words[k];
+}
+
+// the first block (ascending) a merge would overfill: status = 1 + b
+__global__ void k_merge_check(const uint32_t *__restrict__ fill, const uint32_t *__restrict__ lo,
+                              const uint32_t *__restrict__ hi, uint64_t nb, int B, unsigned *__restrict__ status) {
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < (int64_t)nb;
+       b += (int64_t)gridDim.x * blockDim.x)
+    if (hi[b] > lo[b] && (int64_t)fill[b] + (hi[b] - lo[b]) > B) atomicMin(status, (unsigned)(b + 1));
+}
+
+// blocks at or past `first` keep their data (the reference's loop stops at
+// the first overflow, ck:393-397)
+__global__ void k_cut_segs(uint32_t *__restrict__ lo, uint32_t *__restrict__ hi, uint64_t nb,
+                           const unsigned *__restrict__ status) {
+  const unsigned st = *status;
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < (int64_t)nb;
+       b += (int64_t)gridDim.x * blockDim.x)
+    if (st != kNone && (uint64_t)b >= (uint64_t)(st - 1)) lo[b] = hi[b] = 0;
+}
+
+__global__ void k_seg_flag_sum(const uint8_t *__restrict__ flag, const uint32_t *__restrict__ lo,
+                               const uint32_t *__restrict__ hi, uint64_t nb, int64_t *__restrict__ out) {
+  unsigned long long c = 0;
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < (int64_t)nb;
+       b += (int64_t)gridDim.x * blockDim.x)
+    for (uint32_t k = lo[b]; k < hi[b]; k++) c += flag[k];
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd((unsigned long long *)out, c);
+}
+
+// backing_insert_batch codes: P_BACKING when placed, P_FULL otherwise
+__global__ void k_backing_codes(const uint8_t *__restrict__ ok, int64_t n, uint8_t *__restrict__ codes,
+                                int64_t *__restrict__ fails) {
+  unsigned long long c = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    codes[i] = ok[i] ? kBacking : kFull;
+    c += ok[i] ? 0 : 1;
+  }
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd((unsigned long long *)fails, c);
+}
+
+__global__ void k_flag_sum(const uint8_t *__restrict__ f, int64_t n, int64_t *__restrict__ out) {
+  unsigned long long c = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    c += f[i];
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd((unsigned long long *)out, c);
+}
+
+// ---------------------------------------------------------------------------
 // host pipeline pieces
 // ---------------------------------------------------------------------------
 inline int bits_for(uint64_t v) {  // bits needed to represent v
@@ -815,6 +1077,187 @@ int backing_ordered(const BDev &P, const uint64_t *keys, const uint32_t *bidx, i
   return 0;
 }
 
+cudaError_t sort_pairs_u32(Scratch &S, const uint32_t *kin, uint32_t *kout, const uint32_t *vin, uint32_t *vout,
+                           int64_t n, int end_bit) {
+  size_t tb = 0;
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, tb, kin, kout, vin, vout, n, 0, end_bit, S.st);
+  if (e) return e;
+  void *tmp = S.get<char>(tb);
+  if (!tmp) return S.err;
+  return cub::DeviceRadixSort::SortPairs(tmp, tb, kin, kout, vin, vout, n, 0, end_bit, S.st);
+}
+
+// Routing of m items (a = b1s, b = b2s, u32) against the committed fills:
+// dest[k] = the sequential walk's decision (block or -1).  a_sorted: items are
+// already in ascending a order (the insert pipeline's leftovers), so the
+// a-order permutation is the identity and needs no sort.  Tries the
+// fixpoint kernel; falls back to the one-warp walk if it did not converge
+// (never observed) -- either way the result is the walk's.
+int route_items(Scratch &S, const uint32_t *a, const uint32_t *b, int64_t m, const uint32_t *fill, uint64_t nb,
+                uint32_t B, bool a_sorted, int32_t *dest) {
+  cudaStream_t st = S.st;
+  if (m <= 0) return 0;
+  const char *force = getenv("FK_ROUTE");  // "seq" | "prefix" | "jacobi" (tests / measurements)
+  const bool want_seq = force && !strcmp(force, "seq");
+  const bool want_prefix = force && !strcmp(force, "prefix");
+  if (!want_seq && !want_prefix) {
+    const int kb = bits_for(nb - 1) ? bits_for(nb - 1) : 1;
+    uint32_t *perm1 = S.get<uint32_t>(m), *perm2 = S.get<uint32_t>(m), *pos1 = S.get<uint32_t>(m),
+             *pos2 = S.get<uint32_t>(m), *qA = S.get<uint32_t>(m), *qB = S.get<uint32_t>(m);
+    uint32_t *iota = S.get<uint32_t>(m), *bs = S.get<uint32_t>(m), *as = a_sorted ? nullptr : S.get<uint32_t>(m);
+    uint32_t *s1 = S.get<uint32_t>(nb), *e1 = S.get<uint32_t>(nb), *s2 = S.get<uint32_t>(nb),
+             *e2 = S.get<uint32_t>(nb);
+    uint32_t *P1 = S.get<uint32_t>(m + 1), *P2 = S.get<uint32_t>(m + 1);
+    const int T = (int)((m + kJTile - 1) / kJTile);
+    uint32_t *ts = S.get<uint32_t>((size_t)4 * T);
+    unsigned *ctl = S.get<unsigned>(8);
+    FK_P(perm1); FK_P(perm2); FK_P(pos1); FK_P(pos2); FK_P(qA); FK_P(qB); FK_P(iota); FK_P(bs);
+    FK_P(s1); FK_P(e1); FK_P(s2); FK_P(e2); FK_P(P1); FK_P(P2); FK_P(ts); FK_P(ctl);
+    if (!a_sorted) FK_P(as);
+    k_iota_u32<<<grid_for(m), 256, 0, st>>>(iota, m);
+    FK_CHECK_LAUNCH();
+    FK_S(cudaMemsetAsync(s1, 0, nb * 4, st));
+    FK_S(cudaMemsetAsync(e1, 0, nb * 4, st));
+    FK_S(cudaMemsetAsync(s2, 0, nb * 4, st));
+    FK_S(cudaMemsetAsync(e2, 0, nb * 4, st));
+    FK_S(cudaMemsetAsync(ts, 0, (size_t)16 * T, st));
+    FK_S(cudaMemsetAsync(ctl, 0, 32, st));
+    if (a_sorted) {
+      FK_S(cudaMemcpyAsync(perm1, iota, m * 4, cudaMemcpyDeviceToDevice, st));
+      FK_S(cudaMemcpyAsync(pos1, iota, m * 4, cudaMemcpyDeviceToDevice, st));
+      k_seg_bounds_u32<<<grid_for(m), 256, 0, st>>>(a, m, s1, e1);
+    } else {
+      FK_S(sort_pairs_u32(S, a, as, iota, perm1, m, kb));
+      k_invert_perm<<<grid_for(m), 256, 0, st>>>(perm1, m, pos1);
+      k_seg_bounds_u32<<<grid_for(m), 256, 0, st>>>(as, m, s1, e1);
+    }
+    FK_CHECK_LAUNCH();
+    FK_S(sort_pairs_u32(S, b, bs, iota, perm2, m, kb));
+    k_invert_perm<<<grid_for(m), 256, 0, st>>>(perm2, m, pos2);
+    k_seg_bounds_u32<<<grid_for(m), 256, 0, st>>>(bs, m, s2, e2);
+    k_seg_rank<<<grid_for(m), 256, 0, st>>>(a, perm2, s2, e2, m, qA);
+    k_seg_rank<<<grid_for(m), 256, 0, st>>>(b, perm1, s1, e1, m, qB);
+    FK_CHECK_LAUNCH();
+    RouteJ R{a, b, fill, perm1, perm2, pos1, pos2, qA, qB, s1, s2, dest, P1, P2, ts, ctl, m, T, B};
+    int grid = coop_grid((const void *)k_btcf_route_jacobi, kJT);
+    if (!grid) return FK_E_ARG;
+    if (T < grid) grid = T;
+    void *args[] = {(void *)&R};
+    FK_S(cudaLaunchCooperativeKernel((const void *)k_btcf_route_jacobi, dim3(grid), dim3(kJT), args, 0, st));
+    unsigned h[2] = {0, 0};
+    FK_S(cudaMemcpyAsync(h, ctl + 3, 8, cudaMemcpyDeviceToHost, st));
+    FK_S(cudaStreamSynchronize(st));
+    if (getenv("FK_ROUTE_STATS")) fprintf(stderr, "fk route: m=%lld sweeps=%u converged=%u\n", (long long)m, h[0], h[1]);
+    if (h[1]) return 0;
+    // not converged: fall through to the sequential walk
+  }
+  uint32_t *load = S.get<uint32_t>(nb);
+  FK_P(load);
+  size_t sm = (size_t)nb * 4;
+  if (want_prefix) {
+    if (!a_sorted) return FK_E_ARG;
+    FK_S(cudaMemcpyAsync(load, fill, nb * 4, cudaMemcpyDeviceToDevice, st));
+    FK_S(cudaFuncSetAttribute(k_btcf_route_prefix, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRouteSmem));
+    k_btcf_route_prefix<<<1, kRouteW, kRouteSmem, st>>>(a, b, m, load, B, dest);
+  } else if (sm <= 200 * 1024) {
+    if (sm > 48 * 1024)
+      FK_S(cudaFuncSetAttribute(k_btcf_route_seq<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    k_btcf_route_seq<true><<<1, 32, sm, st>>>(a, b, m, fill, nb, load, B, dest);
+  } else {
+    FK_S(cudaMemcpyAsync(load, fill, nb * 4, cudaMemcpyDeviceToDevice, st));
+    k_btcf_route_seq<false><<<1, 32, 0, st>>>(a, b, m, fill, nb, load, B, dest);
+  }
+  FK_CHECK_LAUNCH();
+  return 0;
+}
+
+// ---- contract entries (host side) ----------------------------------------
+template <typename S_t>
+int merge_words_t(const BDev &P, const void *words, int64_t n_words, const int64_t *starts, const int64_t *ends,
+                  int64_t b_lo, int64_t b_hi, int64_t *status_out, cudaStream_t st) {
+  Scratch S(st);
+  uint64_t *skey = S.get<uint64_t>(n_words > 0 ? n_words : 1);
+  uint32_t *lo = S.get<uint32_t>(P.nb), *hi = S.get<uint32_t>(P.nb);
+  unsigned *status = S.get<unsigned>(1);
+  FK_P(skey); FK_P(lo); FK_P(hi); FK_P(status);
+  FK_S(cudaMemsetAsync(status, 0xFF, 4, st));
+  k_contract_segs<<<grid_for(P.nb), 256, 0, st>>>(starts, ends, b_lo, b_hi, P.nb, lo, hi);
+  if (n_words > 0) k_contract_keys<S_t><<<grid_for(P.nb), 256, 0, st>>>((const S_t *)words, lo, hi, P.nb, 0, skey);
+  k_merge_check<<<grid_for(P.nb), 256, 0, st>>>(P.fill, lo, hi, P.nb, P.B, status);
+  k_cut_segs<<<grid_for(P.nb), 256, 0, st>>>(lo, hi, P.nb, status);
+  FK_CHECK_LAUNCH();
+  int rc = merge_segments<S_t>(P, skey, lo, hi, 0, 0, nullptr, status, st);
+  if (rc) return rc;
+  unsigned h = kNone;
+  FK_S(cudaMemcpyAsync(&h, status, 4, cudaMemcpyDeviceToHost, st));
+  FK_S(cudaStreamSynchronize(st));
+  *status_out = h == kNone ? 0 : (int64_t)h;
+  return 0;
+}
+
+template <typename S_t>
+int delete_blocklocal_t(const BDev &P, const void *words, int64_t n_words, const int64_t *starts,
+                        const int64_t *ends, int64_t b_lo, int64_t b_hi, uint8_t *removed, int64_t *n_out,
+                        cudaStream_t st) {
+  Scratch S(st);
+  const int64_t nw = n_words > 0 ? n_words : 1;
+  uint64_t *skey = S.get<uint64_t>(nw);
+  uint32_t *sval = S.get<uint32_t>(nw), *lo = S.get<uint32_t>(P.nb), *hi = S.get<uint32_t>(P.nb);
+  uint8_t *dummy = S.get<uint8_t>(nw);
+  int64_t *cnt = S.get<int64_t>(1);
+  FK_P(skey); FK_P(sval); FK_P(lo); FK_P(hi); FK_P(dummy); FK_P(cnt);
+  FK_S(cudaMemsetAsync(cnt, 0, 8, st));
+  k_iota_u32<<<grid_for(nw), 256, 0, st>>>(sval, nw);
+  k_contract_segs<<<grid_for(P.nb), 256, 0, st>>>(starts, ends, b_lo, b_hi, P.nb, lo, hi);
+  if (n_words > 0)
+    k_contract_keys<S_t><<<grid_for(P.nb), 256, 0, st>>>((const S_t *)words, lo, hi, P.nb, P.f, skey);
+  FK_CHECK_LAUNCH();
+  int threads;
+  size_t smem;
+  if (per_block_launch_cfg<S_t>(P.B, 1, &threads, &smem)) return FK_E_ARG;
+  auto dkern = k_btcf_delete<S_t>;
+  if (smem > 48 * 1024) FK_S(cudaFuncSetAttribute(dkern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int64_t ctas = ((int64_t)P.nb + threads / 32 - 1) / (threads / 32);
+  int64_t cap = (int64_t)num_sms() * 32;
+  // hit[k] (per sorted item) is the contract's removed[k]
+  dkern<<<(int)(ctas < cap ? ctas : cap), threads, smem, st>>>(P, skey, sval, lo, hi, removed, dummy);
+  k_seg_flag_sum<<<grid_for(P.nb), 256, 0, st>>>(removed, lo, hi, P.nb, cnt);
+  FK_CHECK_LAUNCH();
+  cudaError_t err;
+  *n_out = read_i64(cnt, st, &err);
+  FK_S(err);
+  return 0;
+}
+
+template <typename S_t, int OP>
+int backing_batch_t(const BDev &P, const uint64_t *fps, int64_t n, uint8_t *out, int64_t *count_out,
+                    cudaStream_t st) {
+  Scratch S(st);
+  uint32_t *idx = S.get<uint32_t>(n);
+  uint8_t *ok = S.get<uint8_t>(n);
+  int64_t *cnt = S.get<int64_t>(1);
+  FK_P(idx); FK_P(ok); FK_P(cnt);
+  FK_S(cudaMemsetAsync(cnt, 0, 8, st));
+  if (P.bsize) {
+    k_iota_u32<<<grid_for(n), 256, 0, st>>>(idx, n);
+    int rc = backing_ordered<S_t, OP>(P, fps, idx, n, ok, S);
+    if (rc) return rc;
+  } else {
+    FK_S(cudaMemsetAsync(ok, 0, n, st));
+  }
+  if (OP == 0) {
+    k_backing_codes<<<grid_for(n), 256, 0, st>>>(ok, n, out, cnt);  // cnt = fails
+  } else {
+    FK_S(cudaMemcpyAsync(out, ok, n, cudaMemcpyDeviceToDevice, st));
+    k_flag_sum<<<grid_for(n), 256, 0, st>>>(ok, n, cnt);
+  }
+  FK_CHECK_LAUNCH();
+  cudaError_t err;
+  *count_out = read_i64(cnt, st, &err);
+  FK_S(err);
+  return 0;
+}
+
 // ---- insert_batch (tcf_bulk.py:179-257) ------------------------------------
 template <typename S_t>
 int btcf_insert(const BDev &P, const uint64_t *keys, int64_t n, uint64_t *failed_keys, int64_t *n_failed,
@@ -849,28 +1292,14 @@ int btcf_insert(const BDev &P, const uint64_t *keys, int64_t n, uint64_t *failed
   int64_t m = read_i64(cnt, st, &err);
   FK_S(err);
   if (m > 0) {
-    uint32_t *lb1 = S.get<uint32_t>(m), *lb2 = S.get<uint32_t>(m), *load = S.get<uint32_t>(P.nb);
+    uint32_t *lb1 = S.get<uint32_t>(m), *lb2 = S.get<uint32_t>(m);
     int32_t *dest = S.get<int32_t>(m);
-    FK_P(lb1); FK_P(lb2); FK_P(load); FK_P(dest);
+    FK_P(lb1); FK_P(lb2); FK_P(dest);
     k_left_blocks<<<grid_for(m), 256, 0, st>>>(P, keys, sval, lpos, m, lb1, lb2);
     FK_CHECK_LAUNCH();
-    uint32_t Bu = (uint32_t)P.B;
-    size_t sm = (size_t)P.nb * 4;
-    if ((P.nb >= (1u << 16) && !getenv("FK_ROUTE_WARP")) || getenv("FK_ROUTE_PREFIX")) {
-      // large tables: block-parallel conflict-free prefixes (FK_ROUTE_WARP
-      // forces the single-warp walk, FK_ROUTE_PREFIX this one)
-      FK_S(cudaMemcpyAsync(load, P.fill, P.nb * 4, cudaMemcpyDeviceToDevice, st));
-      FK_S(cudaFuncSetAttribute(k_btcf_route_prefix, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRouteSmem));
-      k_btcf_route_prefix<<<1, kRouteW, kRouteSmem, st>>>(lb1, lb2, m, load, Bu, dest);
-    } else if (sm <= 200 * 1024) {
-      if (sm > 48 * 1024)
-        FK_S(cudaFuncSetAttribute(k_btcf_route_seq<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-      k_btcf_route_seq<true><<<1, 32, sm, st>>>(lb1, lb2, m, P.fill, P.nb, load, Bu, dest);
-    } else {
-      FK_S(cudaMemcpyAsync(load, P.fill, P.nb * 4, cudaMemcpyDeviceToDevice, st));
-      k_btcf_route_seq<false><<<1, 32, 0, st>>>(lb1, lb2, m, P.fill, P.nb, load, Bu, dest);
-    }
-    FK_CHECK_LAUNCH();
+    // phase 2 routing (tcf_bulk.py:210-223): leftovers are in (b1, word) order
+    rc = route_items(S, lb1, lb2, m, P.fill, P.nb, (uint32_t)P.B, true, dest);
+    if (rc) return rc;
     // group by destination; segment 0 = backing (tcf_bulk.py:225-234)
     uint64_t *k2 = S.get<uint64_t>(m), *skey2 = S.get<uint64_t>(m);
     uint32_t *v2 = S.get<uint32_t>(m), *sval2 = S.get<uint32_t>(m);
@@ -1161,6 +1590,89 @@ int fk_btcf_merge_lists(const fk_btcf_geom *g, void *blocks, uint32_t *fill, con
     case 1: return merge_segments<uint8_t>(P, sorted_keys, seg_lo, seg_hi, 0, 0, nullptr, status, st);
     case 4: return merge_segments<uint32_t>(P, sorted_keys, seg_lo, seg_hi, 0, 0, nullptr, status, st);
     default: return merge_segments<uint16_t>(P, sorted_keys, seg_lo, seg_hi, 0, 0, nullptr, status, st);
+  }
+}
+
+// ---- contract-shaped entries (one per reference kernel-contract function) ----
+
+int fk_btcf_route(const uint32_t *fill, int64_t num_blocks, int block_slots, const int64_t *b1s, const int64_t *b2s,
+                  int64_t n, int64_t *dest, void *stream) {
+  if (!fill || num_blocks < 1 || num_blocks > 0xFFFFFFF0LL || block_slots < 1 || n < 0 || n > 0xFFFFFFF0LL)
+    return FK_E_ARG;
+  if (n == 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  Scratch S(st);
+  uint32_t *a = S.get<uint32_t>(n), *b = S.get<uint32_t>(n);
+  int32_t *d = S.get<int32_t>(n);
+  FK_P(a); FK_P(b); FK_P(d);
+  k_i64_to_u32<<<grid_for(n), 256, 0, st>>>(b1s, n, a);
+  k_i64_to_u32<<<grid_for(n), 256, 0, st>>>(b2s, n, b);
+  FK_CHECK_LAUNCH();
+  int rc = route_items(S, a, b, n, fill, (uint64_t)num_blocks, (uint32_t)block_slots, false, d);
+  if (rc) return rc;
+  k_i32_to_i64<<<grid_for(n), 256, 0, st>>>(d, n, dest);
+  FK_CHECK_LAUNCH();
+  FK_S(cudaStreamSynchronize(st));
+  return 0;
+}
+
+int fk_btcf_merge_words(const fk_btcf_geom *g, void *blocks, uint32_t *fill, const void *words, int64_t n_words,
+                        const int64_t *starts, const int64_t *ends, int64_t b_lo, int64_t b_hi, int64_t *status_out,
+                        void *stream) {
+  if (!geom_ok(g) || !status_out || n_words < 0 || n_words > 0xFFFFFFF0LL || b_lo < 0 || b_hi > g->num_blocks)
+    return FK_E_ARG;
+  *status_out = 0;
+  if (b_hi <= b_lo) return 0;
+  BDev P = make_dev(g, blocks, fill, nullptr, 1);
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (g->slot_bytes) {
+    case 1: return merge_words_t<uint8_t>(P, words, n_words, starts, ends, b_lo, b_hi, status_out, st);
+    case 4: return merge_words_t<uint32_t>(P, words, n_words, starts, ends, b_lo, b_hi, status_out, st);
+    default: return merge_words_t<uint16_t>(P, words, n_words, starts, ends, b_lo, b_hi, status_out, st);
+  }
+}
+
+int fk_btcf_delete_blocklocal(const fk_btcf_geom *g, void *blocks, uint32_t *fill, const void *words,
+                              int64_t n_words, const int64_t *starts, const int64_t *ends, int64_t b_lo, int64_t b_hi,
+                              uint8_t *removed, int64_t *n_removed, void *stream) {
+  if (!geom_ok(g) || !n_removed || n_words < 0 || n_words > 0xFFFFFFF0LL || b_lo < 0 || b_hi > g->num_blocks)
+    return FK_E_ARG;
+  *n_removed = 0;
+  if (b_hi <= b_lo || n_words == 0) return 0;
+  BDev P = make_dev(g, blocks, fill, nullptr, 1);
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (g->slot_bytes) {
+    case 1: return delete_blocklocal_t<uint8_t>(P, words, n_words, starts, ends, b_lo, b_hi, removed, n_removed, st);
+    case 4: return delete_blocklocal_t<uint32_t>(P, words, n_words, starts, ends, b_lo, b_hi, removed, n_removed, st);
+    default: return delete_blocklocal_t<uint16_t>(P, words, n_words, starts, ends, b_lo, b_hi, removed, n_removed, st);
+  }
+}
+
+int fk_backing_insert_batch(const fk_btcf_geom *g, void *backing, const uint64_t *fps, int64_t n, uint8_t *codes,
+                            int64_t *n_fail, void *stream) {
+  if (!geom_ok(g) || !n_fail || n < 0 || n > 0xFFFFFFF0LL) return FK_E_ARG;
+  *n_fail = 0;
+  if (n == 0) return 0;
+  BDev P = make_dev(g, nullptr, nullptr, backing, 1);
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (g->slot_bytes) {
+    case 1: return backing_batch_t<uint8_t, 0>(P, fps, n, codes, n_fail, st);
+    case 4: return backing_batch_t<uint32_t, 0>(P, fps, n, codes, n_fail, st);
+    default: return backing_batch_t<uint16_t, 0>(P, fps, n, codes, n_fail, st);
+  }
+}
+
+int fk_backing_delete_batch(const fk_btcf_geom *g, void *backing, const uint64_t *fps, int64_t n, uint8_t *removed,
+                            int64_t *n_removed, void *stream) {
+  if (!geom_ok(g) || !n_removed || n < 0 || n > 0xFFFFFFF0LL) return FK_E_ARG;
+  *n_removed = 0;
+  if (n == 0) return 0;
+  BDev P = make_dev(g, nullptr, nullptr, backing, 1);
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (g->slot_bytes) {
+    case 1: return backing_batch_t<uint8_t, 1>(P, fps, n, removed, n_removed, st);
+    case 4: return backing_batch_t<uint32_t, 1>(P, fps, n, removed, n_removed, st);
+    default: return backing_batch_t<uint16_t, 1>(P, fps, n, removed, n_removed, st);
   }
 }
 

@@ -1,0 +1,58 @@
+"""The reference's own test suite (pkg/tests, unmodified) against the B200
+build, in two drop-in seams (VERDICT r1 "next" #3):
+
+* kernel contract: the unmodified reference package (baseline/_ref, pip-
+  installed by oracle/install_ref.sh) with paper_2212_09005_b200._b200kernels
+  registered as its compiled backend -- the reference's facades on our
+  kernels, one C-ABI entry per contract function; test_backends.py compares
+  it with the reference's pure-Python kernels on raw arrays;
+* facades: `filterkit` resolved to this package (tables resident in HBM).
+
+Each seam runs in a subprocess pytest over baseline/_ref/ref_tests (copied
+unmodified by oracle/install_ref.sh; /root/reference itself is not on the GPU
+box).  Every test must pass; the summary lines are printed for the record.
+"""
+
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REF = os.path.join(ROOT, "baseline", "_ref")
+SUITE = os.path.join(REF, "ref_tests")
+PLUGINS = os.path.join(ROOT, "tests", "refsuite")
+FILES = ["test_tcf.py", "test_tcf_bulk.py", "test_gqf.py", "test_acceptance.py", "test_bench.py",
+         "test_hashing.py", "test_countgroups.py", "test_workloads.py"]
+
+needs_suite = pytest.mark.skipif(not os.path.isdir(SUITE),
+                                 reason="baseline/_ref/ref_tests not installed (run oracle/install_ref.sh)")
+
+
+def _run(plugin, paths, files):
+    env = dict(os.environ)
+    env["PYTHONPATH"] = os.pathsep.join(paths + [env.get("PYTHONPATH", "")])
+    cmd = [sys.executable, "-m", "pytest", "-q", "-p", plugin, "-p", "no:cacheprovider", "-rfEs",
+           "--rootdir", SUITE] + files
+    r = subprocess.run(cmd, cwd=SUITE, env=env, capture_output=True, text=True, timeout=2400)
+    tail = r.stdout[-6000:] + r.stderr[-3000:]
+    print(tail)
+    out = os.path.join(ROOT, "gpurun_out")
+    if os.path.isdir(out):
+        with open(os.path.join(out, "refsuite_%s.log" % plugin), "w") as fh:
+            fh.write(r.stdout + r.stderr)
+    assert r.returncode == 0, tail
+    return r.stdout
+
+
+@needs_suite
+def test_reference_suite_on_b200_kernel_contract():
+    _run("fk_backend_plugin", [REF, PLUGINS, ROOT], FILES + ["test_backends.py"])
+
+
+@needs_suite
+def test_reference_suite_on_b200_facades():
+    _run("fk_alias_plugin", [PLUGINS, ROOT], FILES)

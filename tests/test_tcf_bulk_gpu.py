@@ -193,3 +193,21 @@ def test_device_validate_agrees_with_host_checks():
     corrupt(lambda b, fl: b.__setitem__(base, b[base + 2] + 1))            # unsorted prefix
     corrupt(lambda b, fl: b.__setitem__(base + int(fl[blk]), 77))          # tail not empty
     corrupt(lambda b, fl: fl.__setitem__(blk, fl[blk] - 1) or b.__setitem__(base + int(fl[blk]), 0))  # count mismatch
+
+
+@pytest.mark.parametrize("mode", ["jacobi", "seq", "prefix"])
+def test_route_modes_bit_exact(oracle, monkeypatch, mode):
+    """The three routers (fixpoint sweeps -- the default --, the one-warp walk
+    and the block-parallel prefix walk) give the reference's sequential
+    decisions (ck:408-444): configs[0] at 0.9 load, then an overfilled small
+    table where both blocks of some leftovers are full (dest = -1, backing)."""
+    monkeypatch.setenv("FK_ROUTE", mode)
+    f, o = _pair(oracle, num_blocks=8192)
+    keys = counter_keys(41, int(0.9 * 2 ** 20))
+    assert np.array_equal(f.insert_batch(keys), o.insert_batch(keys))
+    _same(f, o)
+    f, o = _pair(oracle, num_blocks=200, backing_fraction=0.02)
+    for s, n in enumerate([20_000, 8_000, 4_000]):
+        keys = counter_keys(50 + s, n)
+        assert np.array_equal(f.insert_batch(keys), o.insert_batch(keys)), s
+        _same(f, o)
