@@ -740,9 +740,20 @@ int apply_t(const fk_gqf_geom *g, const fk_gqf_tables *cur, const fk_gqf_tables 
   unsigned long long *dc = S.get<unsigned long long>(1);
   if (S.err) return -(int)S.err;
   FK_CU(cudaMemsetAsync(dc, 0, sizeof(unsigned long long), st));
+  // point order counts the batch's own slots too (a later item can move an
+  // earlier one's), unless the batch is non-decreasing (k_not_ascending)
+  unsigned *nasc = S.get<unsigned>(1);
+  if (S.err) return -(int)S.err;
+  unsigned h_nasc = 1;
+  if (order == FK_ORDER_POINT) {
+    FK_CU(cudaMemsetAsync(nasc, 0, sizeof(unsigned), st));
+    k_not_ascending<<<blocks_for(n), 256, 0, st>>>(keys, keys_are_fps, g->seed, fmask, n, nasc);
+    FK_CU(cudaMemcpyAsync(&h_nasc, nasc, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    FK_CU(cudaStreamSynchronize(st));
+  }
   k_diff_count<S_t><<<blocks_for(g->phys), 256, 0, st>>>(
       reinterpret_cast<const S_t *>(cur->slots), cur->runends, reinterpret_cast<const S_t *>(nxt->slots),
-      nxt->runends, g->phys, order == FK_ORDER_BULK ? 1 : 0, dc);
+      nxt->runends, g->phys, (order == FK_ORDER_BULK || !h_nasc) ? 1 : 0, dc);
   unsigned long long hdc = 0;
   FK_CU(cudaMemcpyAsync(&hdc, dc, sizeof(hdc), cudaMemcpyDeviceToHost, st));
   FK_CU(cudaStreamSynchronize(st));

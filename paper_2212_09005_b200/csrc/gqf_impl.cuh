@@ -490,6 +490,19 @@ __global__ void k_diff_count(const S *__restrict__ a, const uint64_t *__restrict
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
 }
 
+// *flag = 1 when the batch's fingerprints are NOT non-decreasing in input
+// order.  A non-decreasing batch never moves the slots it wrote itself (each
+// item lands after every earlier one), so its sequential shift work is made
+// of old slots only -- the bulk shift metric.
+__global__ void k_not_ascending(const uint64_t *__restrict__ keys, int keys_are_fps, uint64_t seed, uint64_t fmask,
+                                int64_t n, unsigned *__restrict__ flag) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x + 1; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t a = keys_are_fps ? keys[i - 1] & fmask : mix64(keys[i - 1] ^ seed) & fmask;
+    const uint64_t b = keys_are_fps ? keys[i] & fmask : mix64(keys[i] ^ seed) & fmask;
+    if (a > b) *flag = 1u;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // exact sequential path (reference algorithm, _pykernels.py:485-656), used
 // only when a batch may hit a capacity error

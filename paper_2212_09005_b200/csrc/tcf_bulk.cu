@@ -908,13 +908,16 @@ __global__ void k_contract_segs(const int64_t *__restrict__ starts, const int64_
   }
 }
 
-// skey[k] = (b << f) | word for every item k of block b's segment
+// skey[k] = (b << f) | word for every item k of block b's segment (f < 0:
+// the word alone -- the merge kernel reads only the word bits)
 template <typename S>
 __global__ void k_contract_keys(const S *__restrict__ words, const uint32_t *__restrict__ lo,
                                 const uint32_t *__restrict__ hi, uint64_t nb, int f, uint64_t *__restrict__ skey) {
   for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < (int64_t)nb;
-       b += (int64_t)gridDim.x * blockDim.x)
-    for (uint32_t k = lo[b]; k < hi[b]; k++) skey[k] = ((uint64_t)b << f) | (uint64_t)words[k];
+       b += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t bk = f < 0 ? 0 : ((uint64_t)b << f);
+    for (uint32_t k = lo[b]; k < hi[b]; k++) skey[k] = bk | (uint64_t)words[k];
+  }
 }
 
 // the first block (ascending) a merge would overfill: status = 1 + b
@@ -1182,7 +1185,7 @@ int merge_words_t(const BDev &P, const void *words, int64_t n_words, const int64
   FK_P(skey); FK_P(lo); FK_P(hi); FK_P(status);
   FK_S(cudaMemsetAsync(status, 0xFF, 4, st));
   k_contract_segs<<<grid_for(P.nb), 256, 0, st>>>(starts, ends, b_lo, b_hi, P.nb, lo, hi);
-  if (n_words > 0) k_contract_keys<S_t><<<grid_for(P.nb), 256, 0, st>>>((const S_t *)words, lo, hi, P.nb, 0, skey);
+  if (n_words > 0) k_contract_keys<S_t><<<grid_for(P.nb), 256, 0, st>>>((const S_t *)words, lo, hi, P.nb, -1, skey);
   k_merge_check<<<grid_for(P.nb), 256, 0, st>>>(P.fill, lo, hi, P.nb, P.B, status);
   k_cut_segs<<<grid_for(P.nb), 256, 0, st>>>(lo, hi, P.nb, status);
   FK_CHECK_LAUNCH();
