@@ -560,24 +560,59 @@ __global__ void __launch_bounds__(kRouteW, 1) k_btcf_route_prefix(const uint32_t
 // a sweep that changes no decision has found the fixpoint.  One cooperative
 // kernel runs the sweeps (two grid barriers each); if it has not converged
 // after kJacobiMax sweeps the caller runs the sequential walk instead.
-constexpr int kJT = 256, kJItems = 4, kJTile = kJT * kJItems, kJacobiMax = 4096;
+constexpr int kJT = 256, kJItems = 1, kJTile = kJT * kJItems, kJacobiMax = 4096;
+// never a decision (decisions are a block index or -1)
+constexpr uint32_t kNoB = 0xFFFFFFFEu;
+
+// Per item, everything a sweep reads besides the two prefix arrays is
+// static, so it is gathered once: the eight P-array positions of the two
+// loads (own position / segment start in each order, for each block) and
+// the committed fills.
+struct RouteItem {
+  uint4 p;  // P1 pos (a), P1 seg start (a), P2 pos (a), P2 seg start (a)
+  uint4 q;  // P1 pos (b), P1 seg start (b), P2 pos (b), P2 seg start (b)
+  uint4 c;  // a, b, fill[a], fill[b]
+};
 
 struct RouteJ {
-  const uint32_t *a, *b, *fill;
-  const uint32_t *perm1, *perm2, *pos1, *pos2, *qA, *qB, *s1, *s2;
-  int32_t *d;
-  uint32_t *P1, *P2;     // [m + 1] exclusive prefix sums
-  uint32_t *ts;          // [2 parities][2 orders][T] tile sums
-  unsigned *ctl;         // [0..2] changed counts (sweep % 3), [3] sweeps run, [4] converged
+  const RouteItem *it;        // [m] item order
+  const uint32_t *perm1;      // [m] a-order position -> item
+  const uint32_t *perm2;      // [m] b-order position -> item
+  const uint32_t *a_of1;      // [m] a of the item at a-order position p
+  const uint32_t *b_of2;      // [m] b of the item at b-order position p, or kNoB when its a == b
+  const uint32_t *pos1, *pos2;  // [m] item -> positions (tile of its flags)
+  int32_t *d;                 // [m] decisions (in/out)
+  uint32_t *P1, *P2;          // [m + 1] exclusive prefix sums
+  uint32_t *ts;               // [2 parities][2 orders][T] tile sums
+  unsigned *ctl;              // [3] sweeps run, [4] converged
+  unsigned *chg;              // [gridDim] this CTA's decisions changed in the last sweep
+  unsigned long long *clk;    // optional (FK_ROUTE_STATS): globaltimer at each phase end, CTA 0
   int64_t m;
   int T;
   uint32_t B;
 };
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __device__ __forceinline__ int32_t route_rule(uint32_t l1, uint32_t l2, uint32_t a, uint32_t b, uint32_t B) {
   const bool pa = l1 <= l2;
   const uint32_t lp = pa ? l1 : l2;
   return lp < B ? (int32_t)(pa ? a : b) : -1;
+}
+
+// tile sums of the flags of decision d (warp-aggregated per tile)
+__device__ __forceinline__ void route_tally(const RouteJ &R, uint32_t *tsn, bool live, int32_t d, uint32_t a,
+                                            uint32_t b, uint32_t p1, uint32_t p2) {
+  const bool c1 = live && d == (int32_t)a, c2 = live && !c1 && d == (int32_t)b;
+  const unsigned act = __ballot_sync(0xFFFFFFFFu, c1 || c2);
+  if (!(c1 || c2)) return;
+  const uint32_t slot = c1 ? p1 / kJTile : (uint32_t)R.T + p2 / kJTile;
+  const unsigned peers = __match_any_sync(act, slot);
+  if ((threadIdx.x & 31) == (unsigned)(__ffs(peers) - 1)) atomicAdd(&tsn[slot], (unsigned)__popc(peers));
 }
 
 __global__ void __launch_bounds__(kJT) k_btcf_route_jacobi(RouteJ R) {
@@ -593,92 +628,182 @@ __global__ void __launch_bounds__(kJT) k_btcf_route_jacobi(RouteJ R) {
   const int T = R.T;
   const int64_t nth = (int64_t)gridDim.x * blockDim.x;
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t mr = (m + 31) & ~(int64_t)31;  // warp-uniform trip counts (ballots below)
   // sweep 0's iterate: the rule on the committed fills alone, with its tile sums
-  for (int64_t k = tid; k < m; k += nth) {
-    const uint32_t a = R.a[k], b = R.b[k];
-    const int32_t d = route_rule(R.fill[a], R.fill[b], a, b, R.B);
-    R.d[k] = d;
-    if (d == (int32_t)a) atomicAdd(&R.ts[R.pos1[k] / kJTile], 1u);
-    else if (d == (int32_t)b) atomicAdd(&R.ts[T + R.pos2[k] / kJTile], 1u);
+  for (int64_t k = tid; k < mr; k += nth) {
+    const bool live = k < m;
+    uint4 c = make_uint4(0, 0, 0, 0);
+    uint32_t p1 = 0, p2 = 0;
+    int32_t d = -1;
+    if (live) {
+      c = R.it[k].c;
+      p1 = R.pos1[k];
+      p2 = R.pos2[k];
+      d = route_rule(c.z, c.w, c.x, c.y, R.B);
+      R.d[k] = d;
+    }
+    route_tally(R, R.ts, live, d, c.x, c.y, p1, p2);
   }
   grid.sync();
-  unsigned sweep = 0;
-  for (;; sweep++) {
+  if (R.clk && tid == 0) R.clk[0] = gtimer();
+  for (unsigned sweep = 0;; sweep++) {
     const int par = sweep & 1;
     uint32_t *ts = R.ts + (size_t)par * 2 * T, *tsn = R.ts + (size_t)(par ^ 1) * 2 * T;
     // ---- phase S: P1, P2 of the current iterate (tile scans + tile offsets)
     for (int64_t i = tid; i < 2 * (int64_t)T; i += nth) tsn[i] = 0;
-    if (tid == 0) R.ctl[(sweep + 1) % 3] = 0;
     for (int t = blockIdx.x; t < T; t += gridDim.x) {
       // offsets: sums of the tile sums before t, both orders packed (P1 << 32 | P2)
       unsigned long long part = 0;
-      for (int u = threadIdx.x; u < t; u += kJT)
-        part += ((unsigned long long)ts[u] << 32) | ts[T + u];
+      for (int u = threadIdx.x; u < t; u += kJT) part += ((unsigned long long)__ldcg(&ts[u]) << 32) | __ldcg(&ts[T + u]);
       unsigned long long off = Red(tmp.red).Sum(part);
       if (threadIdx.x == 0) s_off = off;
       __syncthreads();
       off = s_off;
       unsigned long long v[kJItems];
       const int64_t p0 = (int64_t)t * kJTile + (int64_t)threadIdx.x * kJItems;
+      uint32_t i1[kJItems], i2[kJItems];
+#pragma unroll
+      for (int j = 0; j < kJItems; j++) {
+        const int64_t p = p0 + j;
+        i1[j] = p < m ? R.perm1[p] : 0;
+        i2[j] = p < m ? R.perm2[p] : 0;
+      }
 #pragma unroll
       for (int j = 0; j < kJItems; j++) {
         const int64_t p = p0 + j;
         unsigned long long c = 0;
         if (p < m) {
-          const uint32_t i1 = R.perm1[p], i2 = R.perm2[p];
-          const int32_t d1 = __ldcg(&R.d[i1]), d2 = __ldcg(&R.d[i2]);
-          const uint32_t a2 = R.a[i2], b2 = R.b[i2];
-          c = ((unsigned long long)(d1 == (int32_t)R.a[i1]) << 32) | (unsigned long long)(d2 == (int32_t)b2 && a2 != b2);
+          const int32_t d1 = __ldcg(&R.d[i1[j]]), d2 = __ldcg(&R.d[i2[j]]);
+          c = ((unsigned long long)(d1 == (int32_t)R.a_of1[p]) << 32) | (unsigned long long)(d2 == (int32_t)R.b_of2[p]);
         }
         v[j] = c;
       }
-      Scan(tmp.scan).ExclusiveSum(v, v);
+      unsigned long long tot;
+      Scan(tmp.scan).ExclusiveSum(v, v, tot);
 #pragma unroll
       for (int j = 0; j < kJItems; j++) {
         const int64_t p = p0 + j;
-        if (p <= m) {
+        if (p < m) {
           const unsigned long long x = v[j] + off;
           R.P1[p] = (uint32_t)(x >> 32);
           R.P2[p] = (uint32_t)x;
         }
       }
+      if (t == T - 1 && threadIdx.x == 0) {  // the totals
+        const unsigned long long x = tot + off;
+        R.P1[m] = (uint32_t)(x >> 32);
+        R.P2[m] = (uint32_t)x;
+      }
       __syncthreads();
-      // P[m] (the totals) when m is a multiple of the tile
-      if (t == T - 1 && threadIdx.x == kJT - 1 && p0 + kJItems == m) {
-        // v holds exclusive sums; the last item's own flags are re-read
-        const uint32_t i1 = R.perm1[m - 1], i2 = R.perm2[m - 1];
-        const int32_t d1 = __ldcg(&R.d[i1]), d2 = __ldcg(&R.d[i2]);
-        const uint32_t a2 = R.a[i2], b2 = R.b[i2];
-        R.P1[m] = R.P1[m - 1] + (d1 == (int32_t)R.a[i1]);
-        R.P2[m] = R.P2[m - 1] + (d2 == (int32_t)b2 && a2 != b2);
-      }
     }
+    if (R.clk && tid == 0 && sweep < 64) R.clk[1 + 3 * sweep] = gtimer();
     grid.sync();
+    if (R.clk && tid == 0 && sweep < 64) R.clk[2 + 3 * sweep] = gtimer();
     // ---- phase D: every decision from the counts of the current iterate
+    // U items per thread per trip, every load of the U items issued before
+    // any is used (the sweep is a latency chain: item -> P reads -> tally)
+    constexpr int U = 1;
     unsigned changed = 0;
-    for (int64_t k = tid; k < m; k += nth) {
-      const uint32_t a = R.a[k], b = R.b[k];
-      const uint32_t l1 = R.fill[a] + (R.P1[R.pos1[k]] - R.P1[R.s1[a]]) + (R.P2[R.qA[k]] - R.P2[R.s2[a]]);
-      const uint32_t l2 = R.fill[b] + (R.P1[R.qB[k]] - R.P1[R.s1[b]]) + (R.P2[R.pos2[k]] - R.P2[R.s2[b]]);
-      const int32_t d = route_rule(l1, l2, a, b, R.B);
-      if (d != R.d[k]) {
-        R.d[k] = d;
-        changed++;
+    for (int64_t k0 = tid; k0 < mr; k0 += U * nth) {
+      RouteItem it[U];
+      int32_t dold[U];
+      uint32_t v[U][8];
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int64_t k = k0 + u * nth;
+        if (k < m) {
+          it[u] = R.it[k];
+          dold[u] = R.d[k];
+        }
       }
-      if (d == (int32_t)a) atomicAdd(&tsn[R.pos1[k] / kJTile], 1u);
-      else if (d == (int32_t)b) atomicAdd(&tsn[T + R.pos2[k] / kJTile], 1u);
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        if (k0 + u * nth < m) {
+          v[u][0] = __ldcg(&R.P1[it[u].p.x]);
+          v[u][1] = __ldcg(&R.P1[it[u].p.y]);
+          v[u][2] = __ldcg(&R.P2[it[u].p.z]);
+          v[u][3] = __ldcg(&R.P2[it[u].p.w]);
+          v[u][4] = __ldcg(&R.P1[it[u].q.x]);
+          v[u][5] = __ldcg(&R.P1[it[u].q.y]);
+          v[u][6] = __ldcg(&R.P2[it[u].q.z]);
+          v[u][7] = __ldcg(&R.P2[it[u].q.w]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int64_t k = k0 + u * nth;
+        if (k >= mr) break;  // warp-uniform (mr and nth are multiples of 32)
+        const bool live = k < m;
+        int32_t d = -1;
+        uint4 c = make_uint4(0, 0, 0, 0);
+        uint32_t p1 = 0, p2 = 0;
+        if (live) {
+          c = it[u].c;
+          p1 = it[u].p.x;
+          p2 = it[u].q.z;
+          const uint32_t l1 = c.z + (v[u][0] - v[u][1]) + (v[u][2] - v[u][3]);
+          const uint32_t l2 = c.w + (v[u][4] - v[u][5]) + (v[u][6] - v[u][7]);
+          d = route_rule(l1, l2, c.x, c.y, R.B);
+          if (d != dold[u]) {
+            R.d[k] = d;
+            changed++;
+          }
+        }
+        route_tally(R, tsn, live, d, c.x, c.y, p1, p2);
+      }
     }
-    changed = __reduce_add_sync(0xFFFFFFFFu, changed);
-    if ((threadIdx.x & 31) == 0 && changed) atomicAdd(&R.ctl[sweep % 3], changed);
+    // one flag per CTA (a single counter would take ~5K same-address atomics
+    // per sweep); each CTA ORs all flags after the barrier.  A CTA rewrites
+    // its flag only in the next phase D, after every CTA has read it (they
+    // all pass the phase-S barrier in between).
+    const int any = __syncthreads_or(changed != 0);
+    if (threadIdx.x == 0) R.chg[blockIdx.x] = (unsigned)any;
+    if (R.clk && threadIdx.x == 0 && sweep < 64) {
+      // slowest CTA's phase-D work (start = CTA 0's post-barrier time)
+      const unsigned long long w = gtimer();
+      atomicMax(&R.clk[1 + 3 * 64 + sweep], w);
+    }
     grid.sync();
-    const unsigned c = __ldcg(&R.ctl[sweep % 3]);
-    if (c == 0 || sweep + 1 >= (unsigned)kJacobiMax) {
+    if (R.clk && tid == 0 && sweep < 64) R.clk[3 + 3 * sweep] = gtimer();
+    unsigned mine = 0;
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) mine |= __ldcg(&R.chg[i]);
+    const unsigned cc = (unsigned)__syncthreads_or(mine != 0);
+    if (cc == 0 || sweep + 1 >= (unsigned)kJacobiMax) {
       if (tid == 0) {
         R.ctl[3] = sweep + 1;
-        R.ctl[4] = c == 0 ? 1u : 0u;
+        R.ctl[4] = cc == 0 ? 1u : 0u;
       }
       return;
     }
+  }
+}
+
+// the static per-item gather indices of the sweeps (RouteItem)
+__global__ void k_route_items(const uint32_t *__restrict__ a, const uint32_t *__restrict__ b,
+                              const uint32_t *__restrict__ fill, const uint32_t *__restrict__ pos1,
+                              const uint32_t *__restrict__ pos2, const uint32_t *__restrict__ qA,
+                              const uint32_t *__restrict__ qB, const uint32_t *__restrict__ s1,
+                              const uint32_t *__restrict__ s2, int64_t m, RouteItem *__restrict__ it) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < m; k += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t x = a[k], y = b[k];
+    RouteItem r;
+    r.p = make_uint4(pos1[k], s1[x], qA[k], s2[x]);
+    r.q = make_uint4(qB[k], s1[y], pos2[k], s2[y]);
+    r.c = make_uint4(x, y, fill[x], fill[y]);
+    it[k] = r;
+  }
+}
+
+// a_of1[p] = a of the item at a-order position p; b_of2[p] = b of the item
+// at b-order position p, or kNoB when that item's blocks coincide (its
+// choice counts as an a choice)
+__global__ void k_route_orders(const uint32_t *__restrict__ a, const uint32_t *__restrict__ b,
+                               const uint32_t *__restrict__ perm1, const uint32_t *__restrict__ perm2, int64_t m,
+                               uint32_t *__restrict__ a_of1, uint32_t *__restrict__ b_of2) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < m; p += (int64_t)gridDim.x * blockDim.x) {
+    a_of1[p] = a[perm1[p]];
+    const uint32_t i = perm2[p];
+    b_of2[p] = a[i] == b[i] ? kNoB : b[i];
   }
 }
 
@@ -1113,9 +1238,9 @@ int route_items(Scratch &S, const uint32_t *a, const uint32_t *b, int64_t m, con
     uint32_t *P1 = S.get<uint32_t>(m + 1), *P2 = S.get<uint32_t>(m + 1);
     const int T = (int)((m + kJTile - 1) / kJTile);
     uint32_t *ts = S.get<uint32_t>((size_t)4 * T);
-    unsigned *ctl = S.get<unsigned>(8);
+    unsigned *ctl = S.get<unsigned>(8), *chg = S.get<unsigned>(4096);
     FK_P(perm1); FK_P(perm2); FK_P(pos1); FK_P(pos2); FK_P(qA); FK_P(qB); FK_P(iota); FK_P(bs);
-    FK_P(s1); FK_P(e1); FK_P(s2); FK_P(e2); FK_P(P1); FK_P(P2); FK_P(ts); FK_P(ctl);
+    FK_P(s1); FK_P(e1); FK_P(s2); FK_P(e2); FK_P(P1); FK_P(P2); FK_P(ts); FK_P(ctl); FK_P(chg);
     if (!a_sorted) FK_P(as);
     k_iota_u32<<<grid_for(m), 256, 0, st>>>(iota, m);
     FK_CHECK_LAUNCH();
@@ -1141,16 +1266,40 @@ int route_items(Scratch &S, const uint32_t *a, const uint32_t *b, int64_t m, con
     k_seg_rank<<<grid_for(m), 256, 0, st>>>(a, perm2, s2, e2, m, qA);
     k_seg_rank<<<grid_for(m), 256, 0, st>>>(b, perm1, s1, e1, m, qB);
     FK_CHECK_LAUNCH();
-    RouteJ R{a, b, fill, perm1, perm2, pos1, pos2, qA, qB, s1, s2, dest, P1, P2, ts, ctl, m, T, B};
+    RouteItem *items = S.get<RouteItem>(m);
+    uint32_t *a_of1 = S.get<uint32_t>(m), *b_of2 = S.get<uint32_t>(m);
+    FK_P(items); FK_P(a_of1); FK_P(b_of2);
+    k_route_items<<<grid_for(m), 256, 0, st>>>(a, b, fill, pos1, pos2, qA, qB, s1, s2, m, items);
+    k_route_orders<<<grid_for(m), 256, 0, st>>>(a, b, perm1, perm2, m, a_of1, b_of2);
+    FK_CHECK_LAUNCH();
+    const bool stats = getenv("FK_ROUTE_STATS") != nullptr;
+    unsigned long long *clk = stats ? S.get<unsigned long long>(1 + 4 * 64) : nullptr;
+    if (stats) FK_S(cudaMemsetAsync(clk, 0, 8 * (1 + 4 * 64), st));
+    RouteJ R{items, perm1, perm2, a_of1, b_of2, pos1, pos2, dest, P1, P2, ts, ctl, chg, clk, m, T, B};
     int grid = coop_grid((const void *)k_btcf_route_jacobi, kJT);
     if (!grid) return FK_E_ARG;
-    if (T < grid) grid = T;
+    const int64_t want = (m + kJT - 1) / kJT;
+    if (want < grid) grid = (int)(want < T ? T : want);
+    if (grid > 4096) grid = 4096;
     void *args[] = {(void *)&R};
     FK_S(cudaLaunchCooperativeKernel((const void *)k_btcf_route_jacobi, dim3(grid), dim3(kJT), args, 0, st));
     unsigned h[2] = {0, 0};
     FK_S(cudaMemcpyAsync(h, ctl + 3, 8, cudaMemcpyDeviceToHost, st));
     FK_S(cudaStreamSynchronize(st));
-    if (getenv("FK_ROUTE_STATS")) fprintf(stderr, "fk route: m=%lld sweeps=%u converged=%u\n", (long long)m, h[0], h[1]);
+    if (stats) {
+      unsigned long long hc[1 + 4 * 64];
+      FK_S(cudaMemcpy(hc, clk, sizeof(hc), cudaMemcpyDeviceToHost));
+      double s_work = 0, s_bar = 0, d_all = 0, d_max = 0;
+      const unsigned ns = h[0] < 64 ? h[0] : 64;
+      for (unsigned i = 0; i < ns; i++) {
+        s_work += (double)(hc[1 + 3 * i] - (i ? hc[3 * i] : hc[0]));
+        s_bar += (double)(hc[2 + 3 * i] - hc[1 + 3 * i]);
+        d_all += (double)(hc[3 + 3 * i] - hc[2 + 3 * i]);
+        d_max += (double)(hc[1 + 3 * 64 + i] - hc[2 + 3 * i]);
+      }
+      fprintf(stderr, "fk route: m=%lld sweeps=%u converged=%u grid=%d  per sweep (us, CTA 0): S work %.2f, S barrier %.2f, D work+barrier %.2f (slowest CTA's D work %.2f)\n",
+              (long long)m, h[0], h[1], grid, s_work / ns / 1e3, s_bar / ns / 1e3, d_all / ns / 1e3, d_max / ns / 1e3);
+    }
     if (h[1]) return 0;
     // not converged: fall through to the sequential walk
   }
