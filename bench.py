@@ -1077,6 +1077,10 @@ def main():
             dev_idx = local_rank % torch.cuda.device_count()
             torch.cuda.set_device(dev_idx)
             if backend == "nccl":
+                # communicator init on stderr (comm / rank / nranks / transports) so the
+                # scaling run's NCCL setup can be checked from the log
+                os.environ.setdefault("NCCL_DEBUG", "INFO")
+                os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
                 dist.init_process_group("nccl", device_id=torch.device("cuda", dev_idx))
             else:
                 dist.init_process_group(backend)

@@ -338,19 +338,31 @@ int fk_shard_unpermute(const uint32_t *perm, const void *src, int64_t n, int ele
 
 /* Fused exchange over peer memory (CUDA IPC mappings; NVLink / NVSwitch
  * stores between GPUs) -- the data path of the sharded filters without a
- * collective library.  fk_shard_partition with keys_out = NULL only computes
- * perm and counts; fk_shard_dispatch then writes key perm[i] of owner o
- * straight into peer_keys[o][dst_off[o] + i - seg_start[o]] (and its value,
- * and the tag (rank << 32) | input index into peer_src[o]); after the
- * owners ran their local op, fk_shard_combine writes each result into
- * peer_out[tag >> 32][tag & 0xffffffff].  Pointer arrays are DEVICE arrays
- * of G entries.  Replaces the all-to-all exchange of SURVEY 8(e). */
+ * collective library.  Pointer arrays are DEVICE arrays of G = 2^log2_shards
+ * entries; offset arrays are device int64.  Replaces the all-to-all exchange
+ * of SURVEY 8(e).
+ *
+ * fk_shard_partition with keys_out = NULL computes perm and counts only;
+ * fk_shard_dispatch writes key perm[i] of owner o (8 bytes, and its 64-bit
+ * value if vals) to peer_keys[o][dst_off[o] + i - seg_start[o]].  Every owner's
+ * receive buffer thus holds the sources in rank order, each in its input
+ * order, so a key's source and position follow from its offset.
+ * fk_shard_combine (owner side): received item j of source s (recv_off[s] <=
+ * j < recv_off[s+1], recv_off has G+1 entries) sends its result to
+ * peer_back[s][back_off[s] + j - recv_off[s]] -- the key's position in the
+ * source's owner-grouped order (one contiguous run per owner); the source
+ * restores input order with fk_shard_unpermute.
+ * fk_shard_signal: after the stream's prior work, stores epoch into
+ * peer_flags[o][rank] for every o (system-scope release);
+ * fk_shard_wait: the stream waits until flags[s] >= epoch for all s
+ * (acquire), trapping after timeout_s instead of hanging.  All asynchronous. */
 int fk_shard_dispatch(const uint64_t *keys, const uint64_t *vals, const uint32_t *perm, int64_t n, uint64_t seed,
-                      int shift, int log2_shards, uint32_t rank, const int64_t *seg_start, const int64_t *dst_off,
-                      uint64_t *const *peer_keys, uint64_t *const *peer_vals, uint64_t *const *peer_src,
-                      void *stream);
-int fk_shard_combine(const uint64_t *src, const void *res, int64_t m, int elem_bytes, void *const *peer_out,
-                     void *stream);
+                      int shift, int log2_shards, const int64_t *seg_start, const int64_t *dst_off,
+                      uint64_t *const *peer_keys, uint64_t *const *peer_vals, void *stream);
+int fk_shard_combine(const void *res, int64_t m, int elem_bytes, int log2_shards, const int64_t *recv_off,
+                     const int64_t *back_off, void *const *peer_back, void *stream);
+int fk_shard_signal(uint32_t *const *peer_flags, int log2_shards, uint32_t rank, uint32_t epoch, void *stream);
+int fk_shard_wait(const uint32_t *flags, int log2_shards, uint32_t epoch, double timeout_s, void *stream);
 
 /* Whole-allocation device buffers shareable with the other ranks through
  * CUDA IPC (handles are 64 bytes; open the other ranks' handles, not your own). */

@@ -89,9 +89,10 @@ _SIGS = {
                                         c_vp]),
     "fk_shard_partition": (c_i32, [c_vp, c_vp, c_i64, c_u64, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "fk_shard_unpermute": (c_i32, [c_vp, c_vp, c_i64, c_i32, c_vp, c_vp]),
-    "fk_shard_dispatch": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_u64, c_i32, c_i32, ctypes.c_uint32, c_vp, c_vp, c_vp,
-                                  c_vp, c_vp, c_vp]),
-    "fk_shard_combine": (c_i32, [c_vp, c_vp, c_i64, c_i32, c_vp, c_vp]),
+    "fk_shard_dispatch": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_u64, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "fk_shard_combine": (c_i32, [c_vp, c_i64, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp]),
+    "fk_shard_signal": (c_i32, [c_vp, c_i32, ctypes.c_uint32, ctypes.c_uint32, c_vp]),
+    "fk_shard_wait": (c_i32, [c_vp, c_i32, ctypes.c_uint32, ctypes.c_double, c_vp]),
     "fk_ipc_alloc": (c_i32, [c_i64, ctypes.POINTER(c_vp)]),
     "fk_ipc_free": (c_i32, [c_vp]),
     "fk_ipc_get_handle": (c_i32, [c_vp, c_vp]),

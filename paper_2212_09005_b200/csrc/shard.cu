@@ -10,9 +10,10 @@
 //
 // fk_shard_partition stably groups a batch by owner (one-digit CUB radix
 // sort of the owner ids, then a gather of keys and optional 64-bit values)
-// and counts per owner; the caller exchanges the groups with one NCCL
-// all-to-all.  fk_shard_unpermute_* scatter the per-key results that come
-// back into input order.
+// and counts per owner; the caller exchanges the groups either over peer
+// memory (fk_shard_dispatch / fk_shard_combine / fk_shard_signal /
+// fk_shard_wait, below) or with one NCCL all-to-all.  fk_shard_unpermute
+// scatters the per-key results that come back into input order.
 #include <cub/cub.cuh>
 #include <string.h>
 
@@ -66,16 +67,24 @@ __global__ void k_unpermute(const uint32_t *__restrict__ perm, const T *__restri
 }
 
 // Fused exchange over peer memory (CUDA IPC mappings of the other ranks'
-// buffers; NVLink / NVSwitch stores between GPUs).  dispatch: the gather of
-// the stable owner partition writes every key straight into its owner's
-// receive buffer, at this rank's offset there, with a (rank, input index)
-// tag; combine: the owner writes each per-key result straight into the
-// source rank's output array at the key's input index.
+// buffers; NVLink / NVSwitch stores between GPUs).
+//   dispatch: the gather of the stable owner partition writes every key (8 B,
+//     plus its value if any) straight into its owner's receive buffer, at this
+//     rank's offset there.  The receive layout -- sources in rank order, each
+//     source's keys in its input order -- identifies every key's source and
+//     position, so no tag travels with it.
+//   combine: the owner writes each received key's result straight into its
+//     source's return buffer, at the key's position in the source's
+//     owner-grouped order: one contiguous run per (owner, source) pair; the
+//     source restores its input order locally (fk_shard_unpermute).
+//   signal / wait: stream-ordered cross-GPU handoff -- after the exchange
+//     kernel, every rank stores an epoch into every peer's flag word for it
+//     (system-scope release); the receiving stream spins (acquire) until all
+//     sources reached the epoch.  No host synchronisation.
 __global__ void k_dispatch(const uint64_t *__restrict__ keys, const uint64_t *__restrict__ vals,
                            const uint32_t *__restrict__ perm, int64_t n, uint64_t seed, int shift, uint32_t gmask,
                            const int64_t *__restrict__ seg_start, const int64_t *__restrict__ dst_off,
-                           uint64_t *const *__restrict__ pk, uint64_t *const *__restrict__ pv,
-                           uint64_t *const *__restrict__ ps, uint32_t rank) {
+                           uint64_t *const *__restrict__ pk, uint64_t *const *__restrict__ pv) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t p = perm[i];
     const uint64_t k = keys[p];
@@ -83,16 +92,46 @@ __global__ void k_dispatch(const uint64_t *__restrict__ keys, const uint64_t *__
     const int64_t j = dst_off[o] + (i - seg_start[o]);
     pk[o][j] = k;
     if (vals) pv[o][j] = vals[p];
-    ps[o][j] = ((uint64_t)rank << 32) | p;
   }
+  __threadfence_system();
 }
 
 template <typename T>
-__global__ void k_combine(const uint64_t *__restrict__ src, const T *__restrict__ res, int64_t m,
-                          T *const *__restrict__ pout) {
+__global__ void k_combine(const T *__restrict__ res, int64_t m, int G, const int64_t *__restrict__ recv_off,
+                          const int64_t *__restrict__ back_off, T *const *__restrict__ pback) {
+  __shared__ int64_t s_off[257], s_back[256];
+  for (int s = threadIdx.x; s <= G; s += blockDim.x) {
+    s_off[s] = recv_off[s];
+    if (s < G) s_back[s] = back_off[s];
+  }
+  __syncthreads();
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t t = src[j];
-    pout[t >> 32][(uint32_t)t] = res[j];
+    int s = 0;
+    while (s + 1 < G && j >= s_off[s + 1]) s++;
+    pback[s][s_back[s] + (j - s_off[s])] = res[j];
+  }
+  __threadfence_system();
+}
+
+__global__ void k_signal(uint32_t *const *__restrict__ pflags, int G, uint32_t rank, uint32_t epoch) {
+  const int o = threadIdx.x;
+  if (o >= G) return;
+  __threadfence_system();
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(pflags[o] + rank), "r"(epoch) : "memory");
+}
+
+__global__ void k_wait(const uint32_t *__restrict__ flags, int G, uint32_t epoch, unsigned long long timeout_ns) {
+  const int s = threadIdx.x;
+  if (s >= G) return;
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + s) : "memory");
+    if ((int32_t)(v - epoch) >= 0) break;
+    __nanosleep(256);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > timeout_ns) __trap();  // a peer never arrived: fail loudly instead of hanging
   }
 }
 
@@ -135,30 +174,48 @@ int fk_shard_partition(const uint64_t *keys, const uint64_t *vals, int64_t n, ui
 }
 
 int fk_shard_dispatch(const uint64_t *keys, const uint64_t *vals, const uint32_t *perm, int64_t n, uint64_t seed,
-                      int shift, int log2_shards, uint32_t rank, const int64_t *seg_start, const int64_t *dst_off,
-                      uint64_t *const *peer_keys, uint64_t *const *peer_vals, uint64_t *const *peer_src,
-                      void *stream) {
-  if (n < 0 || log2_shards < 0 || log2_shards > 8 || !peer_keys || !peer_src || (vals && !peer_vals)) return FK_E_ARG;
+                      int shift, int log2_shards, const int64_t *seg_start, const int64_t *dst_off,
+                      uint64_t *const *peer_keys, uint64_t *const *peer_vals, void *stream) {
+  if (n < 0 || log2_shards < 0 || log2_shards > 8 || !peer_keys || (vals && !peer_vals)) return FK_E_ARG;
   if (n == 0) return 0;
   const int sh = log2_shards == 0 ? 64 : shift;
   k_dispatch<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(keys, vals, perm, n, seed, sh,
                                                             (uint32_t)((1 << log2_shards) - 1), seg_start, dst_off,
-                                                            peer_keys, peer_vals, peer_src, rank);
+                                                            peer_keys, peer_vals);
   FK_CHECK_LAUNCH();
   return 0;
 }
 
-int fk_shard_combine(const uint64_t *src, const void *res, int64_t m, int elem_bytes, void *const *peer_out,
-                     void *stream) {
-  if (m < 0 || !peer_out) return FK_E_ARG;
+int fk_shard_combine(const void *res, int64_t m, int elem_bytes, int log2_shards, const int64_t *recv_off,
+                     const int64_t *back_off, void *const *peer_back, void *stream) {
+  if (m < 0 || log2_shards < 0 || log2_shards > 8 || !peer_back || !recv_off || !back_off) return FK_E_ARG;
   if (m == 0) return 0;
   cudaStream_t st = (cudaStream_t)stream;
+  const int G = 1 << log2_shards;
   if (elem_bytes == 1)
-    k_combine<uint8_t><<<grid_for(m), 256, 0, st>>>(src, (const uint8_t *)res, m, (uint8_t *const *)peer_out);
+    k_combine<uint8_t><<<grid_for(m), 256, 0, st>>>((const uint8_t *)res, m, G, recv_off, back_off,
+                                                    (uint8_t *const *)peer_back);
   else if (elem_bytes == 8)
-    k_combine<uint64_t><<<grid_for(m), 256, 0, st>>>(src, (const uint64_t *)res, m, (uint64_t *const *)peer_out);
+    k_combine<uint64_t><<<grid_for(m), 256, 0, st>>>((const uint64_t *)res, m, G, recv_off, back_off,
+                                                     (uint64_t *const *)peer_back);
   else
     return FK_E_ARG;
+  FK_CHECK_LAUNCH();
+  return 0;
+}
+
+int fk_shard_signal(uint32_t *const *peer_flags, int log2_shards, uint32_t rank, uint32_t epoch, void *stream) {
+  if (!peer_flags || log2_shards < 0 || log2_shards > 8) return FK_E_ARG;
+  const int G = 1 << log2_shards;
+  k_signal<<<1, G < 32 ? 32 : G, 0, (cudaStream_t)stream>>>(peer_flags, G, rank, epoch);
+  FK_CHECK_LAUNCH();
+  return 0;
+}
+
+int fk_shard_wait(const uint32_t *flags, int log2_shards, uint32_t epoch, double timeout_s, void *stream) {
+  if (!flags || log2_shards < 0 || log2_shards > 8 || timeout_s <= 0) return FK_E_ARG;
+  const int G = 1 << log2_shards;
+  k_wait<<<1, G < 32 ? 32 : G, 0, (cudaStream_t)stream>>>(flags, G, epoch, (unsigned long long)(timeout_s * 1e9));
   FK_CHECK_LAUNCH();
   return 0;
 }

@@ -3,11 +3,12 @@
 The reference is a single-process package; this is the new build's scale-out
 path.  Each rank owns an independent sub-filter and every batch
 call is: partition the rank's keys by owner (fk_shard_partition, a stable
-device partition on a fingerprint prefix) -> one NCCL all-to-all of the keys
-(after a G-int count exchange) -> the local sub-filter kernel on what arrived,
-in (source rank, input index) order -> the reverse all-to-all of the per-key
-results -> fk_shard_unpermute back to input order.  There is no other
-data-path collective.
+device partition on a fingerprint prefix) -> an all-gather of the G per-owner
+counts -> the keys move to their owners (by default the peer-memory dispatch
+kernel, NVLink stores into the owners' buffers; FK_SHARD_PEER=0: one NCCL
+all-to-all) -> the local sub-filter kernel on what arrived, in (source rank,
+input index) order -> the per-key results move back (peer-memory combine or
+the reverse all-to-all) -> fk_shard_unpermute back to input order.
 
 * TCF: owner = top log2(G) bits of mix64(key ^ seed).  b1, b2, the tag and the
   backing schedule come from other hash streams, so shard s is exactly a
@@ -16,9 +17,9 @@ data-path collective.
   ``Gqf(q - log2 G, r)`` sees the low q' + r fingerprint bits, so its counts
   (and every answer) equal a single global ``Gqf(q, r)``'s.
 
-``world`` must be a power of two (1, 2, 4, 8).  The exchange uses
-``torch.distributed.all_to_all_single`` on the group's backend (NCCL over
-NVLink on the B200 box).  ``_Router`` takes its partition / unpermute ops as
+``world`` must be a power of two (1, 2, 4, 8).  ``_Router`` (the all-to-all
+fallback) uses ``torch.distributed.all_to_all_single`` on the group's backend
+(NCCL over NVLink on the B200 box).  ``_Router`` takes its partition / unpermute ops as
 an object so that the exchange logic can be exercised with world_size-2
 gloo on CPU (tests/test_sharding_cpu.py); the product ops are the CUDA
 kernels and refuse non-CUDA tensors.
@@ -159,10 +160,14 @@ class _Router:
 
 class _PeerBuffers:
     """Device buffers every rank can store into: allocated whole (cudaMalloc)
-    so a CUDA IPC handle covers them, handles exchanged once per growth, the
-    other ranks' buffers opened into this process (NVLink peer mappings)."""
+    so a CUDA IPC handle covers them, the other ranks' buffers opened into
+    this process (NVLink peer mappings).  Capacities grow by a decision every
+    rank makes identically from the all-gathered count matrix, so sizing needs
+    no extra collective; handles are exchanged only when they grow.  The flag
+    words of the stream-ordered handoff (one u32 per source rank) are
+    allocated once and never move."""
 
-    NAMES = ("keys", "vals", "src", "out")
+    NAMES = ("keys", "vals", "back")
 
     def __init__(self, torch, group, world, rank):
         self.torch, self.group, self.world, self.rank = torch, group, world, rank
@@ -172,38 +177,35 @@ class _PeerBuffers:
         self.peers = {}   # name -> [pointer of rank r's buffer] (own included)
         self.tables = {}  # name -> int64 CUDA tensor of the pointers (kernel argument)
 
-    def _free(self):
-        for name in self.NAMES:
+    def _close_peers(self, names):
+        for name in names:
             for r, ptr in enumerate(self.peers.get(name, [])):
                 if r != self.rank and ptr:
                     self.lib.fk_ipc_close(ctypes.c_void_p(ptr))
-            if self.local.get(name):
-                self.lib.fk_ipc_free(ctypes.c_void_p(self.local[name]))
-        self.local, self.peers, self.tables = {}, {}, {}
+            self.peers.pop(name, None)
+            self.tables.pop(name, None)
 
-    def ensure(self, need):
-        """Collective: every rank calls it with its own need (items)."""
+    def _free_local(self, names):
+        for name in names:
+            if self.local.get(name):
+                self.lib.fk_ipc_free(ctypes.c_void_p(self.local.pop(name)))
+
+    def _exchange(self, names, nbytes):
+        """Allocate `names` (nbytes each), exchange handles, map the peers'."""
         import torch.distributed as dist
         torch = self.torch
-        objs = [None] * self.world
-        dist.all_gather_object(objs, int(need), group=self.group)
-        want = max(objs)
-        if want <= self.cap:
-            return
-        cap = max(want, 2 * self.cap, 1 << 16)
-        self._free()
         handles = {}
-        for name in self.NAMES:
+        for name in names:
             ptr = ctypes.c_void_p()
-            _lib.check(self.lib.fk_ipc_alloc(cap * 8, ctypes.byref(ptr)), "ipc alloc")
+            _lib.check(self.lib.fk_ipc_alloc(nbytes, ctypes.byref(ptr)), "ipc alloc")
             self.local[name] = ptr.value
             h = ctypes.create_string_buffer(64)
             _lib.check(self.lib.fk_ipc_get_handle(ptr, h), "ipc handle")
             handles[name] = h.raw
         everyone = [None] * self.world
-        dist.all_gather_object(everyone, handles, group=self.group)
+        dist.all_gather_object(everyone, handles, group=self.group)  # once per growth, not per batch
         ok = True
-        for name in self.NAMES:
+        for name in names:
             ptrs = []
             for r in range(self.world):
                 if r == self.rank:
@@ -216,13 +218,39 @@ class _PeerBuffers:
                 ptrs.append(out.value or 0)
             self.peers[name] = ptrs
             self.tables[name] = torch.tensor(ptrs, dtype=torch.int64, device="cuda")
-        # every rank must be able to reach every other one, or nobody uses it
-        oks = [None] * self.world
+        oks = [None] * self.world  # every rank must reach every other one, or nobody uses it
         dist.all_gather_object(oks, ok, group=self.group)
-        if not all(oks):
-            self._free()
+        return all(oks)
+
+    def ensure(self, want):
+        """Every rank calls it with the same `want` (items)."""
+        import torch.distributed as dist
+        if want <= self.cap:
+            return
+        cap = max(int(want), 2 * self.cap, 1 << 16)
+        first = self.cap == 0
+        if not first:
+            # unmap the peers' old buffers everywhere before anyone frees its own
+            self._close_peers(self.NAMES)
+            dist.barrier(group=self.group)
+            self._free_local(self.NAMES)
+        ok = self._exchange(self.NAMES, cap * 8)
+        if first and ok:
+            ok = self._exchange(("flags",), 4 * self.world)
+            if ok:
+                self.view("flags", self.world, self.torch.int32).zero_()
+                self.torch.cuda.current_stream().synchronize()
+                dist.barrier(group=self.group)  # flags are zero before any peer signals
+        if not ok:
+            self.release()
             raise _NoPeerAccess()
         self.cap = cap
+
+    def release(self):
+        names = self.NAMES + ("flags",)
+        self._close_peers(names)
+        self._free_local(names)
+        self.cap = 0
 
     def view(self, name, n, dtype):
         """This rank's own buffer `name` as a CUDA tensor of n items of dtype."""
@@ -230,7 +258,7 @@ class _PeerBuffers:
 
     def __del__(self):
         try:
-            self._free()
+            self.release()
         except Exception:
             pass
 
@@ -247,18 +275,40 @@ class _DevView:
         itemsize = torch.empty(0, dtype=dtype).element_size()
 
         class _Iface:
-            __cuda_array_interface__ = {"shape": (int(n),), "typestr": {1: "|u1", 8: "<i8"}[itemsize],
+            __cuda_array_interface__ = {"shape": (int(n),), "typestr": {1: "|u1", 4: "<i4", 8: "<i8"}[itemsize],
                                         "data": (int(ptr), False), "version": 3}
         t = torch.as_tensor(_Iface(), device="cuda")
         return t.view(dtype) if t.dtype != dtype else t
 
 
+def exchange_plan(C, me):
+    """Offsets of the peer exchange from the all-gathered count matrix
+    C[source][owner] (int64 numpy), as rank `me` needs them: seg_start[o] (my
+    owner-o group in my partitioned order), dst_off[o] (where it lands in
+    owner o's receive buffer: after the earlier sources' groups), recv_off[s]
+    (source s's run in my receive buffer, G+1 entries), back_off[s] (where my
+    results for source s land in its partitioned order), and the buffer
+    capacity every rank derives identically."""
+    C = np.asarray(C, dtype=np.int64)
+    G = C.shape[0]
+    seg_start = np.concatenate(([0], np.cumsum(C[me])[:-1]))
+    dst_off = (np.cumsum(C, axis=0) - C)[me]
+    recv_off = np.concatenate(([0], np.cumsum(C[:, me])))
+    back_off = (np.cumsum(C, axis=1) - C)[:, me]
+    want = int(max(C.sum(axis=0).max(), C.sum(axis=1).max())) if G else 0
+    return seg_start, dst_off, recv_off, back_off, want
+
+
 class _PeerRouter(_Router):
     """Owner routing through peer memory instead of an all-to-all: the
-    dispatch kernel stores every key into its owner's receive buffer, the
-    combine kernel stores every result into its source rank's output buffer
-    (fk_shard_dispatch / fk_shard_combine).  Only per-owner counts (G ints)
-    and a barrier per direction go through torch.distributed."""
+    dispatch kernel stores every key (8 bytes) into its owner's receive
+    buffer, the combine kernel stores every result into its source's return
+    buffer in the source's owner-grouped order, and stream-ordered flag
+    kernels hand the buffers over between GPUs.  Per batch: one all-gather of
+    the G per-owner counts (a tensor collective) and one host synchronisation
+    (to read them); no barriers."""
+
+    WAIT_TIMEOUT_S = 120.0
 
     def __init__(self, torch, group, world, seed, shift, ops):
         super().__init__(torch, group, world, seed, shift, ops)
@@ -266,11 +316,17 @@ class _PeerRouter(_Router):
         self.rank = dist.get_rank(group)
         self.bufs = _PeerBuffers(torch, group, world, self.rank)
         self.fallback = False  # set collectively if peer mappings are unavailable
+        self.epoch = 0
 
-    def _barrier(self):
-        import torch.distributed as dist
-        self.torch.cuda.current_stream().synchronize()
-        dist.barrier(group=self.group)
+    def _handoff(self):
+        """Stream-ordered: signal every peer that this rank's exchange stores
+        are done, then wait until every peer signalled the same epoch."""
+        self.epoch = (self.epoch + 1) & 0xFFFFFFFF
+        lib, sp = self.ops.lib, _lib.stream_ptr(self.torch)
+        _lib.check(lib.fk_shard_signal(_lib.dptr(self.bufs.tables["flags"]), self.log2g, self.rank, self.epoch, sp),
+                   "shard signal")
+        _lib.check(lib.fk_shard_wait(ctypes.c_void_p(self.bufs.local["flags"]), self.log2g, self.epoch,
+                                     self.WAIT_TIMEOUT_S, sp), "shard wait")
 
     def route(self, keys, vals=None):
         torch = self.torch
@@ -283,30 +339,29 @@ class _PeerRouter(_Router):
         c = counts.to(self._coll_device())
         allc = [torch.empty_like(c) for _ in range(self.world)]
         dist.all_gather(allc, c, group=self.group)
-        C = np.array([a.tolist() for a in allc], dtype=np.int64)  # C[source][owner]
+        C = torch.stack(allc).cpu().numpy()  # the batch's one host synchronisation
         me = self.rank
-        recv_n = int(C[:, me].sum())
+        seg_start, dst_off, recv_off, back_off, want = exchange_plan(C, me)
         try:
-            self.bufs.ensure(max(recv_n, keys.numel()))
+            self.bufs.ensure(want)
         except _NoPeerAccess:  # collective decision: every rank falls back together
             self.fallback = True
             return super().route(keys, vals)
-        seg_start = np.concatenate(([0], np.cumsum(C[me])[:-1]))
-        dst_off = np.cumsum(C, axis=0) - C  # rows above: earlier source ranks
-        dev = keys.device
-        ss = torch.tensor(seg_start, dtype=torch.int64, device=dev)
-        do = torch.tensor(dst_off[me], dtype=torch.int64, device=dev)
+        recv_n = int(recv_off[-1])
+        offs = torch.tensor(np.concatenate([seg_start, dst_off, recv_off, back_off]), dtype=torch.int64,
+                            device=keys.device)
+        G = self.world
+        ss, do, ro, bo = offs[:G], offs[G:2 * G], offs[2 * G:3 * G + 1], offs[3 * G + 1:]
         t = self.bufs.tables
-        lib = self.ops.lib
-        _lib.check(lib.fk_shard_dispatch(_lib.dptr(keys), _lib.dptr(vals), _lib.dptr(perm), keys.numel(),
-                                         self.seed & ((1 << 64) - 1), self.shift, self.log2g, me, _lib.dptr(ss),
-                                         _lib.dptr(do), _lib.dptr(t["keys"]),
-                                         _lib.dptr(t["vals"]) if vals is not None else None, _lib.dptr(t["src"]),
-                                         _lib.stream_ptr(torch)), "shard dispatch")
-        self._barrier()  # every rank's keys have landed in its owners' buffers
+        _lib.check(self.ops.lib.fk_shard_dispatch(_lib.dptr(keys), _lib.dptr(vals), _lib.dptr(perm), keys.numel(),
+                                                  self.seed & ((1 << 64) - 1), self.shift, self.log2g, _lib.dptr(ss),
+                                                  _lib.dptr(do), _lib.dptr(t["keys"]),
+                                                  _lib.dptr(t["vals"]) if vals is not None else None,
+                                                  _lib.stream_ptr(torch)), "shard dispatch")
+        self._handoff()  # every source's keys have landed in this rank's receive buffer
         rk = self.bufs.view("keys", recv_n, torch.int64)
         rv = self.bufs.view("vals", recv_n, torch.int64) if vals is not None else None
-        return rk, rv, (keys.numel(), recv_n)
+        return rk, rv, (perm, keys.numel(), recv_n, ro, bo)
 
     def unroute(self, res, plan):
         if plan is None:
@@ -314,15 +369,33 @@ class _PeerRouter(_Router):
         if self.fallback:
             return super().unroute(res, plan)
         torch = self.torch
-        n, recv_n = plan
+        perm, n, recv_n, ro, bo = plan
         res = res.contiguous()
-        eb = res.element_size()
-        src = self.bufs.view("src", recv_n, torch.int64)
-        _lib.check(self.ops.lib.fk_shard_combine(_lib.dptr(src), _lib.dptr(res), recv_n, eb,
-                                                 _lib.dptr(self.bufs.tables["out"]), _lib.stream_ptr(torch)),
-                   "shard combine")
-        self._barrier()  # every owner has stored this rank's results
-        return self.bufs.view("out", n, res.dtype).clone()
+        _lib.check(self.ops.lib.fk_shard_combine(_lib.dptr(res), recv_n, res.element_size(), self.log2g,
+                                                 _lib.dptr(ro), _lib.dptr(bo), _lib.dptr(self.bufs.tables["back"]),
+                                                 _lib.stream_ptr(torch)), "shard combine")
+        self._handoff()  # every owner has stored this rank's results
+        return self.ops.unpermute(perm, self.bufs.view("back", n, res.dtype))
+
+
+def failed_flags(torch, keys, failed):
+    """Per-item failure flags (u8) for a batch whose failed keys came back as
+    a multiset of values: a key that failed m times flags its LAST m copies
+    (the local insert places the earlier copies of equal keys first), so
+    duplicates where only some copies failed are not all reported."""
+    flag = torch.zeros(keys.numel(), dtype=torch.uint8, device=keys.device)
+    if failed.numel() == 0 or keys.numel() == 0:
+        return flag
+    uf, fcnt = torch.unique(failed, return_counts=True)
+    order = torch.argsort(keys, stable=True)
+    ks = keys[order]
+    _, inv, gcnt = torch.unique_consecutive(ks, return_inverse=True, return_counts=True)
+    gend = torch.cumsum(gcnt, 0)[inv]                      # one past each item's group end
+    from_end = gend - 1 - torch.arange(ks.numel(), device=keys.device)
+    pos = torch.searchsorted(uf, ks).clamp(max=uf.numel() - 1)
+    m = torch.where(uf[pos] == ks, fcnt[pos], torch.zeros_like(fcnt[pos]))
+    flag[order] = (from_end < m).to(torch.uint8)
+    return flag
 
 
 def _make_router(torch, group, world, seed, shift, ops):
@@ -445,8 +518,7 @@ class ShardedBulkTcf(_Sharded):
         k, kind = self._keys(keys)
         rk, _, plan = self._router.route(k)
         failed = self._local.insert_batch(rk)
-        flag = torch.isin(rk, failed).to(torch.uint8) if failed.numel() else \
-            torch.zeros(rk.numel(), dtype=torch.uint8, device=rk.device)
+        flag = failed_flags(torch, rk, failed)
         mine = self._router.unroute(flag, plan).bool()
         out = k[mine]
         return out if kind == "cuda" else out.cpu().numpy().view(np.uint64)

@@ -150,3 +150,56 @@ def test_gqf_sharded_counts_equal_global(results, oracle):
     assert code == 0
     for r in range(world):
         assert np.array_equal(results[r]["gqf_counts"], g.count_many(results[r]["gqf_keys"]))
+
+
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_peer_exchange_plan_round_trip(G):
+    """The peer-memory exchange's offsets (exchange_plan), played through in
+    numpy exactly as the kernels address memory: dispatch stores key i of
+    owner o at dst_off[o] + i - seg_start[o] of o's receive buffer, combine
+    stores received item j of source s at back_off[s] + j - recv_off[s] of
+    s's return buffer, the source unpermutes.  Every owner receives each
+    source's keys in (source rank, input order) with no tag, and every
+    source gets each key's answer back at its input position."""
+    from paper_2212_09005_b200.sharding import exchange_plan
+    rng = np.random.default_rng(G)
+    n = [int(rng.integers(0, 300)) for _ in range(G)]
+    n[0] = 0  # an empty batch still takes part
+    keys = [rng.integers(0, 1 << 62, n[r]).astype(np.int64) for r in range(G)]
+    owner = [(k * 2654435761 >> 7) % G for k in keys]
+    perm = [np.argsort(o, kind="stable") for o in owner]
+    C = np.array([np.bincount(owner[r], minlength=G) for r in range(G)], dtype=np.int64)
+    plans = [exchange_plan(C, r) for r in range(G)]
+    assert len({p[4] for p in plans}) == 1  # every rank sizes the buffers the same way
+    cap = plans[0][4]
+    recv = [np.full(cap, -1, np.int64) for _ in range(G)]
+    for r in range(G):  # dispatch
+        ss, do = plans[r][0], plans[r][1]
+        for i, p in enumerate(perm[r]):
+            o = owner[r][p]
+            recv[o][do[o] + i - ss[o]] = keys[r][p]
+    for o in range(G):  # owners see (source rank, input order)
+        ro = plans[o][2]
+        expect = np.concatenate([keys[s][owner[s] == o] for s in range(G)]) if C[:, o].sum() else np.zeros(0)
+        assert np.array_equal(recv[o][:ro[-1]], expect)
+    back = [np.full(cap, -1, np.int64) for _ in range(G)]
+    for o in range(G):  # combine: the answer is the key itself, doubled
+        ro, bo = plans[o][2], plans[o][3]
+        for j in range(ro[-1]):
+            s = int(np.searchsorted(ro, j, side="right") - 1)
+            back[s][bo[s] + j - ro[s]] = 2 * recv[o][j]
+    for r in range(G):  # unpermute
+        out = np.empty(n[r], np.int64)
+        out[perm[r]] = back[r][:n[r]]
+        assert np.array_equal(out, 2 * keys[r])
+
+
+def test_failed_flags_counts_duplicates():
+    """Sharded bulk insert: a key that failed m times flags its last m copies
+    only (not every copy, as a membership test would)."""
+    from paper_2212_09005_b200.sharding import failed_flags
+    keys = torch.tensor([5, 7, 5, 9, 5, 7, 11], dtype=torch.int64)
+    failed = torch.tensor([5, 7, 5], dtype=torch.int64)
+    got = failed_flags(torch, keys, failed).tolist()
+    assert got == [0, 0, 1, 0, 1, 1, 0]
+    assert failed_flags(torch, keys, failed[:0]).tolist() == [0] * 7

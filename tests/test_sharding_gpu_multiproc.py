@@ -67,7 +67,8 @@ def _free_port():
 @pytest.mark.parametrize("peer", ["1", "0"])
 def test_two_rank_sharded_facades(oracle, peer):
     """peer = 1: the fused peer-memory exchange (fk_shard_dispatch /
-    fk_shard_combine over CUDA IPC mappings); 0: the all-to-all router."""
+    fk_shard_combine over CUDA IPC mappings, stream-ordered fk_shard_signal /
+    fk_shard_wait handoffs); 0: the all-to-all router."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
