@@ -75,6 +75,16 @@ cudaError_t cub_sort_keys_u32(Scratch &S, const uint32_t *kin, uint32_t *kout, i
   return cub::DeviceRadixSort::SortKeys(tmp, tb, kin, kout, n, 0, end_bit, S.st);
 }
 
+cudaError_t cub_sort_keys_u32_bits(Scratch &S, const uint32_t *kin, uint32_t *kout, int64_t n, int begin_bit,
+                                   int end_bit) {
+  size_t tb = 0;
+  cudaError_t e = cub::DeviceRadixSort::SortKeys(nullptr, tb, kin, kout, n, begin_bit, end_bit, S.st);
+  if (e) return e;
+  void *tmp = S.get<char>(tb);
+  if (!tmp) return S.err;
+  return cub::DeviceRadixSort::SortKeys(tmp, tb, kin, kout, n, begin_bit, end_bit, S.st);
+}
+
 cudaError_t cub_sort_pairs_u8_u32(Scratch &S, const uint8_t *kin, uint8_t *kout, const uint32_t *vin, uint32_t *vout,
                                   int64_t n, int end_bit) {
   size_t tb = 0;
@@ -242,6 +252,87 @@ int validate_t(const fk_gqf_geom *g, const fk_gqf_tables *t, int64_t *out, cudaS
 
 // a batch touching at most this many distinct fingerprints takes the
 // region-local path (tunable: FK_GQF_SMALL; 0 disables)
+// Partition counting (k_part_*) of plain counted inserts: two kPartBits MSD
+// passes then shared-memory aggregation of the low W = qr - 2 kPartBits bits.
+// Used from 2^22 occurrences (smaller batches keep the CUB sort; tunable:
+// FK_GQF_PART=0 disables, FK_GQF_PART_MIN sets the threshold).
+// Pass 2 uses p2 <= kPartBits bits, so partitions average ~3 K occurrences.
+inline bool part_plan(int64_t n, int qr, int *W, int *p2) {
+  const char *e = getenv("FK_GQF_PART");
+  if (e && atoi(e) == 0) return false;
+  const char *m = getenv("FK_GQF_PART_MIN");
+  const int64_t nmin = m ? atoll(m) : (1LL << 22);
+  int b = 1;
+  while (b < kPartBits && (n >> (kPartBits + b)) > 3072) b++;
+  const int w = qr - kPartBits - b;
+  if (n < nmin || w < 4 || qr - kPartBits > 32) return false;
+  *W = w;
+  *p2 = b;
+  return true;
+}
+
+__global__ void k_part_total(const int64_t *__restrict__ uoff, const int64_t *__restrict__ ucount, int64_t NP,
+                             const unsigned *__restrict__ overflow, int64_t *__restrict__ out) {
+  out[0] = uoff[NP - 1] + ucount[NP - 1];
+  out[1] = *overflow;
+}
+
+// Count a plain insert batch by partitions: uniq / sums / *d_num like the
+// sort + run-length path.  Returns 0, 1 when a partition overflowed its
+// shared-memory table (nothing usable; recount on the sort path), or < 0.
+int part_count(Scratch &S, const uint64_t *keys, int keys_are_fps, uint64_t seed, uint64_t fmask, int qr, int W,
+               int p2, int64_t n, uint64_t *uniq, uint64_t *sums, int64_t *d_num) {
+  cudaStream_t st = S.st;
+  const int64_t NP = 1LL << (kPartBits + p2);
+  unsigned long long *hist1 = S.get<unsigned long long>(kPartBins), *bounds1 = S.get<unsigned long long>(kPartBins + 1),
+                     *cursor1 = S.get<unsigned long long>(kPartBins),
+                     *tstart = S.get<unsigned long long>(kPartBins + 1);
+  unsigned long long *hist2 = S.get<unsigned long long>(NP + 1), *bounds2 = S.get<unsigned long long>(NP + 1);
+  int64_t *ucount = S.get<int64_t>(NP), *uoff = S.get<int64_t>(NP);
+  uint32_t *buf1 = S.get<uint32_t>(n), *buf2 = S.get<uint32_t>(n);
+  uint64_t *out_fp = S.get<uint64_t>(n);
+  unsigned *ovf = S.get<unsigned>(1);
+  if (S.err) return -(int)S.err;
+  FK_TRY(cudaMemsetAsync(hist1, 0, kPartBins * sizeof(unsigned long long), st));
+  FK_TRY(cudaMemsetAsync(hist2, 0, (NP + 1) * sizeof(unsigned long long), st));
+  FK_TRY(cudaMemsetAsync(ovf, 0, sizeof(unsigned), st));
+  static bool attr = false;
+  if (!attr) {
+    FK_TRY(cudaFuncSetAttribute(k_part1_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPartSmem));
+    FK_TRY(cudaFuncSetAttribute(k_part2_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPartSmem));
+    attr = true;
+  }
+  const int sms = num_sms();
+  k_part1_hist<<<sms * 4, kPartThreads, 0, st>>>(keys, keys_are_fps, seed, fmask, qr, n, hist1);
+  k_part_plan1<<<1, kPartBins, 0, st>>>(hist1, bounds1, cursor1, tstart);
+  k_part1_scatter<<<sms * 4, kPartThreads, kPartSmem, st>>>(keys, keys_are_fps, seed, fmask, qr, n, cursor1, buf1);
+  k_part2_hist<<<sms * 4, kPartThreads, 0, st>>>(buf1, bounds1, tstart, W, p2, hist2);
+  {
+    size_t tb = 0;
+    FK_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tb, hist2, bounds2, NP + 1, st));
+    void *tmp = S.get<char>(tb);
+    if (!tmp) return -(int)S.err;
+    FK_TRY(cub::DeviceScan::ExclusiveSum(tmp, tb, hist2, bounds2, NP + 1, st));
+  }
+  FK_TRY(cudaMemcpyAsync(hist2, bounds2, NP * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, st));  // cursors
+  k_part2_scatter<<<sms * 4, kPartThreads, kPartSmem, st>>>(buf1, bounds1, tstart, W, p2, hist2, buf2);
+  uint32_t *out_cnt = buf1;  // pass-1 output is dead now
+  int lg = 12;  // log2(kAggSlots); FK_GQF_PART_SLOTS (a power of two below it) exercises the overflow path
+  if (const char *e = getenv("FK_GQF_PART_SLOTS"))
+    while (lg > 1 && (1 << lg) > atoi(e)) lg--;
+  k_part_aggregate<<<sms * 6, kAggThreads, 0, st>>>(buf2, bounds2, NP, W, out_fp, out_cnt, ucount, ovf, lg);
+  FK_TRY(cub_excl_sum_i64(S, ucount, uoff, NP));
+  k_part_total<<<1, 1, 0, st>>>(uoff, ucount, NP, ovf, d_num + 2);
+  int64_t h2[2];
+  FK_TRY(cudaMemcpyAsync(h2, d_num + 2, sizeof(h2), cudaMemcpyDeviceToHost, st));
+  FK_TRY(cudaStreamSynchronize(st));
+  if (h2[1]) return 1;
+  k_part_compact<<<blocks_for(NP * 32), 256, 0, st>>>(out_fp, out_cnt, bounds2, ucount, uoff, NP, uniq, sums);
+  FK_TRY(cudaMemcpyAsync(d_num, d_num + 2, sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+  FK_CHECK_LAUNCH();
+  return 0;
+}
+
 inline int64_t small_batch_limit(const fk_gqf_geom *g) {
   const char *e = getenv("FK_GQF_SMALL");
   if (e) return atoll(e);
@@ -438,7 +529,8 @@ int apply_t(const fk_gqf_geom *g, const fk_gqf_tables *cur, const fk_gqf_tables 
   uint64_t *uniq = S.get<uint64_t>(n), *sums = S.get<uint64_t>(n);
   int64_t *d_num = S.get<int64_t>(4);
   if (S.err) return -(int)S.err;
-  if (split) {
+  // the split sort of the occurrences (hi_s, lo_s sorted by fingerprint)
+  auto split_sort = [&]() -> int {
     uint32_t *lo = S.get<uint32_t>(n);
     lo_s = S.get<uint32_t>(n);
     uint8_t *hi = nullptr;
@@ -449,21 +541,32 @@ int apply_t(const fk_gqf_geom *g, const fk_gqf_tables *cur, const fk_gqf_tables 
     if (S.err) return -(int)S.err;
     k_hash_split<<<blocks_for(n), 256, 0, st>>>(keys, keys_are_fps, g->seed, fmask, n, hi, lo);
     if (qr <= 32) {
-      FK_CU(cub_sort_keys_u32(S, lo, lo_s, n, qr));
+      FK_TRY(cub_sort_keys_u32(S, lo, lo_s, n, qr));
     } else {
       uint32_t *lo_p = S.get<uint32_t>(n);
       const int nseg = 1 << (qr - 32);
       int64_t *bounds = S.get<int64_t>(nseg + 1);
       if (S.err) return -(int)S.err;
-      FK_CU(cub_sort_pairs_u8_u32(S, hi, hi_s, lo, lo_p, n, qr - 32));
+      FK_TRY(cub_sort_pairs_u8_u32(S, hi, hi_s, lo, lo_p, n, qr - 32));
       k_u8_bounds<<<1, 256, 0, st>>>(hi_s, n, nseg, bounds);
       std::vector<int64_t> hb(nseg + 1);
-      FK_CU(cudaMemcpyAsync(hb.data(), bounds, (nseg + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-      FK_CU(cudaStreamSynchronize(st));
+      FK_TRY(cudaMemcpyAsync(hb.data(), bounds, (nseg + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+      FK_TRY(cudaStreamSynchronize(st));
       for (int sgi = 0; sgi < nseg; sgi++)
-        if (hb[sgi + 1] > hb[sgi]) FK_CU(cub_sort_keys_u32(S, lo_p + hb[sgi], lo_s + hb[sgi], hb[sgi + 1] - hb[sgi], 32));
+        if (hb[sgi + 1] > hb[sgi]) FK_TRY(cub_sort_keys_u32(S, lo_p + hb[sgi], lo_s + hb[sgi], hb[sgi + 1] - hb[sgi], 32));
     }
-    FK_CU(cub_rle_counts_split(S, hi_s, lo_s, uniq, sums, d_num, n));
+    return 0;
+  };
+  if (split) {
+    int W = 0, p2 = 0, rc = 1;
+    if (part_plan(n, qr, &W, &p2))
+      rc = part_count(S, keys, keys_are_fps, g->seed, fmask, qr, W, p2, n, uniq, sums, d_num);
+    if (rc < 0) return rc;
+    if (rc == 1) {  // the sort + run-length path
+      int rs = split_sort();
+      if (rs) return rs;
+      FK_CU(cub_rle_counts_split(S, hi_s, lo_s, uniq, sums, d_num, n));
+    }
   } else {
     fps = S.get<uint64_t>(n);
     fps_s = S.get<uint64_t>(n);
@@ -682,6 +785,10 @@ int apply_t(const fk_gqf_geom *g, const fk_gqf_tables *cur, const fk_gqf_tables 
         if (!fps_s) {  // sorted occurrences from the split sort
           fps_s = S.get<uint64_t>(n);
           if (S.err) return -(int)S.err;
+          if (!lo_s) {  // counted by partitions: sort the occurrences now
+            int rs = split_sort();
+            if (rs) return rs;
+          }
           k_widen_split<<<blocks_for(n), 256, 0, st>>>(hi_s, lo_s, n, fps_s);
         }
         if (!del_s) del_s = S.get<uint64_t>(n);

@@ -250,6 +250,390 @@ __global__ void k_u8_bounds(const uint8_t *__restrict__ hs, int64_t n, int nseg,
   }
 }
 
+// ---- partitioned counting of plain counted inserts -------------------------
+// Counting the occurrences of a batch (insert of every occurrence, no delta
+// array) is a group-by on the fingerprint.  Instead of sorting every
+// occurrence on all q + r bits and run-length encoding the result:
+//   1. two MSD partition passes (kPartBits each) scatter the hashed
+//      occurrences by their top 2 * kPartBits fingerprint bits; a CTA stages a
+//      tile in shared memory grouped by digit (unstable ranks: order inside a
+//      partition does not matter), reserves one contiguous range per digit
+//      with one global atomic, and writes the groups out coalesced;
+//   2. one CTA per partition aggregates its low W bits in a shared-memory
+//      hash table, sorts only the distinct fingerprints (bitonic), and writes
+//      (fingerprint, count) runs; a compaction pass packs the partitions.
+// Partitions whose distinct fingerprints overflow the table set a flag and
+// the caller recounts the batch on the full-sort path.
+constexpr int kPartBits = 9;
+constexpr int kPartBins = 1 << kPartBits;
+constexpr int kPartThreads = 512;
+constexpr int kPartItems = 8;                          // per thread: 4 K occurrences per tile
+constexpr int kPartTile = kPartThreads * kPartItems;
+constexpr int kAggThreads = 256;
+constexpr int kAggSlots = 4096;                        // hash table entries per partition CTA
+
+__device__ __forceinline__ uint64_t part_fp(const uint64_t *keys, int keys_are_fps, uint64_t seed, uint64_t fmask,
+                                            int64_t i) {
+  const uint64_t k = __ldcs(keys + i);
+  return (keys_are_fps ? k : mix64(k ^ seed)) & fmask;
+}
+
+// Pass-1 histogram: digit = fingerprint bits [qr - kPartBits, qr).
+__global__ void __launch_bounds__(kPartThreads) k_part1_hist(const uint64_t *__restrict__ keys, int keys_are_fps,
+                                                             uint64_t seed, uint64_t fmask, int qr, int64_t n,
+                                                             unsigned long long *__restrict__ hist) {
+  __shared__ unsigned sh[kPartBins];
+  for (int i = threadIdx.x; i < kPartBins; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&sh[part_fp(keys, keys_are_fps, seed, fmask, i) >> (qr - kPartBits)], 1u);
+  __syncthreads();
+  for (int i = threadIdx.x; i < kPartBins; i += blockDim.x)
+    if (sh[i]) atomicAdd(&hist[i], (unsigned long long)sh[i]);
+}
+
+// Tile scatter shared by both passes: every thread holds kPartItems
+// (digit, value) pairs; the tile is regrouped by digit in shared memory and
+// each digit's group is written to cursor[digit] (reserved with one atomic).
+__device__ __forceinline__ void part_scatter_tile(const uint32_t (&dg)[kPartItems], const uint32_t (&val)[kPartItems],
+                                                  const bool (&ok)[kPartItems], unsigned long long *cursor,
+                                                  uint32_t *out, unsigned *s_cnt, unsigned *s_off,
+                                                  unsigned long long *s_base, uint32_t *s_val, uint16_t *s_dg) {
+  for (int i = threadIdx.x; i < kPartBins; i += blockDim.x) s_cnt[i] = 0;
+  __syncthreads();
+  unsigned rk[kPartItems];
+#pragma unroll
+  for (int j = 0; j < kPartItems; j++) rk[j] = ok[j] ? atomicAdd(&s_cnt[dg[j]], 1u) : 0u;
+  __syncthreads();
+  // exclusive offsets of the digit groups inside the tile (512 bins, one
+  // thread each) and one global reservation per non-empty digit
+  {
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __shared__ unsigned s_w[kPartThreads / 32];
+    const unsigned v = threadIdx.x < kPartBins ? s_cnt[threadIdx.x] : 0u;
+    unsigned inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned t = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+      if ((int)lane >= o) inc += t;
+    }
+    if (lane == 31) s_w[warp] = inc;
+    __syncthreads();
+    unsigned base = inc - v;
+    for (int w = 0; w < (int)warp; w++) base += s_w[w];
+    if (threadIdx.x < kPartBins) {
+      s_off[threadIdx.x] = base;
+      s_base[threadIdx.x] = v ? atomicAdd(&cursor[threadIdx.x], (unsigned long long)v) : 0ull;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kPartItems; j++)
+    if (ok[j]) {
+      const unsigned pos = s_off[dg[j]] + rk[j];
+      s_val[pos] = val[j];
+      s_dg[pos] = (uint16_t)dg[j];
+    }
+  __syncthreads();
+  const unsigned tot = s_off[kPartBins - 1] + s_cnt[kPartBins - 1];
+  for (unsigned pos = threadIdx.x; pos < tot; pos += blockDim.x) {
+    const unsigned d = s_dg[pos];
+    out[s_base[d] + (pos - s_off[d])] = s_val[pos];
+  }
+  __syncthreads();
+}
+
+// Pass 1: hash every occurrence, keep its low qr - kPartBits bits (u32) and
+// scatter by the top kPartBits.  cursor[d] starts at the digit's offset.
+// dynamic shared memory of the scatter kernels: tile values, digits, and the
+// per-digit counters / offsets / reserved bases
+constexpr size_t kPartSmem = (size_t)kPartTile * 6 + (size_t)kPartBins * 16;
+struct PartSmem {
+  unsigned long long *base;
+  unsigned *cnt, *off;
+  uint32_t *val;
+  uint16_t *dg;
+  __device__ explicit PartSmem(unsigned char *p) {
+    base = reinterpret_cast<unsigned long long *>(p);
+    cnt = reinterpret_cast<unsigned *>(p + kPartBins * 8);
+    off = cnt + kPartBins;
+    val = reinterpret_cast<uint32_t *>(p + kPartBins * 16);
+    dg = reinterpret_cast<uint16_t *>(p + kPartBins * 16 + (size_t)kPartTile * 4);
+  }
+};
+
+__global__ void __launch_bounds__(kPartThreads) k_part1_scatter(const uint64_t *__restrict__ keys, int keys_are_fps,
+                                                                uint64_t seed, uint64_t fmask, int qr, int64_t n,
+                                                                unsigned long long *__restrict__ cursor,
+                                                                uint32_t *__restrict__ out) {
+  extern __shared__ __align__(16) unsigned char part_sm[];
+  PartSmem P(part_sm);
+  const int sh = qr - kPartBits;
+  const uint64_t lmask = (1ull << sh) - 1;
+  for (int64_t t0 = (int64_t)blockIdx.x * kPartTile; t0 < n; t0 += (int64_t)gridDim.x * kPartTile) {
+    uint32_t dg[kPartItems], val[kPartItems];
+    bool ok[kPartItems];
+#pragma unroll
+    for (int j = 0; j < kPartItems; j++) {
+      const int64_t i = t0 + (int64_t)j * kPartThreads + threadIdx.x;
+      ok[j] = i < n;
+      const uint64_t fp = ok[j] ? part_fp(keys, keys_are_fps, seed, fmask, i) : 0ull;
+      dg[j] = (uint32_t)(fp >> sh);
+      val[j] = (uint32_t)(fp & lmask);
+    }
+    part_scatter_tile(dg, val, ok, cursor, out, P.cnt, P.off, P.base, P.val, P.dg);
+  }
+}
+
+// Pass-2 histogram over the pass-1 output: partition p = (d1 << kPartBits) | d2
+// with d1 from the item's position (bounds1) and d2 = bits [sh2, sh2 + kPartBits)
+// of the stored value.
+// tile t of pass 2 -> its pass-1 digit d1 (tile_start[d1] = d1's first tile)
+__device__ __forceinline__ int part_tile_digit(const unsigned long long *tile_start, int64_t t) {
+  int lo = 0, hi = kPartBins;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (tile_start[mid] <= (unsigned long long)t) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// Pass-2 histogram, per pass-1 digit and tile (the scatter's tiling), so the
+// global counters take one atomic per (tile, digit).
+__global__ void __launch_bounds__(kPartThreads) k_part2_hist(const uint32_t *__restrict__ in,
+                                                             const unsigned long long *__restrict__ bounds1,
+                                                             const unsigned long long *__restrict__ tile_start,
+                                                             int sh2, int p2, unsigned long long *__restrict__ hist) {
+  __shared__ unsigned sh[kPartBins];
+  const int64_t ntiles = (int64_t)tile_start[kPartBins];
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    for (int i = threadIdx.x; i < kPartBins; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+    const int d1 = part_tile_digit(tile_start, t);
+    const int64_t a = (int64_t)bounds1[d1] + (t - (int64_t)tile_start[d1]) * kPartTile;
+    int64_t e = (int64_t)bounds1[d1 + 1];
+    if (e > a + kPartTile) e = a + kPartTile;
+    for (int64_t i = a + threadIdx.x; i < e; i += blockDim.x) atomicAdd(&sh[(__ldcs(in + i) >> sh2) & ((1u << p2) - 1)], 1u);
+    __syncthreads();
+    for (int i = threadIdx.x; i < (1 << p2); i += blockDim.x)
+      if (sh[i]) atomicAdd(&hist[((uint64_t)d1 << p2) | i], (unsigned long long)sh[i]);
+    __syncthreads();
+  }
+}
+
+// bounds1 / cursor1 (exclusive sums of the 512 pass-1 counts) and every
+// digit's first pass-2 tile; tile_start[kPartBins] = the number of tiles
+__global__ void __launch_bounds__(kPartBins) k_part_plan1(const unsigned long long *__restrict__ hist1,
+                                                          unsigned long long *__restrict__ bounds1,
+                                                          unsigned long long *__restrict__ cursor1,
+                                                          unsigned long long *__restrict__ tile_start) {
+  __shared__ unsigned long long sw[kPartBins / 32][2];
+  const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned long long c = hist1[threadIdx.x];
+  const unsigned long long nt = (c + kPartTile - 1) / kPartTile;
+  unsigned long long ic = c, it = nt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long a = __shfl_up_sync(0xFFFFFFFFu, ic, o), b = __shfl_up_sync(0xFFFFFFFFu, it, o);
+    if ((int)lane >= o) {
+      ic += a;
+      it += b;
+    }
+  }
+  if (lane == 31) {
+    sw[warp][0] = ic;
+    sw[warp][1] = it;
+  }
+  __syncthreads();
+  unsigned long long bc = ic - c, bt = it - nt;
+  for (int w = 0; w < (int)warp; w++) {
+    bc += sw[w][0];
+    bt += sw[w][1];
+  }
+  bounds1[threadIdx.x] = bc;
+  cursor1[threadIdx.x] = bc;
+  tile_start[threadIdx.x] = bt;
+  if (threadIdx.x == kPartBins - 1) {
+    bounds1[kPartBins] = bc + c;
+    tile_start[kPartBins] = bt + nt;
+  }
+}
+
+// Pass 2: tiles never straddle a pass-1 digit (grid-stride over
+// (digit, tile) pairs), so the partition is d1 << kPartBits | d2 and the
+// scatter keeps the low sh2 bits.
+__global__ void __launch_bounds__(kPartThreads) k_part2_scatter(const uint32_t *__restrict__ in,
+                                                                const unsigned long long *__restrict__ bounds1,
+                                                                const unsigned long long *__restrict__ tile_start,
+                                                                int sh2, int p2, unsigned long long *__restrict__ cursor,
+                                                                uint32_t *__restrict__ out) {
+  extern __shared__ __align__(16) unsigned char part_sm[];
+  PartSmem P(part_sm);
+  const uint32_t lmask = sh2 >= 32 ? 0xFFFFFFFFu : ((1u << sh2) - 1u);
+  const int64_t ntiles = (int64_t)tile_start[kPartBins];
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int d1 = part_tile_digit(tile_start, t);
+    const int64_t a = (int64_t)bounds1[d1] + (t - (int64_t)tile_start[d1]) * kPartTile;
+    const int64_t e = (int64_t)bounds1[d1 + 1];
+    uint32_t dg[kPartItems], val[kPartItems];
+    bool ok[kPartItems];
+#pragma unroll
+    for (int j = 0; j < kPartItems; j++) {
+      const int64_t i = a + (int64_t)j * kPartThreads + threadIdx.x;
+      ok[j] = i < e;
+      const uint32_t v = ok[j] ? __ldcs(in + i) : 0u;
+      dg[j] = (v >> sh2) & ((1u << p2) - 1);
+      val[j] = v & lmask;
+    }
+    part_scatter_tile(dg, val, ok, cursor + ((uint64_t)d1 << p2), out, P.cnt, P.off, P.base, P.val, P.dg);
+  }
+}
+
+// One CTA per partition: hash-aggregate the low W bits, bitonic-sort the
+// distinct ones, write (fp, count) at the partition's own offset.
+__global__ void __launch_bounds__(kAggThreads) k_part_aggregate(const uint32_t *__restrict__ in,
+                                                                const unsigned long long *__restrict__ bounds2,
+                                                                int64_t NP, int W, uint64_t *__restrict__ out_fp,
+                                                                uint32_t *__restrict__ out_cnt,
+                                                                int64_t *__restrict__ ucount,
+                                                                unsigned *__restrict__ overflow, int lg_slots) {
+  __shared__ uint64_t tab[kAggSlots];  // keys | counts while counting, then sorted (key << 32 | count) words
+  __shared__ unsigned s_n, s_bad;
+  uint32_t *hk = reinterpret_cast<uint32_t *>(tab), *hc = hk + kAggSlots;
+  constexpr uint32_t kEmpty = 0xFFFFFFFFu;
+  for (int64_t p = blockIdx.x; p < NP; p += gridDim.x) {
+    const int64_t a = (int64_t)bounds2[p], e = (int64_t)bounds2[p + 1];
+    if (a == e) {
+      if (threadIdx.x == 0) ucount[p] = 0;
+      continue;
+    }
+    const uint32_t nslots = 1u << lg_slots;  // <= kAggSlots (smaller only to exercise the overflow path)
+    for (int i = threadIdx.x; i < kAggSlots; i += kAggThreads) {
+      hk[i] = kEmpty;
+      hc[i] = 0;
+    }
+    if (threadIdx.x == 0) {
+      s_n = 0;
+      s_bad = 0;
+    }
+    __syncthreads();
+    for (int64_t i0 = a; i0 < e; i0 += kAggThreads * 8) {
+      uint32_t v[8];  // eight loads in flight before the table updates
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        const int64_t i = i0 + u * kAggThreads + threadIdx.x;
+        v[u] = i < e ? __ldcs(in + i) : kEmpty;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        const uint32_t k = v[u];
+        if (k == kEmpty) continue;  // (keys have W <= 31 bits)
+        uint32_t h = (k * 0x9E3779B1u) >> (32 - lg_slots);
+        uint32_t probes = 0;
+        for (;;) {
+          // plain read first: most occurrences find their key already there
+          // and need one shared-memory atomic, not two
+          uint32_t old = *(volatile uint32_t *)&hk[h];
+          if (old == kEmpty) old = atomicCAS(&hk[h], kEmpty, k);
+          if (old == kEmpty || old == k) {
+            atomicAdd(&hc[h], 1u);
+            break;
+          }
+          h = (h + 1) & (nslots - 1);
+          if (++probes == nslots) {
+            s_bad = 1;
+            break;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (s_bad) {
+      if (threadIdx.x == 0) {
+        ucount[p] = -1;
+        atomicOr(overflow, 1u);
+      }
+      __syncthreads();
+      continue;
+    }
+    // compact the occupied entries to the front (order arbitrary), as
+    // 64-bit (key << 32 | count) words in place of the table
+    uint64_t *kv = tab;
+    uint64_t mine[kAggSlots / kAggThreads];
+    int nm = 0;
+#pragma unroll
+    for (int j = 0; j < kAggSlots / kAggThreads; j++) {
+      const int i = j * kAggThreads + threadIdx.x;
+      if (hk[i] != kEmpty) mine[nm++] = ((uint64_t)hk[i] << 32) | hc[i];
+    }
+    __syncthreads();
+    for (int j = 0; j < nm; j++) kv[atomicAdd(&s_n, 1u)] = mine[j];
+    __syncthreads();
+    const unsigned d = s_n;
+    unsigned m2 = 1;
+    while (m2 < d) m2 <<= 1;
+    for (unsigned i = d + threadIdx.x; i < m2; i += kAggThreads) kv[i] = ~0ull;  // pads sort last
+    __syncthreads();
+    // bitonic sort; stages whose partner distance is below 64 stay inside a
+    // warp's own 64-element chunks (no block barrier), the rest sync the CTA
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr unsigned NW = kAggThreads / 32;
+    for (unsigned k2 = 2; k2 <= m2; k2 <<= 1) {
+      for (unsigned j2 = k2 >> 1; j2 > 0; j2 >>= 1) {
+        const unsigned lj = __ffs(j2) - 1;  // j2 is a power of two: shifts, not divisions
+        if (j2 >= 64) {
+          for (unsigned q = threadIdx.x; q < m2 / 2; q += kAggThreads) {
+            const unsigned i = ((q >> lj) << (lj + 1)) | (q & (j2 - 1)), l = i + j2;
+            const uint64_t x = kv[i], y = kv[l];
+            if ((x > y) == ((i & k2) == 0)) {
+              kv[i] = y;
+              kv[l] = x;
+            }
+          }
+          __syncthreads();
+        } else {
+          const unsigned span = m2 < 64 ? m2 : 64;
+          for (unsigned c = warp; c * span < m2; c += NW) {
+            if (lane < span / 2) {
+              const unsigned i = c * span + (((lane >> lj) << (lj + 1)) | (lane & (j2 - 1))), l = i + j2;
+              const uint64_t x = kv[i], y = kv[l];
+              if ((x > y) == ((i & k2) == 0)) {
+                kv[i] = y;
+                kv[l] = x;
+              }
+            }
+          }
+          __syncwarp();
+        }
+      }
+      __syncthreads();
+    }
+    for (unsigned j = threadIdx.x; j < d; j += kAggThreads) {
+      const uint64_t v = kv[j];
+      out_fp[a + j] = ((uint64_t)p << W) | (v >> 32);
+      out_cnt[a + j] = (uint32_t)v;
+    }
+    if (threadIdx.x == 0) ucount[p] = d;
+    __syncthreads();
+  }
+}
+
+// uniq / sums = the partitions' runs, compacted (one warp per partition)
+__global__ void k_part_compact(const uint64_t *__restrict__ out_fp, const uint32_t *__restrict__ out_cnt,
+                               const unsigned long long *__restrict__ bounds2, const int64_t *__restrict__ ucount,
+                               const int64_t *__restrict__ uoff, int64_t NP, uint64_t *__restrict__ uniq,
+                               uint64_t *__restrict__ sums) {
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const unsigned lane = threadIdx.x & 31;
+  for (int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < NP; p += warps) {
+    const int64_t s = (int64_t)bounds2[p], d = uoff[p], U = ucount[p];
+    for (int64_t j = lane; j < U; j += 32) {
+      uniq[d + j] = out_fp[s + j];
+      sums[d + j] = out_cnt[s + j];
+    }
+  }
+}
+
 __global__ void k_gather_u64(const uint64_t *__restrict__ src, const uint32_t *__restrict__ idx,
                              uint64_t dflt, int64_t n, uint64_t *__restrict__ dst) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)

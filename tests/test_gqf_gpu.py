@@ -586,3 +586,47 @@ def test_churn_fuzz_vs_oracle(oracle, monkeypatch, seed, q):
     assert raised > 0  # the capacity paths ran
     g.validate()
     assert list(g.enumerate_items()) == list(g._enumerate_host())
+
+
+@pytest.mark.parametrize("q,r,n,dup", [(20, 8, 600_000, 0), (18, 16, 150_000, 7), (22, 16, 2_000_000, 3)])
+def test_partition_counting_equals_full_sort(oracle, monkeypatch, q, r, n, dup):
+    """Plain counted bulk inserts of large batches are counted by two MSD
+    partition passes and shared-memory hash aggregation (k_part_*); the
+    image equals the sort + run-length path's (FK_GQF_PART=0) and, where the
+    C oracle is quick, the oracle's.  (22, 16): 38-bit fingerprints."""
+    from paper_2212_09005_b200 import Gqf
+    rng = np.random.default_rng(q + r)
+    base = rng.integers(0, 2 ** 63, n, dtype=np.uint64)
+    keys = np.concatenate([base] + [base[: n // (4 * dup)]] * dup) if dup else base
+    keys = rng.permutation(keys)
+    monkeypatch.setenv("FK_GQF_PART_MIN", "1000")
+    a = Gqf(q=q, r=r)
+    a.bulk_insert(keys)
+    monkeypatch.setenv("FK_GQF_PART", "0")
+    b = Gqf(q=q, r=r)
+    b.bulk_insert(keys)
+    for name in ("_slots", "_occupieds", "_runends", "_offsets", "_stats"):
+        assert np.array_equal(getattr(a, name), getattr(b, name)), name
+    a.validate()
+    if n <= 600_000:
+        o = _oracle(a, oracle)
+        assert o.bulk_insert(keys) == []
+        same_image(a, o)
+
+
+def test_partition_counting_overflow_falls_back(oracle, monkeypatch):
+    """A partition with more distinct fingerprints than its shared-memory
+    table holds (table capped at 8 entries here) makes the batch recount on
+    the sort + run-length path: same image and counts as the oracle."""
+    from paper_2212_09005_b200 import Gqf
+    rng = np.random.default_rng(11)
+    base = rng.integers(0, 2 ** 63, 60_000, dtype=np.uint64)
+    keys = rng.permutation(np.concatenate([base, np.full(20_000, base[7], np.uint64)]))
+    monkeypatch.setenv("FK_GQF_PART_MIN", "1000")
+    monkeypatch.setenv("FK_GQF_PART_SLOTS", "8")
+    g = Gqf(q=17, r=16)
+    o = _oracle(g, oracle)
+    g.bulk_insert(keys)
+    assert o.bulk_insert(keys) == []
+    same_image(g, o)
+    assert g.count_many(base[7:8])[0] == o.count_many(base[7:8])[0]
