@@ -320,6 +320,21 @@ int fk_gqf_insert_batch(const fk_gqf_geom *g, const fk_gqf_tables *t, const uint
 int fk_gqf_delete_batch(const fk_gqf_geom *g, const fk_gqf_tables *t, const uint64_t *fps, const uint64_t *deltas,
                         int64_t n, uint8_t *found, int64_t *shift_out, void *stream);
 
+/* ---- inspection on the device ----------------------------- */
+
+/* Gqf.cluster_stats (gqf.py:416-428): out3 (HOST int64[3]) = {number of
+ * maximal contiguous used-slot spans, the longest, their total slots} from a
+ * global rank/select over the bit vectors.  Synchronous. */
+int fk_gqf_cluster_stats(const fk_gqf_geom *g, const fk_gqf_tables *t, int64_t *out3, void *stream);
+
+/* Tcf.items / BulkTcf.items (tcf.py:196-208, tcf_bulk.py:342-352): idx_out
+ * (device int64[n]) gets the positions of the live slots among n slot_bytes
+ * words in ascending order, *count (device int64) their number.  A slot is
+ * live when its word is > TOMBSTONE, or, with fill (bulk TCF blocks of
+ * block_slots), when it lies in its block's filled prefix.  Asynchronous. */
+int fk_live_slots(const void *slots, int slot_bytes, int64_t n, const uint32_t *fill, int block_slots,
+                  int64_t *idx_out, int64_t *count, void *stream);
+
 /* ---- hash-prefix sharding (new in this build) -------------- */
 
 /* Stable partition of a key batch by owner shard, owner = bits

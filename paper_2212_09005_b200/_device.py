@@ -80,6 +80,26 @@ class DeviceTables:
         self.lent.clear()
 
 
+def live_slots(torch, lib, tables, name, fill_name=None, block_slots=1):
+    """(positions, words) of the live slots of table `name`, selected on the
+    device (fk_live_slots) so only the live entries cross to the host."""
+    dt, c = tables.spec[name]
+    if not c:
+        return np.zeros(0, np.int64), np.zeros(0, dt)
+    dev = tables.dev[name]
+    idx = torch.empty(c, dtype=torch.int64, device=dev.device)
+    cnt = torch.zeros(1, dtype=torch.int64, device=dev.device)
+    fill = _lib.dptr(tables.dev[fill_name]) if fill_name else None
+    _lib.check(lib.fk_live_slots(_lib.dptr(dev), np.dtype(dt).itemsize, c, fill, block_slots, _lib.dptr(idx),
+                                 _lib.dptr(cnt), _lib.stream_ptr(torch)), "live slots")
+    m = int(cnt.item())
+    idx = idx[:m]
+    itemsize = np.dtype(dt).itemsize
+    tdt = {1: torch.uint8, 2: torch.int16, 4: torch.int32, 8: torch.int64}[itemsize]
+    words = dev[: c * itemsize].view(tdt)[idx]
+    return idx.cpu().numpy(), words.cpu().numpy().view(dt)
+
+
 def keys_in(torch, keys, device):
     """-> (device int64 tensor, kind): kind 'cuda' (results stay on device,
     asynchronous), 'host' (CPU torch tensor; results come back as CPU

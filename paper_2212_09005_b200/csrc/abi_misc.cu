@@ -1,8 +1,29 @@
-// abi_misc.cu -- version + hashing-parity entry points of the C ABI.
+// abi_misc.cu -- version, hashing-parity and inspection entry points of the C ABI.
+#include <cub/cub.cuh>
+
 #include "../../include/filterkit_b200.h"
 #include "fk_common.cuh"
+#include "fk_scratch.cuh"
 
 namespace fk {
+
+// slot i holds a live word (> TOMBSTONE); with fill (sorted bulk blocks):
+// i lies in its block's filled prefix
+struct LiveSlot {
+  const void *slots;
+  int bytes;
+  const uint32_t *fill;
+  int B;
+  __device__ bool operator()(int64_t i) const {
+    if (fill) return (uint32_t)(i % B) < fill[i / B];
+    switch (bytes) {
+      case 1: return reinterpret_cast<const uint8_t *>(slots)[i] > 1;
+      case 2: return reinterpret_cast<const uint16_t *>(slots)[i] > 1;
+      case 4: return reinterpret_cast<const uint32_t *>(slots)[i] > 1;
+      default: return reinterpret_cast<const uint64_t *>(slots)[i] > 1;
+    }
+  }
+};
 
 // fp, b1, b2, backing start, backing step per key (hashing.py:66-117).
 __global__ void k_hash_streams(const uint64_t *__restrict__ keys, int64_t n, uint64_t seed, uint64_t fpmask,
@@ -162,6 +183,28 @@ int fk_fastmod_check(const uint64_t *x, int64_t n, uint64_t d, uint64_t *out, vo
   if (grid > num_sms() * 16) grid = num_sms() * 16;
   k_fastmod<<<grid, 256, 0, (cudaStream_t)stream>>>(x, n, make_fastmod(d), out);
   FK_CHECK_LAUNCH();
+  return 0;
+}
+
+// Tcf.items / BulkTcf.items on the device (fk/tcf.py:196-208,
+// fk/tcf_bulk.py:342-352): positions of the live slots, ascending.
+int fk_live_slots(const void *slots, int slot_bytes, int64_t n, const uint32_t *fill, int block_slots,
+                  int64_t *idx_out, int64_t *count, void *stream) {
+  if (n < 0 || !idx_out || !count || (fill && block_slots < 1)) return FK_E_ARG;
+  if (slot_bytes != 1 && slot_bytes != 2 && slot_bytes != 4 && slot_bytes != 8) return FK_E_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n == 0) {
+    FK_TRY(cudaMemsetAsync(count, 0, sizeof(int64_t), st));
+    return 0;
+  }
+  Scratch S(st);
+  LiveSlot pred{slots, slot_bytes, fill, block_slots};
+  cub::CountingInputIterator<int64_t> it(0);
+  size_t tb = 0;
+  FK_TRY(cub::DeviceSelect::If(nullptr, tb, it, idx_out, count, n, pred, st));
+  void *tmp = S.get<char>(tb);
+  if (!tmp) return -(int)S.err;
+  FK_TRY(cub::DeviceSelect::If(tmp, tb, it, idx_out, count, n, pred, st));
   return 0;
 }
 

@@ -921,6 +921,62 @@ int fk_gqf_validate(const fk_gqf_geom *g, const fk_gqf_tables *t, int64_t *out, 
   }
 }
 
+int fk_gqf_cluster_stats(const fk_gqf_geom *g, const fk_gqf_tables *t, int64_t *out3, void *stream) {
+  if (!geom_ok(g) || !t || !out3) return FK_E_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  Scratch S(st);
+  const int64_t nw = g->phys >> 6;
+  int64_t *po = S.get<int64_t>(nw), *pr = S.get<int64_t>(nw), *oo = S.get<int64_t>(nw), *orr = S.get<int64_t>(nw);
+  if (S.err) return -(int)S.err;
+  k_word_popc<<<blocks_for(nw), 256, 0, st>>>(t->occupieds, nw, po);
+  k_word_popc<<<blocks_for(nw), 256, 0, st>>>(t->runends, nw, pr);
+  FK_TRY(cub_excl_sum_i64(S, po, oo, nw));
+  FK_TRY(cub_excl_sum_i64(S, pr, orr, nw));
+  int64_t h[4];
+  FK_TRY(cudaMemcpyAsync(&h[0], oo + nw - 1, 8, cudaMemcpyDeviceToHost, st));
+  FK_TRY(cudaMemcpyAsync(&h[1], po + nw - 1, 8, cudaMemcpyDeviceToHost, st));
+  FK_TRY(cudaMemcpyAsync(&h[2], orr + nw - 1, 8, cudaMemcpyDeviceToHost, st));
+  FK_TRY(cudaMemcpyAsync(&h[3], pr + nw - 1, 8, cudaMemcpyDeviceToHost, st));
+  FK_TRY(cudaStreamSynchronize(st));
+  const int64_t K = h[0] + h[1];
+  if (K != h[2] + h[3]) return FK_E_INVARIANT;  // occupieds / runends set-bit counts differ
+  out3[0] = out3[1] = out3[2] = 0;
+  if (K == 0) return 0;
+  int64_t *Q = S.get<int64_t>(K), *E = S.get<int64_t>(K), *brk = S.get<int64_t>(K), *len = S.get<int64_t>(K);
+  int64_t *cid = S.get<int64_t>(K), *ukey = S.get<int64_t>(K), *clen = S.get<int64_t>(K), *d3 = S.get<int64_t>(4);
+  if (S.err) return -(int)S.err;
+  k_bit_positions<<<blocks_for(nw), 256, 0, st>>>(t->occupieds, nw, oo, Q);
+  k_bit_positions<<<blocks_for(nw), 256, 0, st>>>(t->runends, nw, orr, E);
+  k_run_clusters<<<blocks_for(K), 256, 0, st>>>(Q, E, K, brk, len);
+  size_t tb = 0;
+  FK_TRY(cub::DeviceScan::InclusiveSum(nullptr, tb, brk, cid, K, st));
+  void *tmp = S.get<char>(tb);
+  if (!tmp) return -(int)S.err;
+  FK_TRY(cub::DeviceScan::InclusiveSum(tmp, tb, brk, cid, K, st));
+  // per-cluster lengths (sum of its runs' lengths: runs of a cluster are contiguous)
+  tb = 0;
+  FK_TRY(cub::DeviceReduce::ReduceByKey(nullptr, tb, cid, ukey, len, clen, d3, cuda::std::plus<>(), K, st));
+  tmp = S.get<char>(tb);
+  if (!tmp) return -(int)S.err;
+  FK_TRY(cub::DeviceReduce::ReduceByKey(tmp, tb, cid, ukey, len, clen, d3, cuda::std::plus<>(), K, st));
+  int64_t nc = 0;
+  FK_TRY(cudaMemcpyAsync(&nc, d3, 8, cudaMemcpyDeviceToHost, st));
+  FK_TRY(cudaStreamSynchronize(st));
+  tb = 0;
+  FK_TRY(cub::DeviceReduce::Max(nullptr, tb, clen, d3 + 1, nc, st));
+  tmp = S.get<char>(tb);
+  if (!tmp) return -(int)S.err;
+  FK_TRY(cub::DeviceReduce::Max(tmp, tb, clen, d3 + 1, nc, st));
+  tb = 0;
+  FK_TRY(cub::DeviceReduce::Sum(nullptr, tb, clen, d3 + 2, nc, st));
+  tmp = S.get<char>(tb);
+  if (!tmp) return -(int)S.err;
+  FK_TRY(cub::DeviceReduce::Sum(tmp, tb, clen, d3 + 2, nc, st));
+  FK_TRY(cudaMemcpyAsync(out3, d3, 3 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  FK_TRY(cudaStreamSynchronize(st));
+  return 0;
+}
+
 int fk_gqf_rebuild_index(const fk_gqf_geom *g, const fk_gqf_tables *t, void *stream) {
   if (!geom_ok(g) || !t) return FK_E_ARG;
   return rebuild_index(g, t, (cudaStream_t)stream);

@@ -250,6 +250,34 @@ __global__ void k_u8_bounds(const uint8_t *__restrict__ hs, int64_t n, int nseg,
   }
 }
 
+// ---- cluster statistics (Gqf.cluster_stats, gqf.py:416-428) ----------------
+// Positions of the set bits of a bit vector, word w's at off[w] onward.
+__global__ void k_bit_positions(const uint64_t *__restrict__ bv, int64_t nw, const int64_t *__restrict__ off,
+                                int64_t *__restrict__ pos) {
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t x = bv[w];
+    int64_t o = off[w];
+    while (x) {
+      pos[o++] = (w << 6) + __ffsll((long long)x) - 1;
+      x &= x - 1;
+    }
+  }
+}
+
+// Run k = occupied quotient Q[k] ending at E[k] (the k-th runend bit),
+// starting at max(Q[k], E[k-1] + 1); a cluster starts where Q[k] > E[k-1] + 1.
+// brk[k] = 1 at cluster starts, len[k] = run length.
+__global__ void k_run_clusters(const int64_t *__restrict__ Q, const int64_t *__restrict__ E, int64_t K,
+                               int64_t *__restrict__ brk, int64_t *__restrict__ len) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < K; k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t pe = k ? E[k - 1] : -2;
+    const bool b = k == 0 || Q[k] > pe + 1;
+    const int64_t start = b ? Q[k] : pe + 1;
+    brk[k] = b ? 1 : 0;
+    len[k] = E[k] - start + 1;
+  }
+}
+
 // ---- partitioned counting of plain counted inserts -------------------------
 // Counting the occurrences of a batch (insert of every occurrence, no delta
 // array) is a group-by on the fingerprint.  Instead of sorting every

@@ -379,15 +379,21 @@ class Gqf:
         return (int(s), int(e))
 
     def cluster_stats(self):
-        _, starts, ends = self._derive_structure()
-        if not len(starts):
+        """Max/mean/count of maximal contiguous used-slot spans (gqf.py:
+        416-428), by a global rank/select over the bit vectors on the device
+        (fk_gqf_cluster_stats)."""
+        out = np.zeros(3, dtype=np.int64)
+        with self._op_lock:
+            self._sync_in()
+            rc = self._lib.fk_gqf_cluster_stats(ctypes.byref(self._geom), ctypes.byref(self._tables(self._cur)),
+                                                out.ctypes.data_as(ctypes.c_void_p), _lib.stream_ptr(self._torch))
+        if rc == _lib.FK_E_INVARIANT:
+            raise ValidationError("occupieds and runends set-bit counts differ")
+        _lib.check(rc, "gqf cluster_stats")
+        num, longest, total = (int(x) for x in out)
+        if num == 0:
             return {"num_clusters": 0, "max_cluster": 0, "mean_cluster": 0.0}
-        brk = np.flatnonzero(starts[1:] > ends[:-1] + 1)
-        first = np.concatenate(([0], brk + 1))
-        last = np.concatenate((brk, [len(starts) - 1]))
-        lengths = ends[last] - starts[first] + 1
-        return {"num_clusters": int(len(lengths)), "max_cluster": int(lengths.max()),
-                "mean_cluster": float(lengths.mean())}
+        return {"num_clusters": num, "max_cluster": longest, "mean_cluster": total / num}
 
     def validate(self):
         """Structural invariants (gqf.py:430-492), checked on the device by

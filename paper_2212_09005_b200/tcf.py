@@ -31,7 +31,7 @@ from enum import IntEnum
 
 import numpy as np
 
-from . import _lib
+from . import _device, _lib
 from ._device import DeviceTables as _DeviceTables, check_backend as _check_backend
 from .errors import FilterFullError, ValidationError
 from .hashing import EMPTY, TOMBSTONE
@@ -383,16 +383,20 @@ class Tcf:
 
     # -- inspection (quiescent; host mirrors) ------------------------------------
     def items(self):
+        """All stored (block_index, tag, value) triples, backing entries with
+        block_index -1 (tcf.py:196-208); the live slots are selected on the
+        device (fk_live_slots), only they cross to the host."""
         p = self.params
         fmask = (1 << p.tag_bits) - 1
+        with self._op_lock:
+            self._t.before_device_op()
+            bi, bw = _device.live_slots(self._torch, self._lib, self._t, "blocks")
+            ki, kw = _device.live_slots(self._torch, self._lib, self._t, "backing")
         out = []
-        blocks, backing = self._t.peek("blocks"), self._t.peek("backing")
-        for i in np.flatnonzero(blocks > TOMBSTONE).tolist():
-            w = int(blocks[i])
-            out.append((i // p.block_slots, w & fmask, w >> p.tag_bits))
-        for i in np.flatnonzero(backing > TOMBSTONE).tolist():
-            w = int(backing[i])
-            out.append((-1, w & fmask, w >> p.tag_bits))
+        for idx, words, main in ((bi, bw, True), (ki, kw, False)):
+            w = [int(x) for x in words.tolist()]
+            blk = (idx // p.block_slots).tolist() if main else [-1] * len(w)
+            out.extend((b, x & fmask, x >> p.tag_bits) for b, x in zip(blk, w))
         return out
 
     def occupancy(self, block_index):

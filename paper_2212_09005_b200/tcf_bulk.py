@@ -24,7 +24,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from . import _lib
+from . import _device, _lib
 from ._device import DeviceTables as _DeviceTables, check_backend as _check_backend, keys_in as _keys_in
 from .errors import FilterFullError, ValidationError
 from .hashing import EMPTY, TOMBSTONE
@@ -277,14 +277,16 @@ class BulkTcf:
         return {"inserts_ok": int(c[0]), "inserts_backing": int(c[1]), "deletes_ok": int(c[2])}
 
     def items(self):
-        """All stored (block_index, word) pairs; backing entries get -1."""
+        """All stored (block_index, word) pairs; backing entries get -1
+        (tcf_bulk.py:342-352).  Each block's filled prefix and the live
+        backing slots are selected on the device (fk_live_slots)."""
         p = self.params
-        blocks, fill, backing = self._t.peek("blocks"), self._t.peek("fill"), self._t.peek("backing")
-        out = []
-        for b in np.flatnonzero(fill).tolist():
-            base = b * p.block_slots
-            out.extend((b, int(w)) for w in blocks[base:base + int(fill[b])].tolist())
-        out.extend((-1, int(w)) for w in backing[(backing != EMPTY) & (backing != TOMBSTONE)].tolist())
+        with self._op_lock:
+            self._t.before_device_op()
+            bi, bw = _device.live_slots(self._torch, self._lib, self._t, "blocks", "fill", p.block_slots)
+            ki, kw = _device.live_slots(self._torch, self._lib, self._t, "backing")
+        out = list(zip((bi // p.block_slots).tolist(), [int(x) for x in bw.tolist()]))
+        out.extend((-1, int(x)) for x in kw.tolist())
         return out
 
     _VMSG = ((1, "block %d fill over capacity"), (2, "block %d stores a reserved word"),

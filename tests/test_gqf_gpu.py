@@ -630,3 +630,34 @@ def test_partition_counting_overflow_falls_back(oracle, monkeypatch):
     assert o.bulk_insert(keys) == []
     same_image(g, o)
     assert g.count_many(base[7:8])[0] == o.count_many(base[7:8])[0]
+
+
+def _host_cluster_stats(g):
+    """The reference's cluster_stats (gqf.py:416-428) on the host mirrors."""
+    occ = np.unpackbits(g._occupieds.view(np.uint8), bitorder="little")
+    run = np.unpackbits(g._runends.view(np.uint8), bitorder="little")
+    quotients, ends = np.flatnonzero(occ), np.flatnonzero(run)
+    if not len(quotients):
+        return {"num_clusters": 0, "max_cluster": 0, "mean_cluster": 0.0}
+    starts = np.maximum(quotients, np.concatenate(([-1], ends[:-1])) + 1)
+    breaks = np.flatnonzero(starts[1:] > ends[:-1] + 1)
+    c_starts = np.concatenate(([0], breaks + 1))
+    c_ends = np.concatenate((breaks, [len(starts) - 1]))
+    lengths = ends[c_ends] - starts[c_starts] + 1
+    return {"num_clusters": int(len(lengths)), "max_cluster": int(lengths.max()),
+            "mean_cluster": float(lengths.mean())}
+
+
+@pytest.mark.parametrize("q,r,load", [(12, 8, 0.0), (14, 8, 0.5), (16, 16, 0.9), (20, 8, 0.93)])
+def test_cluster_stats_on_device_equal_reference_formula(q, r, load):
+    """Gqf.cluster_stats runs on the device (fk_gqf_cluster_stats): equal to
+    the reference's host derivation over the same image, empty table and
+    runs spilling into the padding included."""
+    from paper_2212_09005_b200 import Gqf
+    g = Gqf(q=q, r=r)
+    n = int(load * (1 << q) * 0.8)
+    if n:
+        rng = np.random.default_rng(q)
+        keys = rng.integers(0, 2 ** 63, n, dtype=np.uint64)
+        g.bulk_insert(np.concatenate([keys, keys[: n // 5]]))
+    assert g.cluster_stats() == _host_cluster_stats(g)

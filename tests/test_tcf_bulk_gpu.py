@@ -211,3 +211,22 @@ def test_route_modes_bit_exact(oracle, monkeypatch, mode):
         keys = counter_keys(50 + s, n)
         assert np.array_equal(f.insert_batch(keys), o.insert_batch(keys)), s
         _same(f, o)
+
+
+def test_items_selected_on_device():
+    """BulkTcf.items selects each block's filled prefix and the live backing
+    slots on the device (fk_live_slots): the reference's (block, word) list
+    (tcf_bulk.py:342-352), in its order."""
+    from paper_2212_09005_b200 import BulkTcf
+    f = BulkTcf(num_blocks=256)
+    keys = counter_keys(93, int(256 * 128 * 1.03))  # overfill: backing entries
+    f.insert_batch(keys)
+    f.delete_batch(keys[::9])
+    p = f.params
+    blocks, fill, backing = f._blocks, f._fill, f._backing
+    want = []
+    for b in range(p.num_blocks):
+        want.extend((b, int(w)) for w in blocks[b * p.block_slots:b * p.block_slots + int(fill[b])].tolist())
+    want.extend((-1, int(w)) for w in backing[backing > 1].tolist())
+    assert any(b == -1 for b, _ in want)
+    assert f.items() == want

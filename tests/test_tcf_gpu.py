@@ -351,3 +351,25 @@ def test_ordered_batches_past_32bit_index_chunk_exactly(oracle, monkeypatch):
     assert np.array_equal(got, o.delete_many(d))
     _same_tables(f, o)
     assert f.counters == o.counters
+
+
+@pytest.mark.parametrize("kw", [{}, dict(tag_bits=12, slot_bits=16), dict(tag_bits=16, slot_bits=32)])
+def test_items_selected_on_device(oracle, kw):
+    """Tcf.items selects the live slots on the device (fk_live_slots): the
+    same (block, tag, value) triples, in the same order, as the reference's
+    scan of the image (tcf.py:196-208), backing entries included."""
+    from paper_2212_09005_b200 import Tcf
+    f = Tcf(num_blocks=512, **kw)
+    keys = counter_keys(91, int(512 * 16 * 1.02))  # overfill: some land in the backing table
+    vb = f.params.value_bits
+    vals = (keys % (1 << vb)).astype(np.uint64) if vb else None
+    f.insert_many(keys, vals)
+    f.delete_many(keys[::7])
+    p = f.params
+    fm = (1 << p.tag_bits) - 1
+    blocks, backing = f._blocks, f._backing
+    want = [(i // p.block_slots, int(blocks[i]) & fm, int(blocks[i]) >> p.tag_bits)
+            for i in np.flatnonzero(blocks > 1).tolist()]
+    want += [(-1, int(backing[i]) & fm, int(backing[i]) >> p.tag_bits) for i in np.flatnonzero(backing > 1).tolist()]
+    assert any(b == -1 for b, _, _ in want)
+    assert f.items() == want
