@@ -258,6 +258,44 @@ def zipf_queries(torch, filt, keys, stream, s=1.5, reps=3):
             "how": "query_many of %d keys with Zipf(%.1f) ranks over the inserted keys" % (n, s)}
 
 
+def zipf_inserts(torch, f, keys, stream, s=1.5, reps=2):
+    """Zipfian 64-bit keys into a fresh table (north star: "uniform and
+    Zipfian 64-bit keys"): one insert per inserted-key slot of the uniform
+    run, the key drawn with the reference's bounded Zipf(s) ranks over the
+    uniform keys (fk/workloads.py:81-118; 2^24 host draws tiled), so the hot
+    keys repeat millions of times, fill their two blocks and backing chain,
+    and the rest come back FULL.  Concurrent mode only: the ordered mode
+    serialises every copy of a key on its blocks (one round each) by design."""
+    from paper_2212_09005_b200.workloads import zipf_bounded
+    n = keys.numel()
+    rng = np.random.default_rng(54321)
+    ranks = torch.from_numpy(zipf_bounded(rng, s, n, 1 << 24) - 1).to(keys.device)
+    q = keys[ranks.repeat((n + ranks.numel() - 1) // ranks.numel())[:n]]
+    ms = []
+    for _ in range(reps + 1):
+        f._reset()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        codes = f.insert_many(q)
+        b.record(stream)
+        b.synchronize()
+        ms.append(a.elapsed_time(b))
+    ms = float(np.mean(ms[1:]))
+    hist = torch.bincount(codes.to(torch.int64), minlength=4).tolist()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    found = f.query_many(q)
+    b.record(stream)
+    b.synchronize()
+    qms = a.elapsed_time(b)
+    return {"insert_ops_per_s": n / (ms / 1e3), "insert_ms": ms, "query_ops_per_s": n / (qms / 1e3),
+            "query_ms": qms, "zipf_s": s, "distinct_keys": int(torch.unique(q).numel()),
+            "codes": {"primary": hist[0], "secondary": hist[1], "backing": hist[2], "full": hist[3]},
+            "all_found": bool(found.all()),
+            "how": "concurrent-mode insert_many of %d keys with Zipf(%.1f) ranks over the uniform keys, then "
+                   "query_many of the same stream" % (n, s)}
+
+
 def concurrent_mode(torch, nb, args, keys, negs, stream, ceiling=None, steps=2):
     """The paper's free-threaded CAS mode on the same workload (secondary
     numbers; not bit-identical to the sequential reference)."""
@@ -286,6 +324,7 @@ def concurrent_mode(torch, nb, args, keys, negs, stream, ceiling=None, steps=2):
         for op in out:
             out[op]["frac_of_random_access_ceiling"] = out[op]["ops_per_s"] / op_ceiling(op, ceiling)
     out["step_ops_per_s"] = 4 * n / (sum(np.mean(v) for v in res.values()) / 1e3)
+    out["zipf_inserts"] = zipf_inserts(torch, f, keys, stream)
     del f
     torch.cuda.empty_cache()
     return out

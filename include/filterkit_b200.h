@@ -335,6 +335,15 @@ int fk_gqf_cluster_stats(const fk_gqf_geom *g, const fk_gqf_tables *t, int64_t *
 int fk_live_slots(const void *slots, int slot_bytes, int64_t n, const uint32_t *fill, int block_slots,
                   int64_t *idx_out, int64_t *count, void *stream);
 
+/* ---- device key generation -------------------------------- */
+
+/* k-mer windows (workloads.py:147-191): seq (device, n bytes) holds the
+ * reads' bases with one non-ACGT separator byte between reads; out (device
+ * u64[n]) gets the 2-bit packed value (A=0 C=1 G=2 T=3, first base most
+ * significant) of every k-window (1 <= k <= 32) made of ACGT bases only, in
+ * position order, *count (device int64) their number.  Asynchronous. */
+int fk_kmer_windows(const uint8_t *seq, int64_t n, int k, uint64_t *out, int64_t *count, void *stream);
+
 /* ---- hash-prefix sharding (new in this build) -------------- */
 
 /* Stable partition of a key batch by owner shard, owner = bits

@@ -88,6 +88,7 @@ _SIGS = {
     "fk_backing_delete_batch": (c_i32, [ctypes.POINTER(BtcfGeom), c_vp, c_vp, c_i64, c_vp, ctypes.POINTER(c_i64),
                                         c_vp]),
     "fk_gqf_cluster_stats": (c_i32, [ctypes.POINTER(GqfGeom), ctypes.POINTER(GqfTables), c_vp, c_vp]),
+    "fk_kmer_windows": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp, c_vp]),
     "fk_live_slots": (c_i32, [c_vp, c_i32, c_i64, c_vp, c_i32, c_vp, c_vp, c_vp]),
     "fk_shard_partition": (c_i32, [c_vp, c_vp, c_i64, c_u64, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "fk_shard_unpermute": (c_i32, [c_vp, c_vp, c_i64, c_i32, c_vp, c_vp]),

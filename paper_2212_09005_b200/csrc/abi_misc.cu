@@ -186,6 +186,35 @@ int fk_fastmod_check(const uint64_t *x, int64_t n, uint64_t d, uint64_t *out, vo
   return 0;
 }
 
+// k-mer windows (fk/workloads.py:147-191) on the device: seq holds the
+// reads' bases, reads separated by a non-ACGT byte, so a window is valid
+// iff its k bytes are all ACGT (either case); valid windows are kept in
+// position order by the stream compaction.
+__device__ __forceinline__ int base_code(uint8_t c) {
+  switch (c | 0x20) {  // lowercase
+    case 'a': return 0;
+    case 'c': return 1;
+    case 'g': return 2;
+    case 't': return 3;
+    default: return -1;
+  }
+}
+
+__global__ void k_kmer_windows(const uint8_t *__restrict__ seq, int64_t m, int k, uint64_t *__restrict__ val,
+                               uint8_t *__restrict__ ok) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t v = 0;
+    bool good = true;
+    for (int j = 0; j < k; j++) {
+      const int c = base_code(seq[i + j]);
+      good &= c >= 0;
+      v = (v << 2) | (uint64_t)(c & 3);
+    }
+    val[i] = v;
+    ok[i] = good ? 1 : 0;
+  }
+}
+
 // Tcf.items / BulkTcf.items on the device (fk/tcf.py:196-208,
 // fk/tcf_bulk.py:342-352): positions of the live slots, ascending.
 int fk_live_slots(const void *slots, int slot_bytes, int64_t n, const uint32_t *fill, int block_slots,
@@ -205,6 +234,29 @@ int fk_live_slots(const void *slots, int slot_bytes, int64_t n, const uint32_t *
   void *tmp = S.get<char>(tb);
   if (!tmp) return -(int)S.err;
   FK_TRY(cub::DeviceSelect::If(tmp, tb, it, idx_out, count, n, pred, st));
+  return 0;
+}
+
+int fk_kmer_windows(const uint8_t *seq, int64_t n, int k, uint64_t *out, int64_t *count, void *stream) {
+  if (n < 0 || k < 1 || k > 32 || !out || !count) return FK_E_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t m = n - k + 1;
+  if (m <= 0) {
+    FK_TRY(cudaMemsetAsync(count, 0, sizeof(int64_t), st));
+    return 0;
+  }
+  Scratch S(st);
+  uint64_t *val = S.get<uint64_t>(m);
+  uint8_t *ok = S.get<uint8_t>(m);
+  if (S.err) return -(int)S.err;
+  int64_t g = (m + 255) / 256, cap = (int64_t)num_sms() * 16;
+  k_kmer_windows<<<(int)(g < cap ? g : cap), 256, 0, st>>>(seq, m, k, val, ok);
+  FK_CHECK_LAUNCH();
+  size_t tb = 0;
+  FK_TRY(cub::DeviceSelect::Flagged(nullptr, tb, val, ok, out, count, m, st));
+  void *tmp = S.get<char>(tb);
+  if (!tmp) return -(int)S.err;
+  FK_TRY(cub::DeviceSelect::Flagged(tmp, tb, val, ok, out, count, m, st));
   return 0;
 }
 

@@ -661,3 +661,33 @@ def test_cluster_stats_on_device_equal_reference_formula(q, r, load):
         keys = rng.integers(0, 2 ** 63, n, dtype=np.uint64)
         g.bulk_insert(np.concatenate([keys, keys[: n // 5]]))
     assert g.cluster_stats() == _host_cluster_stats(g)
+
+
+@pytest.mark.parametrize("q", [10, 16])
+def test_r32_point_bulk_and_counts_vs_oracle(oracle, q):
+    """32-bit remainders (GqfParams admits r = 32, gqf.py:52-95; u32 slots):
+    point and bulk counted inserts, counts, bulk and point deletes and the
+    image equal the oracle's."""
+    from paper_2212_09005_b200 import Gqf
+    rng = np.random.default_rng(q + 32)
+    n = int(0.6 * (1 << q))
+    keys = rng.integers(0, 2 ** 63, n, dtype=np.uint64)
+    g = Gqf(q=q, r=32)
+    o = _oracle(g, oracle)
+    assert g._slots.dtype == np.uint32
+    g.bulk_insert(np.concatenate([keys, keys[: n // 3]]))
+    assert o.bulk_insert(np.concatenate([keys, keys[: n // 3]])) == []
+    same_image(g, o)
+    extra = rng.integers(0, 2 ** 63, n // 10, dtype=np.uint64)
+    cnt = rng.integers(1, 300, n // 10).astype(np.uint64)
+    g.insert_many(extra, cnt)
+    o.insert_many(extra, cnt)
+    same_image(g, o)
+    probe = np.concatenate([keys[::3], extra, rng.integers(0, 2 ** 63, 2000, dtype=np.uint64)])
+    assert np.array_equal(g.count_many(probe), o.count_many(probe))
+    d = np.concatenate([keys[::2], keys[:50]])
+    assert np.array_equal(g.bulk_delete(d), o.bulk_delete(d))
+    same_image(g, o)
+    assert np.array_equal(g.delete_many(extra[:100], cnt[:100]), o.delete_many(extra[:100], cnt[:100]))
+    same_image(g, o)
+    g.validate()

@@ -84,3 +84,15 @@ def test_counter_stream_device_matches_host():
     torch.cuda.synchronize()
     assert np.array_equal(out[1:].cpu().numpy().view(np.uint64), full[999:4999])
     assert int(out[0]) == 0
+
+
+def test_kmer_windows_device_match_reference_golden(golden, tmp_path):
+    """Device k-mer extraction (fk_kmer_windows) equals the reference's
+    windows on its fixture, for every k, in order."""
+    from paper_2212_09005_b200.workloads import kmer_windows_device
+    g = golden("kmer")
+    p = tmp_path / "reads.fq"
+    p.write_bytes(g["text"].tobytes())
+    for k in (1, 4, 11, 21, 31, 32):
+        got = kmer_windows_device(str(p), k).cpu().numpy().view(np.uint64)
+        assert np.array_equal(got, g["k%d" % k]), k

@@ -109,3 +109,14 @@ def test_gqf_duplicates_and_capacity(golden):
     code, idx = o.insert_many(t["cap_k"])
     assert (code != 0) == bool(t["cap_err"][0])
     _same_image(o, t, "cap_")
+
+
+def test_kmer_windows_host_match_reference_golden(golden, tmp_path):
+    """The host k-mer extractor (and the read parser the device path shares)
+    equals the reference's on its own fixture (tests/golden/kmer.npz)."""
+    from paper_2212_09005_b200.workloads import kmer_windows
+    g = golden("kmer")
+    p = tmp_path / "reads.fq"
+    p.write_bytes(g["text"].tobytes())
+    for k in (1, 4, 11, 21, 31, 32):
+        assert np.array_equal(kmer_windows(str(p), k), g["k%d" % k]), k
