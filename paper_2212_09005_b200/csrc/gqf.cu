@@ -333,6 +333,13 @@ int part_count(Scratch &S, const uint64_t *keys, int keys_are_fps, uint64_t seed
   return 0;
 }
 
+// region-parallel placement of the canonical rebuild (k_region_*); FK_GQF_REGION_PLACE=0
+// keeps the global max-plus scan and item-parallel writes
+inline bool region_place_enabled() {
+  const char *e = getenv("FK_GQF_REGION_PLACE");
+  return !e || atoi(e) != 0;
+}
+
 inline int64_t small_batch_limit(const fk_gqf_geom *g) {
   const char *e = getenv("FK_GQF_SMALL");
   if (e) return atoll(e);
@@ -676,38 +683,82 @@ int apply_t(const fk_gqf_geom *g, const fk_gqf_tables *cur, const fk_gqf_tables 
   if (S.err) return -(int)S.err;
   if (G > 0) FK_CU(cub_merge(S, o2_fp, o2_cnt, hn[0], u2_fp, u2_cnt, hn[2], it_fp, it_cnt));
 
-  // 11. placement: max-plus scan gives every item's last slot
-  MaxPlus *terms = S.get<MaxPlus>(G), *ends = S.get<MaxPlus>(G);
-  uint64_t *L = S.get<uint64_t>(G);
-  if (S.err) return -(int)S.err;
-  if (G > 0) {
-    k_place_terms<<<blocks_for(G), 256, 0, st>>>(it_fp, it_cnt, G, g->r, terms, L);
-    FK_CU(cub_maxplus_scan(S, terms, ends, G));
-  }
-
-  // 12. would the sequential reference have raised?  (inserts only)
+  // 11-12. placement and the capacity predicates.  Region placement
+  // (default): per-region max-plus summaries, a scan over the regions, then
+  // one CTA per region writes its whole slot range of `next` and reports a
+  // broken layout; the result is used unless the batch needs the exact path.
   bool exact = (flags & kApplyForceExact) != 0, load_possible = exact;
-  if (!is_del && G > 0 && !exact) {
-    int64_t *cfirst = S.get<int64_t>(G), *cfs = S.get<int64_t>(G);
-    unsigned *flags = S.get<unsigned>(4);
+  bool region_done = false;
+  unsigned long long region_shift = 0;
+  MaxPlus *ends = nullptr;
+  uint64_t *L = nullptr;
+  if (!exact && region_place_enabled()) {
+    const int64_t nqr = g->quotient_regions;
+    int64_t *ib = S.get<int64_t>(nqr + 1);
+    MaxPlus *summ = S.get<MaxPlus>(nqr), *cum = S.get<MaxPlus>(nqr);
+    unsigned long long *acc = S.get<unsigned long long>(4);  // [0] slots, [1] counts, [2] shift
+    unsigned *rflags = S.get<unsigned>(2);                   // [0] broken layout, [1] not ascending
     if (S.err) return -(int)S.err;
-    FK_CU(cudaMemsetAsync(flags, 0, 4 * sizeof(unsigned), st));
-    k_cluster_check<<<blocks_for(G), 256, 0, st>>>(it_fp, ends, G, g->r, g->phys, cfirst, flags);
-    FK_CU(cub_max_scan_i64(S, cfirst, cfs, G));
-    k_cluster_check2<<<blocks_for(G), 256, 0, st>>>(ends, cfs, cfirst, G, g->phys, flags);
-    int64_t *occ_sum = S.get<int64_t>(4);
-    if (S.err) return -(int)S.err;
-    FK_CU(cudaMemsetAsync(occ_sum, 0, 4 * sizeof(int64_t), st));
-    k_stats<<<blocks_for(G), 256, 0, st>>>(it_cnt, L, G, occ_sum);
-    unsigned h_flags = 0;
-    int64_t h_occ = 0;
-    FK_CU(cudaMemcpyAsync(&h_flags, flags, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
-    FK_CU(cudaMemcpyAsync(&h_occ, occ_sum, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    FK_CU(cudaMemsetAsync(acc, 0, 4 * sizeof(unsigned long long), st));
+    FK_CU(cudaMemsetAsync(rflags, 0, 2 * sizeof(unsigned), st));
+    if (G > 0) k_region_bounds<<<blocks_for(nqr + 1), 256, 0, st>>>(it_fp, G, g->r + kRegionBits, nqr, ib);
+    else FK_CU(cudaMemsetAsync(ib, 0, (nqr + 1) * sizeof(int64_t), st));
+    const int rgrid = (int)(nqr < (int64_t)num_sms() * 8 ? nqr : (int64_t)num_sms() * 8);
+    k_region_summary<<<rgrid, kRegThreads, 0, st>>>(it_fp, it_cnt, ib, nqr, g->r, summ, acc);
+    FK_CU(cub_maxplus_scan(S, summ, cum, nqr));
+    if (order == FK_ORDER_POINT)  // point order: the shift metric counts the batch's own slots unless ascending
+      k_not_ascending<<<blocks_for(n), 256, 0, st>>>(keys, keys_are_fps, g->seed, fmask, n, rflags + 1);
+    k_region_place<S_t><<<rgrid, kRegThreads, 0, st>>>(make_dev(g, nxt), reinterpret_cast<const S_t *>(cur->slots),
+                                                       cur->runends, it_fp, it_cnt, ib, cum, nqr, rflags + 1,
+                                                       order == FK_ORDER_BULK ? 1 : 0, rflags, acc + 2);
+    k_region_stats<<<1, 1, 0, st>>>(acc, G, nxt->stats);
+    unsigned long long hacc[3];
+    unsigned hfl = 0;
+    FK_CU(cudaMemcpyAsync(hacc, acc, sizeof(hacc), cudaMemcpyDeviceToHost, st));
+    FK_CU(cudaMemcpyAsync(&hfl, rflags, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
     FK_CU(cudaStreamSynchronize(st));
-    // every item's pre-insert occupancy is <= the final one, so a final
-    // occupancy below the ceiling rules LOAD_CAPACITY out for any order
-    exact = h_flags != 0 || h_occ >= g->max_occupied;
-    load_possible = h_occ >= g->max_occupied;
+    FK_CHECK_LAUNCH();
+    const int64_t h_occ = (int64_t)hacc[0];
+    if (!is_del) {
+      // every item's pre-insert occupancy is <= the final one, so a final
+      // occupancy below the ceiling rules LOAD_CAPACITY out for any order
+      exact = hfl != 0 || h_occ >= g->max_occupied;
+      load_possible = h_occ >= g->max_occupied;
+    }
+    region_done = hfl == 0;  // (a delete never breaks the layout of a valid table)
+    region_shift = hacc[2];
+  }
+  if (!region_done && !exact) {
+    // global placement: max-plus scan over every item
+    MaxPlus *terms = S.get<MaxPlus>(G);
+    ends = S.get<MaxPlus>(G);
+    L = S.get<uint64_t>(G);
+    if (S.err) return -(int)S.err;
+    if (G > 0) {
+      k_place_terms<<<blocks_for(G), 256, 0, st>>>(it_fp, it_cnt, G, g->r, terms, L);
+      FK_CU(cub_maxplus_scan(S, terms, ends, G));
+    }
+    // would the sequential reference have raised?  (inserts only)
+    if (!is_del && G > 0) {
+      int64_t *cfirst = S.get<int64_t>(G), *cfs = S.get<int64_t>(G);
+      unsigned *cflags = S.get<unsigned>(4);
+      if (S.err) return -(int)S.err;
+      FK_CU(cudaMemsetAsync(cflags, 0, 4 * sizeof(unsigned), st));
+      k_cluster_check<<<blocks_for(G), 256, 0, st>>>(it_fp, ends, G, g->r, g->phys, cfirst, cflags);
+      FK_CU(cub_max_scan_i64(S, cfirst, cfs, G));
+      k_cluster_check2<<<blocks_for(G), 256, 0, st>>>(ends, cfs, cfirst, G, g->phys, cflags);
+      int64_t *occ_sum = S.get<int64_t>(4);
+      if (S.err) return -(int)S.err;
+      FK_CU(cudaMemsetAsync(occ_sum, 0, 4 * sizeof(int64_t), st));
+      k_stats<<<blocks_for(G), 256, 0, st>>>(it_cnt, L, G, occ_sum);
+      unsigned h_flags = 0;
+      int64_t h_occ = 0;
+      FK_CU(cudaMemcpyAsync(&h_flags, cflags, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+      FK_CU(cudaMemcpyAsync(&h_occ, occ_sum, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+      FK_CU(cudaStreamSynchronize(st));
+      exact = h_flags != 0 || h_occ >= g->max_occupied;
+      load_possible = h_occ >= g->max_occupied;
+    }
   }
 
   if (flags & kApplyDry) {
@@ -829,6 +880,14 @@ int apply_t(const fk_gqf_geom *g, const fk_gqf_tables *cur, const fk_gqf_tables 
   }
 
   // 13. canonical rebuild into `next`
+  if (region_done) {  // already written region by region
+    int rc = rebuild_index(g, nxt, st);
+    if (rc) return rc;
+    res->shifted = (int64_t)region_shift;
+    res->swapped = 1;
+    FK_CHECK_LAUNCH();
+    return 0;
+  }
   GqfDev T1 = make_dev(g, nxt);
   FK_CU(cudaMemsetAsync(nxt->slots, 0, (size_t)g->phys * sizeof(S_t), st));
   FK_CU(cudaMemsetAsync(nxt->occupieds, 0, (size_t)(g->phys >> 6) * 8, st));

@@ -886,6 +886,279 @@ __global__ void k_stats(const uint64_t *__restrict__ cnt, const uint64_t *__rest
   }
 }
 
+// ---- region-parallel placement of the canonical rebuild -----------------------
+// The merged items (sorted, canonical counts) are placed region by region:
+//   k_region_summary: one CTA per 8192-quotient region composes its items'
+//     max-plus terms in order (item i maps the end e of everything before it
+//     to max(a_i, e + L_i)), preceded by the clamp e -> max(region start - 1, e);
+//   an inclusive scan of the region summaries gives every region's incoming
+//   end e_in (the spill of earlier regions' runs);
+//   k_region_place: one CTA per region places its items from e_in and writes
+//     its whole responsibility range [P_g, P_g+1) of the new image -- slots
+//     (zeros between clusters), runend bits (atomics only on the boundary
+//     words), its occupieds words, its offset -- so the second image needs
+//     no clearing pass; it counts (slot, runend) changes against the old
+//     image (the shift metric) and flags the canonical layout as unusable
+//     when a cluster would span three regions or pass the table's end (the
+//     reference's CLUSTER / SHIFT_BOUND conditions: the exact path runs).
+constexpr int kRegThreads = 256;
+constexpr int64_t kRegMaxRange = 3 * kRegionSlots;  // a valid region's slot range is < 2 regions
+
+__device__ __forceinline__ MaxPlus mp_id() {
+  MaxPlus m;
+  m.a = kNegInf;
+  m.b = 0;
+  return m;
+}
+
+__device__ __forceinline__ MaxPlus mp_op(const MaxPlus &l, const MaxPlus &rr) {  // l first, then rr
+  MaxPlus o;
+  const int64_t t = l.a + rr.b;
+  o.a = rr.a > t ? rr.a : t;
+  o.b = l.b + rr.b;
+  return o;
+}
+
+__device__ __forceinline__ MaxPlus item_term(const uint64_t *fp, const uint64_t *cnt, int64_t i, int64_t a, int r,
+                                             int64_t *Lout) {
+  const uint64_t f = fp[i];
+  const uint64_t L = enc_len(f & ((1ull << r) - 1), cnt[i], r);
+  const int64_t Ls = L > (1ull << 50) ? (1LL << 50) : (int64_t)L;
+  const bool first = i == a || (fp[i - 1] >> r) != (f >> r);
+  MaxPlus m;
+  m.a = first ? (int64_t)(f >> r) + Ls - 1 : kNegInf;
+  m.b = Ls;
+  *Lout = Ls;
+  return m;
+}
+
+// Exclusive (in thread order) max-plus prefix of every thread's value, and
+// the block total.  All threads call it.
+__device__ __forceinline__ MaxPlus block_excl_mp(MaxPlus v, MaxPlus *sw, MaxPlus *total) {
+  const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  MaxPlus inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    MaxPlus y;
+    y.a = __shfl_up_sync(0xFFFFFFFFu, inc.a, o);
+    y.b = __shfl_up_sync(0xFFFFFFFFu, inc.b, o);
+    if ((int)lane >= o) inc = mp_op(y, inc);
+  }
+  MaxPlus ex;
+  ex.a = __shfl_up_sync(0xFFFFFFFFu, inc.a, 1);
+  ex.b = __shfl_up_sync(0xFFFFFFFFu, inc.b, 1);
+  if (lane == 0) ex = mp_id();
+  if (lane == 31) sw[warp] = inc;
+  __syncthreads();
+  MaxPlus wp = mp_id();
+  for (int w = 0; w < (int)warp; w++) wp = mp_op(wp, sw[w]);
+  MaxPlus t = mp_id();
+  for (int w = 0; w < kRegThreads / 32; w++) t = mp_op(t, sw[w]);
+  *total = t;
+  __syncthreads();
+  return mp_op(wp, ex);
+}
+
+__global__ void __launch_bounds__(kRegThreads) k_region_summary(const uint64_t *__restrict__ fp,
+                                                                const uint64_t *__restrict__ cnt,
+                                                                const int64_t *__restrict__ ib, int64_t nqr, int r,
+                                                                MaxPlus *__restrict__ summ,
+                                                                unsigned long long *__restrict__ acc) {
+  __shared__ MaxPlus sw[kRegThreads / 32];
+  for (int64_t g = blockIdx.x; g < nqr; g += gridDim.x) {
+    const int64_t a = ib[g], e = ib[g + 1], n = e - a;
+    const int64_t c = (n + kRegThreads - 1) / kRegThreads;
+    const int64_t i0 = a + (int64_t)threadIdx.x * c, i1 = min(e, i0 + c);
+    MaxPlus v = mp_id();
+    unsigned long long ls = 0, cs = 0;
+    for (int64_t i = i0; i < i1; i++) {
+      int64_t L;
+      v = mp_op(v, item_term(fp, cnt, i, a, r, &L));
+      ls += (unsigned long long)L;
+      cs += cnt[i];
+    }
+    MaxPlus tot;
+    block_excl_mp(v, sw, &tot);
+    if (threadIdx.x == 0) {
+      MaxPlus clamp;
+      clamp.a = (g << kRegionBits) - 1;
+      clamp.b = 0;
+      summ[g] = mp_op(clamp, tot);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      ls += __shfl_xor_sync(0xFFFFFFFFu, ls, o);
+      cs += __shfl_xor_sync(0xFFFFFFFFu, cs, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+      if (ls) atomicAdd(&acc[0], ls);
+      if (cs) atomicAdd(&acc[1], cs);
+    }
+  }
+}
+
+__device__ __forceinline__ int64_t mp_end(const MaxPlus &m) {  // applied to e = -1
+  const int64_t t = m.b - 1;
+  return m.a > t ? m.a : t;
+}
+
+// Bit j of *chg: slot j of the 64-slot word differs between a and b; of
+// *nz: a's slot j is non-zero.  16-byte vector loads (the word is aligned).
+template <typename S>
+__device__ __forceinline__ void word_slot_masks(const S *a, const S *b, unsigned long long *chg,
+                                                unsigned long long *nz) {
+  constexpr int PER = 16 / (int)sizeof(S), V = 64 / PER;
+  const uint4 *va = reinterpret_cast<const uint4 *>(a), *vb = reinterpret_cast<const uint4 *>(b);
+  unsigned long long c = 0, z = 0;
+#pragma unroll
+  for (int v = 0; v < V; v++) {
+    const uint4 x = va[v], y = vb[v];
+    const S *xs = reinterpret_cast<const S *>(&x), *ys = reinterpret_cast<const S *>(&y);
+#pragma unroll
+    for (int j = 0; j < PER; j++) {
+      c |= (unsigned long long)(xs[j] != ys[j]) << (v * PER + j);
+      z |= (unsigned long long)(xs[j] != 0) << (v * PER + j);
+    }
+  }
+  *chg = c;
+  *nz = z;
+}
+
+// flags[0] |= 1: the canonical layout breaks the reference's bounds (a
+// cluster spans three regions / passes the table end): use the exact path.
+template <typename S>
+__global__ void __launch_bounds__(kRegThreads) k_region_place(GqfDev T1, const S *__restrict__ old_slots,
+                                                              const uint64_t *__restrict__ old_run,
+                                                              const uint64_t *__restrict__ fp,
+                                                              const uint64_t *__restrict__ cnt,
+                                                              const int64_t *__restrict__ ib,
+                                                              const MaxPlus *__restrict__ cum, int64_t nqr,
+                                                              const unsigned *__restrict__ not_asc, int bulk_order,
+                                                              unsigned *__restrict__ flags,
+                                                              unsigned long long *__restrict__ diff) {
+  __shared__ MaxPlus sw[kRegThreads / 32];
+  __shared__ unsigned long long s_run[kRegMaxRange / 64 + 2];
+  __shared__ unsigned long long s_occ[kRegionSlots / 64];
+  __shared__ int s_cs, s_bad;
+  S *slots = reinterpret_cast<S *>(T1.slots);
+  const int r = T1.r;
+  const int64_t phys = T1.phys;
+  const bool old_only = bulk_order || !*not_asc;
+  unsigned long long ndiff = 0;
+  for (int64_t g = blockIdx.x; g < nqr; g += gridDim.x) {
+    const int64_t base = g << kRegionBits;
+    const int64_t e_in = g ? mp_end(cum[g - 1]) : -1;     // end of every earlier region's runs
+    const int64_t e_out = mp_end(cum[g]);                  // >= base - 1 (the summary is clamped)
+    const int64_t P0 = e_in + 1 > base ? e_in + 1 : base;
+    int64_t P1 = g + 1 < nqr ? (e_out + 1 > base + kRegionSlots ? e_out + 1 : base + kRegionSlots) : phys;
+    if (threadIdx.x == 0) {
+      s_cs = 0;
+      s_bad = 0;
+      // the offsets of this region (and of the padding region after the last one)
+      T1.offs[g] = (int32_t)(e_in + 1 > base ? e_in + 1 - base : 0);
+      if (g + 1 == nqr)
+        for (int64_t h = nqr; h < T1.nregions; h++) {
+          const int64_t bh = h << kRegionBits;
+          T1.offs[h] = (int32_t)(e_out + 1 > bh ? e_out + 1 - bh : 0);
+        }
+    }
+    for (int i = threadIdx.x; i < kRegMaxRange / 64 + 2; i += kRegThreads) s_run[i] = 0;
+    for (int i = threadIdx.x; i < kRegionSlots / 64; i += kRegThreads) s_occ[i] = 0;
+    __syncthreads();
+    bool bad = e_out >= phys || P1 > phys || P1 - P0 > kRegMaxRange;
+    if (!bad) {  // zero the range: ragged ends slot by slot, the middle in 16-byte stores
+      constexpr int PER = 16 / (int)sizeof(S);
+      const int64_t q0 = (P0 + PER - 1) / PER * PER, q1 = P1 / PER * PER;
+      if (q0 >= q1) {
+        for (int64_t p = P0 + threadIdx.x; p < P1; p += kRegThreads) slots[p] = 0;
+      } else {
+        for (int64_t p = P0 + threadIdx.x; p < q0; p += kRegThreads) slots[p] = 0;
+        for (int64_t p = q1 + threadIdx.x; p < P1; p += kRegThreads) slots[p] = 0;
+        uint4 *v = reinterpret_cast<uint4 *>(slots + q0);
+        for (int64_t j = threadIdx.x; j < (q1 - q0) / PER; j += kRegThreads) v[j] = make_uint4(0, 0, 0, 0);
+      }
+    }
+    __syncthreads();
+    // place: per-thread chunks composed in order, then each item's end
+    const int64_t a = ib[g], e = ib[g + 1], n = e - a;
+    const int64_t c = (n + kRegThreads - 1) / kRegThreads;
+    const int64_t i0 = a + (int64_t)threadIdx.x * c, i1 = min(e, i0 + c);
+    MaxPlus v = mp_id();
+    for (int64_t i = i0; i < i1; i++) {
+      int64_t L;
+      v = mp_op(v, item_term(fp, cnt, i, a, r, &L));
+    }
+    MaxPlus tot;
+    const MaxPlus pre = block_excl_mp(v, sw, &tot);
+    int64_t run_end = pre.b + e_in > pre.a ? pre.b + e_in : pre.a;  // end of everything before my chunk
+    const int64_t w0 = P0 >> 6;
+    for (int64_t i = i0; i < i1 && !bad; i++) {
+      int64_t L;
+      const MaxPlus t = item_term(fp, cnt, i, a, r, &L);
+      const int64_t prev = run_end;
+      run_end = t.a > prev + L ? t.a : prev + L;
+      const uint64_t f = fp[i];
+      const int64_t quot = (int64_t)(f >> r);
+      const bool first = t.a != kNegInf;
+      const bool last = i + 1 == e || (fp[i + 1] >> r) != (f >> r);
+      if (first) {
+        if (quot > prev + 1) s_cs = 1;  // a cluster starts in this region
+        atomicOr(&s_occ[(quot - base) >> 6], 1ull << (quot & 63));
+      }
+      if (run_end >= P1) {  // (only with a broken layout)
+        s_bad = 1;
+        break;
+      }
+      enc_write<S>(slots, run_end - L + 1, f & ((1ull << r) - 1), cnt[i], r);
+      if (last) atomicOr(&s_run[(run_end >> 6) - w0], 1ull << (run_end & 63));
+    }
+    __syncthreads();
+    // a spill into the next region must come from a cluster that started here
+    if (threadIdx.x == 0 && g + 1 < nqr && e_out >= base + kRegionSlots && !s_cs) s_bad = 1;
+    __syncthreads();
+    bad = bad || s_bad;
+    if (bad) {
+      if (threadIdx.x == 0) atomicOr(&flags[0], 1u);
+      continue;  // the image is discarded
+    }
+    // occupieds words of this region's quotients (and the padding's, zero)
+    const int64_t nw_own = (phys >> 6) - (base >> 6) < kRegionSlots / 64 ? (phys >> 6) - (base >> 6) : kRegionSlots / 64;
+    for (int i = threadIdx.x; i < nw_own; i += kRegThreads) T1.occ[(base >> 6) + i] = s_occ[i];
+    if (g + 1 == nqr)
+      for (int64_t w = ((base + kRegionSlots) >> 6) + threadIdx.x; w < (phys >> 6); w += kRegThreads) T1.occ[w] = 0;
+    // runend words over [P0, P1): boundary words through atomics (neighbours own the other bits)
+    const int64_t w1 = (P1 - 1) >> 6;
+    for (int64_t w = w0 + threadIdx.x; w <= w1; w += kRegThreads) {
+      const int64_t lo = w << 6, hi = lo + 64;
+      unsigned long long mask = ~0ull;
+      if (P0 > lo) mask &= ~0ull << (P0 - lo);
+      if (P1 < hi) mask &= ~0ull >> (hi - P1);
+      const unsigned long long bits = s_run[w - w0] & mask;
+      if (mask == ~0ull) {
+        T1.run[w] = bits;
+      } else {
+        atomicAnd((unsigned long long *)&T1.run[w], ~mask);
+        if (bits) atomicOr((unsigned long long *)&T1.run[w], bits);
+      }
+      // shift metric: (slot, runend) changes against the old image, 64
+      // slots at a time from 16-byte loads
+      unsigned long long chg, nz;
+      word_slot_masks<S>(old_slots + lo, slots + lo, &chg, &nz);
+      const unsigned long long ob = old_run[w];
+      const unsigned long long changed = (chg | (ob ^ bits)) & mask;
+      ndiff += __popcll(old_only ? (changed & (nz | ob)) : changed);
+    }
+    __syncthreads();
+  }
+  for (int o = 16; o > 0; o >>= 1) ndiff += __shfl_xor_sync(0xFFFFFFFFu, ndiff, o);
+  if ((threadIdx.x & 31) == 0 && ndiff) atomicAdd(diff, ndiff);
+}
+
+__global__ void k_region_stats(const unsigned long long *__restrict__ acc, int64_t G, int64_t *__restrict__ stats) {
+  stats[0] = (int64_t)acc[0];
+  stats[1] = (int64_t)acc[1];
+  stats[2] = G;
+}
+
 // shift instrumentation: slots whose (word, runend bit) changed, optionally
 // restricted to positions the old table used
 template <typename S>
