@@ -3,6 +3,7 @@
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
 #include <thrust/iterator/transform_iterator.h>
+#include <stdio.h>
 #include <stdlib.h>
 
 #include <vector>
@@ -340,6 +341,12 @@ inline bool region_place_enabled() {
   return !e || atoi(e) != 0;
 }
 
+// region-local in-place apply of mid-size batches (apply_local_t); FK_GQF_LOCAL=0 disables
+inline bool local_apply_enabled() {
+  const char *e = getenv("FK_GQF_LOCAL");
+  return !e || atoi(e) != 0;
+}
+
 inline int64_t small_batch_limit(const fk_gqf_geom *g) {
   const char *e = getenv("FK_GQF_SMALL");
   if (e) return atoll(e);
@@ -497,6 +504,151 @@ int count_t(const fk_gqf_geom *g, const fk_gqf_tables *t, const uint64_t *keys, 
   return 0;
 }
 
+// Region-local apply in place (batches touching at most a quarter of the
+// regions): only the regions holding new items and their successors are
+// decoded, merged, placed and rewritten; every other region -- its slots,
+// bits and offset -- stays as it is.  The placement scan restarts at each run
+// of listed regions from the old incoming end (old offsets), a plan pass
+// validates every listed region and checks that each run hands the next,
+// unlisted region its old incoming end (else the layout change would reach
+// it: the global path runs instead), and only then does the write pass
+// touch the table.  Returns 0 (applied, or dry run answered), 1 (not
+// applicable: the caller continues with the global path), 2 (the exact
+// path is needed; *load_possible set), or < 0.
+constexpr int kApplyDryFlag = 1;
+template <typename S_t>
+int apply_local_t(Scratch &S, const fk_gqf_geom *g, const fk_gqf_tables *cur, const uint64_t *keys, int keys_are_fps,
+                  uint64_t fmask, int64_t n, const uint64_t *uniq, const uint64_t *c_new, int64_t m, bool is_del,
+                  int order, int flags, fk_gqf_result *res, bool *load_possible) {
+  cudaStream_t st = S.st;
+  const int64_t nqr = g->quotient_regions;
+  if (m <= 0 || nqr < 8) return 1;
+  int64_t *rbu = S.get<int64_t>(nqr + 1), *creg = S.get<int64_t>(nqr), *d_k = S.get<int64_t>(1);
+  uint8_t *cand = S.get<uint8_t>(nqr);
+  if (S.err) return -(int)S.err;
+  k_region_bounds<<<blocks_for(nqr + 1), 256, 0, st>>>(uniq, m, g->r + kRegionBits, nqr, rbu);
+  k_region_candidates<<<blocks_for(nqr), 256, 0, st>>>(rbu, nqr, cand);
+  {
+    cub::CountingInputIterator<int64_t> it(0);
+    size_t tb = 0;
+    FK_TRY(cub::DeviceSelect::Flagged(nullptr, tb, it, cand, creg, d_k, nqr, st));
+    void *tmp = S.get<char>(tb);
+    if (!tmp) return -(int)S.err;
+    FK_TRY(cub::DeviceSelect::Flagged(tmp, tb, it, cand, creg, d_k, nqr, st));
+  }
+  int64_t K = 0;
+  FK_TRY(cudaMemcpyAsync(&K, d_k, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  FK_TRY(cudaStreamSynchronize(st));
+  const bool trace = getenv("FK_GQF_TRACE") != nullptr;
+  if (trace) fprintf(stderr, "fk gqf local: m=%lld listed regions %lld of %lld\n", (long long)m, (long long)K,
+                     (long long)nqr);
+  if (K == 0 || 4 * K > nqr) return 1;
+  GqfDev T0 = make_dev(g, cur);
+  // old items of the listed regions
+  const int64_t nqw = ((1LL << g->q) + 63) >> 6, nw = K * (kRegionSlots / 64);
+  int64_t *gcount = S.get<int64_t>(nw), *goff = S.get<int64_t>(nw);
+  int *d_err = S.get<int>(1);
+  int64_t *d_num = S.get<int64_t>(4);
+  if (S.err) return -(int)S.err;
+  FK_TRY(cudaMemsetAsync(d_err, 0, sizeof(int), st));
+  k_decode_region_words<S_t><<<blocks_for(nw), 256, 0, st>>>(T0, creg, K, nqw, 0, gcount, nullptr, nullptr, nullptr,
+                                                              d_err);
+  FK_TRY(cub_excl_sum_i64(S, gcount, goff, nw));
+  int64_t tail[2];
+  int h_err = 0;
+  FK_TRY(cudaMemcpyAsync(&tail[0], goff + nw - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  FK_TRY(cudaMemcpyAsync(&tail[1], gcount + nw - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  FK_TRY(cudaMemcpyAsync(&h_err, d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  FK_TRY(cudaStreamSynchronize(st));
+  if (h_err) return FK_E_INVARIANT;
+  const int64_t g_old = tail[0] + tail[1];
+  uint64_t *o_fp = S.get<uint64_t>(g_old), *o_cnt = S.get<uint64_t>(g_old);
+  if (S.err) return -(int)S.err;
+  k_decode_region_words<S_t><<<blocks_for(nw), 256, 0, st>>>(T0, creg, K, nqw, 1, nullptr, goff, o_fp, o_cnt, d_err);
+  // merge with the batch's fingerprints (all inside listed regions)
+  uint8_t *keep_o = S.get<uint8_t>(g_old), *keep_u = S.get<uint8_t>(m);
+  uint64_t *o2_fp = S.get<uint64_t>(g_old), *o2_cnt = S.get<uint64_t>(g_old);
+  uint64_t *u2_fp = S.get<uint64_t>(m), *u2_cnt = S.get<uint64_t>(m);
+  if (S.err) return -(int)S.err;
+  k_keep_old<<<blocks_for(g_old), 256, 0, st>>>(o_fp, g_old, uniq, m, keep_o);
+  k_nonzero<<<blocks_for(m), 256, 0, st>>>(c_new, m, keep_u);
+  FK_TRY(cub_select_flagged(S, o_fp, keep_o, o2_fp, d_num, g_old));
+  FK_TRY(cub_select_flagged(S, o_cnt, keep_o, o2_cnt, d_num + 1, g_old));
+  FK_TRY(cub_select_flagged(S, uniq, keep_u, u2_fp, d_num + 2, m));
+  FK_TRY(cub_select_flagged(S, c_new, keep_u, u2_cnt, d_num + 3, m));
+  int64_t hn[4];
+  FK_TRY(cudaMemcpyAsync(hn, d_num, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  FK_TRY(cudaStreamSynchronize(st));
+  const int64_t G = hn[0] + hn[2];
+  uint64_t *it_fp = S.get<uint64_t>(G), *it_cnt = S.get<uint64_t>(G);
+  if (S.err) return -(int)S.err;
+  if (G > 0) FK_TRY(cub_merge(S, o2_fp, o2_cnt, hn[0], u2_fp, u2_cnt, hn[2], it_fp, it_cnt));
+  // summaries of the listed regions, restarted from the old incoming end at each run of them
+  int64_t *ib = S.get<int64_t>(nqr + 1);
+  MaxPlus *summ = S.get<MaxPlus>(K), *cum = S.get<MaxPlus>(K);
+  unsigned long long *acc = S.get<unsigned long long>(4), *acc_old = S.get<unsigned long long>(2);
+  unsigned *rflags = S.get<unsigned>(2);
+  constexpr int64_t SW = kRegMaxRange / 64 + 1;
+  S_t *saved = S.get<S_t>((size_t)K * kRegMaxRange);
+  unsigned long long *saved_run = S.get<unsigned long long>((size_t)K * SW);
+  if (S.err) return -(int)S.err;
+  FK_TRY(cudaMemsetAsync(acc, 0, 4 * sizeof(unsigned long long), st));
+  FK_TRY(cudaMemsetAsync(acc_old, 0, 2 * sizeof(unsigned long long), st));
+  FK_TRY(cudaMemsetAsync(rflags, 0, 2 * sizeof(unsigned), st));
+  if (G > 0) k_region_bounds<<<blocks_for(nqr + 1), 256, 0, st>>>(it_fp, G, g->r + kRegionBits, nqr, ib);
+  else FK_TRY(cudaMemsetAsync(ib, 0, (nqr + 1) * sizeof(int64_t), st));
+  const int rgrid = (int)(K < (int64_t)num_sms() * 8 ? K : (int64_t)num_sms() * 8);
+  k_region_summary<<<rgrid, kRegThreads, 0, st>>>(it_fp, it_cnt, ib, creg, K, cur->offsets, g->r, summ, acc);
+  FK_TRY(cub_maxplus_scan(S, summ, cum, K));
+  k_item_sums<<<blocks_for(g_old), 256, 0, st>>>(o_fp, o_cnt, g_old, g->r, acc_old);
+  if (order == FK_ORDER_POINT)
+    k_not_ascending<<<blocks_for(n), 256, 0, st>>>(keys, keys_are_fps, g->seed, fmask, n, rflags + 1);
+  // plan pass: validate, save the old windows (nothing written)
+  RegionJob<S_t> job{creg, K, nqr, cur->offsets, 1, saved, saved_run};
+  const S_t *cs = reinterpret_cast<const S_t *>(cur->slots);
+  k_region_place<S_t><<<rgrid, kRegThreads, 0, st>>>(T0, cs, cur->runends, it_fp, it_cnt, ib, cum, job, rflags + 1,
+                                                     order == FK_ORDER_BULK ? 1 : 0, rflags, acc + 2);
+  unsigned long long ha[2], ho[2];
+  unsigned hfl = 0;
+  int64_t hst0 = 0;
+  FK_TRY(cudaMemcpyAsync(ha, acc, sizeof(ha), cudaMemcpyDeviceToHost, st));
+  FK_TRY(cudaMemcpyAsync(ho, acc_old, sizeof(ho), cudaMemcpyDeviceToHost, st));
+  FK_TRY(cudaMemcpyAsync(&hfl, rflags, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+  FK_TRY(cudaMemcpyAsync(&hst0, cur->stats, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  FK_TRY(cudaStreamSynchronize(st));
+  FK_CHECK_LAUNCH();
+  const int64_t h_occ = hst0 + (int64_t)ha[0] - (int64_t)ho[0];
+  if (trace) fprintf(stderr, "fk gqf local: plan flags %u, occupancy %lld / %lld\n", hfl, (long long)h_occ,
+                     (long long)g->max_occupied);
+  bool exact = false;
+  if (!is_del) {
+    exact = hfl != 0 || h_occ >= g->max_occupied;
+    *load_possible = h_occ >= g->max_occupied;
+  }
+  if (flags & kApplyDryFlag) {
+    if (!exact && hfl) return 1;  // (a delete whose change reaches an unlisted region: let the global path answer)
+    res->code = exact ? 1 : 0;
+    return 0;
+  }
+  if (exact) return 2;
+  if (hfl) return 1;
+  // write pass, in place
+  job.plan_only = 0;
+  FK_TRY(cudaMemsetAsync(acc + 2, 0, sizeof(unsigned long long), st));
+  k_region_place<S_t><<<rgrid, kRegThreads, 0, st>>>(T0, cs, cur->runends, it_fp, it_cnt, ib, cum, job, rflags + 1,
+                                                     order == FK_ORDER_BULK ? 1 : 0, rflags, acc + 2);
+  k_region_stats_delta<<<1, 1, 0, st>>>(acc, acc_old, G, g_old, cur->stats);
+  int rc = rebuild_index(g, cur, st);
+  if (rc) return rc;
+  unsigned long long hd = 0;
+  FK_TRY(cudaMemcpyAsync(&hd, acc + 2, sizeof(hd), cudaMemcpyDeviceToHost, st));
+  FK_TRY(cudaStreamSynchronize(st));
+  FK_CHECK_LAUNCH();
+  res->shifted = (int64_t)hd;
+  res->swapped = 0;
+  return 0;
+}
+
 // apply_t flags: dry run (steps 1-12 only; res->code = 1 if the batch would
 // need the exact sequential path), or go straight to the exact path.
 constexpr int kApplyDry = 1, kApplyForceExact = 2;
@@ -643,121 +795,139 @@ int apply_t(const fk_gqf_geom *g, const fk_gqf_tables *cur, const fk_gqf_tables 
     k_found_flags<<<blocks_for(n), 256, 0, st>>>(pre, idx_s, seg, c_old, n, found);
   }
 
-  // 8. decode the old table into sorted (fp, count) items
-  int64_t nqw = ((1LL << g->q) + 63) >> 6;
-  int64_t *gcount = S.get<int64_t>(nqw), *goff = S.get<int64_t>(nqw);
-  int *d_err = S.get<int>(4);
-  if (S.err) return -(int)S.err;
-  FK_CU(cudaMemsetAsync(d_err, 0, 4 * sizeof(int), st));
-  k_decode_words<S_t><<<blocks_for(nqw), 256, 0, st>>>(T0, nqw, 0, gcount, nullptr, nullptr, nullptr, d_err);
-  FK_CU(cub_excl_sum_i64(S, gcount, goff, nqw));
-  int64_t tail[2];
-  FK_CU(cudaMemcpyAsync(&tail[0], goff + nqw - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  FK_CU(cudaMemcpyAsync(&tail[1], gcount + nqw - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  int h_err = 0;
-  FK_CU(cudaMemcpyAsync(&h_err, d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
-  FK_CU(cudaStreamSynchronize(st));
-  if (h_err) return FK_E_INVARIANT;
-  int64_t g_old = tail[0] + tail[1];
-  uint64_t *o_fp = S.get<uint64_t>(g_old), *o_cnt = S.get<uint64_t>(g_old);
-  if (S.err) return -(int)S.err;
-  k_decode_words<S_t><<<blocks_for(nqw), 256, 0, st>>>(T0, nqw, 1, nullptr, goff, o_fp, o_cnt, d_err);
-
-  // 9-10. drop old items the batch updates and zero counts, then merge the
-  // two duplicate-free sorted lists
-  uint8_t *keep_o = S.get<uint8_t>(g_old), *keep_u = S.get<uint8_t>(m);
-  uint64_t *o2_fp = S.get<uint64_t>(g_old), *o2_cnt = S.get<uint64_t>(g_old);
-  uint64_t *u2_fp = S.get<uint64_t>(m), *u2_cnt = S.get<uint64_t>(m);
-  if (S.err) return -(int)S.err;
-  k_keep_old<<<blocks_for(g_old), 256, 0, st>>>(o_fp, g_old, uniq, m, keep_o);
-  k_nonzero<<<blocks_for(m), 256, 0, st>>>(c_new, m, keep_u);
-  FK_CU(cub_select_flagged(S, o_fp, keep_o, o2_fp, d_num, g_old));
-  FK_CU(cub_select_flagged(S, o_cnt, keep_o, o2_cnt, d_num + 1, g_old));
-  FK_CU(cub_select_flagged(S, uniq, keep_u, u2_fp, d_num + 2, m));
-  FK_CU(cub_select_flagged(S, c_new, keep_u, u2_cnt, d_num + 3, m));
-  int64_t hn[4];
-  FK_CU(cudaMemcpyAsync(hn, d_num, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  FK_CU(cudaStreamSynchronize(st));
-  int64_t G = hn[0] + hn[2];
-  uint64_t *it_fp = S.get<uint64_t>(G), *it_cnt = S.get<uint64_t>(G);
-  if (S.err) return -(int)S.err;
-  if (G > 0) FK_CU(cub_merge(S, o2_fp, o2_cnt, hn[0], u2_fp, u2_cnt, hn[2], it_fp, it_cnt));
-
-  // 11-12. placement and the capacity predicates.  Region placement
-  // (default): per-region max-plus summaries, a scan over the regions, then
-  // one CTA per region writes its whole slot range of `next` and reports a
-  // broken layout; the result is used unless the batch needs the exact path.
+  // 8'. region-local apply in place (mid-size batches; apply_local_t)
   bool exact = (flags & kApplyForceExact) != 0, load_possible = exact;
   bool region_done = false;
   unsigned long long region_shift = 0;
   MaxPlus *ends = nullptr;
   uint64_t *L = nullptr;
-  if (!exact && region_place_enabled()) {
-    const int64_t nqr = g->quotient_regions;
-    int64_t *ib = S.get<int64_t>(nqr + 1);
-    MaxPlus *summ = S.get<MaxPlus>(nqr), *cum = S.get<MaxPlus>(nqr);
-    unsigned long long *acc = S.get<unsigned long long>(4);  // [0] slots, [1] counts, [2] shift
-    unsigned *rflags = S.get<unsigned>(2);                   // [0] broken layout, [1] not ascending
-    if (S.err) return -(int)S.err;
-    FK_CU(cudaMemsetAsync(acc, 0, 4 * sizeof(unsigned long long), st));
-    FK_CU(cudaMemsetAsync(rflags, 0, 2 * sizeof(unsigned), st));
-    if (G > 0) k_region_bounds<<<blocks_for(nqr + 1), 256, 0, st>>>(it_fp, G, g->r + kRegionBits, nqr, ib);
-    else FK_CU(cudaMemsetAsync(ib, 0, (nqr + 1) * sizeof(int64_t), st));
-    const int rgrid = (int)(nqr < (int64_t)num_sms() * 8 ? nqr : (int64_t)num_sms() * 8);
-    k_region_summary<<<rgrid, kRegThreads, 0, st>>>(it_fp, it_cnt, ib, nqr, g->r, summ, acc);
-    FK_CU(cub_maxplus_scan(S, summ, cum, nqr));
-    if (order == FK_ORDER_POINT)  // point order: the shift metric counts the batch's own slots unless ascending
-      k_not_ascending<<<blocks_for(n), 256, 0, st>>>(keys, keys_are_fps, g->seed, fmask, n, rflags + 1);
-    k_region_place<S_t><<<rgrid, kRegThreads, 0, st>>>(make_dev(g, nxt), reinterpret_cast<const S_t *>(cur->slots),
-                                                       cur->runends, it_fp, it_cnt, ib, cum, nqr, rflags + 1,
-                                                       order == FK_ORDER_BULK ? 1 : 0, rflags, acc + 2);
-    k_region_stats<<<1, 1, 0, st>>>(acc, G, nxt->stats);
-    unsigned long long hacc[3];
-    unsigned hfl = 0;
-    FK_CU(cudaMemcpyAsync(hacc, acc, sizeof(hacc), cudaMemcpyDeviceToHost, st));
-    FK_CU(cudaMemcpyAsync(&hfl, rflags, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
-    FK_CU(cudaStreamSynchronize(st));
-    FK_CHECK_LAUNCH();
-    const int64_t h_occ = (int64_t)hacc[0];
-    if (!is_del) {
-      // every item's pre-insert occupancy is <= the final one, so a final
-      // occupancy below the ceiling rules LOAD_CAPACITY out for any order
-      exact = hfl != 0 || h_occ >= g->max_occupied;
-      load_possible = h_occ >= g->max_occupied;
+  int64_t G = 0;
+  uint64_t *it_fp = nullptr, *it_cnt = nullptr;
+  bool local_exact = false;
+  if (!exact && region_place_enabled() && local_apply_enabled()) {
+    bool lp = false;
+    const int lr = apply_local_t<S_t>(S, g, cur, keys, keys_are_fps, fmask, n, uniq, c_new, m, is_del, order, flags,
+                                      res, &lp);
+    if (lr <= 0) return lr;  // applied (or dry run answered), or an error
+    if (lr == 2) {
+      local_exact = exact = true;
+      load_possible = lp;
     }
-    region_done = hfl == 0;  // (a delete never breaks the layout of a valid table)
-    region_shift = hacc[2];
   }
-  if (!region_done && !exact) {
-    // global placement: max-plus scan over every item
-    MaxPlus *terms = S.get<MaxPlus>(G);
-    ends = S.get<MaxPlus>(G);
-    L = S.get<uint64_t>(G);
+  if (!local_exact) {
+    // 8. decode the old table into sorted (fp, count) items
+    int64_t nqw = ((1LL << g->q) + 63) >> 6;
+    int64_t *gcount = S.get<int64_t>(nqw), *goff = S.get<int64_t>(nqw);
+    int *d_err = S.get<int>(4);
     if (S.err) return -(int)S.err;
-    if (G > 0) {
-      k_place_terms<<<blocks_for(G), 256, 0, st>>>(it_fp, it_cnt, G, g->r, terms, L);
-      FK_CU(cub_maxplus_scan(S, terms, ends, G));
-    }
-    // would the sequential reference have raised?  (inserts only)
-    if (!is_del && G > 0) {
-      int64_t *cfirst = S.get<int64_t>(G), *cfs = S.get<int64_t>(G);
-      unsigned *cflags = S.get<unsigned>(4);
+    FK_CU(cudaMemsetAsync(d_err, 0, 4 * sizeof(int), st));
+    k_decode_words<S_t><<<blocks_for(nqw), 256, 0, st>>>(T0, nqw, 0, gcount, nullptr, nullptr, nullptr, d_err);
+    FK_CU(cub_excl_sum_i64(S, gcount, goff, nqw));
+    int64_t tail[2];
+    FK_CU(cudaMemcpyAsync(&tail[0], goff + nqw - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    FK_CU(cudaMemcpyAsync(&tail[1], gcount + nqw - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    int h_err = 0;
+    FK_CU(cudaMemcpyAsync(&h_err, d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
+    FK_CU(cudaStreamSynchronize(st));
+    if (h_err) return FK_E_INVARIANT;
+    int64_t g_old = tail[0] + tail[1];
+    uint64_t *o_fp = S.get<uint64_t>(g_old), *o_cnt = S.get<uint64_t>(g_old);
+    if (S.err) return -(int)S.err;
+    k_decode_words<S_t><<<blocks_for(nqw), 256, 0, st>>>(T0, nqw, 1, nullptr, goff, o_fp, o_cnt, d_err);
+
+    // 9-10. drop old items the batch updates and zero counts, then merge the
+    // two duplicate-free sorted lists
+    uint8_t *keep_o = S.get<uint8_t>(g_old), *keep_u = S.get<uint8_t>(m);
+    uint64_t *o2_fp = S.get<uint64_t>(g_old), *o2_cnt = S.get<uint64_t>(g_old);
+    uint64_t *u2_fp = S.get<uint64_t>(m), *u2_cnt = S.get<uint64_t>(m);
+    if (S.err) return -(int)S.err;
+    k_keep_old<<<blocks_for(g_old), 256, 0, st>>>(o_fp, g_old, uniq, m, keep_o);
+    k_nonzero<<<blocks_for(m), 256, 0, st>>>(c_new, m, keep_u);
+    FK_CU(cub_select_flagged(S, o_fp, keep_o, o2_fp, d_num, g_old));
+    FK_CU(cub_select_flagged(S, o_cnt, keep_o, o2_cnt, d_num + 1, g_old));
+    FK_CU(cub_select_flagged(S, uniq, keep_u, u2_fp, d_num + 2, m));
+    FK_CU(cub_select_flagged(S, c_new, keep_u, u2_cnt, d_num + 3, m));
+    int64_t hn[4];
+    FK_CU(cudaMemcpyAsync(hn, d_num, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    FK_CU(cudaStreamSynchronize(st));
+    G = hn[0] + hn[2];
+    it_fp = S.get<uint64_t>(G);
+    it_cnt = S.get<uint64_t>(G);
+    if (S.err) return -(int)S.err;
+    if (G > 0) FK_CU(cub_merge(S, o2_fp, o2_cnt, hn[0], u2_fp, u2_cnt, hn[2], it_fp, it_cnt));
+
+    // 11-12. placement and the capacity predicates.  Region placement
+    // (default): per-region max-plus summaries, a scan over the regions, then
+    // one CTA per region writes its whole slot range of `next` and reports a
+    // broken layout; the result is used unless the batch needs the exact path.
+    if (!exact && region_place_enabled()) {
+      const int64_t nqr = g->quotient_regions;
+      int64_t *ib = S.get<int64_t>(nqr + 1);
+      MaxPlus *summ = S.get<MaxPlus>(nqr), *cum = S.get<MaxPlus>(nqr);
+      unsigned long long *acc = S.get<unsigned long long>(4);  // [0] slots, [1] counts, [2] shift
+      unsigned *rflags = S.get<unsigned>(2);                   // [0] broken layout, [1] not ascending
       if (S.err) return -(int)S.err;
-      FK_CU(cudaMemsetAsync(cflags, 0, 4 * sizeof(unsigned), st));
-      k_cluster_check<<<blocks_for(G), 256, 0, st>>>(it_fp, ends, G, g->r, g->phys, cfirst, cflags);
-      FK_CU(cub_max_scan_i64(S, cfirst, cfs, G));
-      k_cluster_check2<<<blocks_for(G), 256, 0, st>>>(ends, cfs, cfirst, G, g->phys, cflags);
-      int64_t *occ_sum = S.get<int64_t>(4);
-      if (S.err) return -(int)S.err;
-      FK_CU(cudaMemsetAsync(occ_sum, 0, 4 * sizeof(int64_t), st));
-      k_stats<<<blocks_for(G), 256, 0, st>>>(it_cnt, L, G, occ_sum);
-      unsigned h_flags = 0;
-      int64_t h_occ = 0;
-      FK_CU(cudaMemcpyAsync(&h_flags, cflags, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
-      FK_CU(cudaMemcpyAsync(&h_occ, occ_sum, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+      FK_CU(cudaMemsetAsync(acc, 0, 4 * sizeof(unsigned long long), st));
+      FK_CU(cudaMemsetAsync(rflags, 0, 2 * sizeof(unsigned), st));
+      if (G > 0) k_region_bounds<<<blocks_for(nqr + 1), 256, 0, st>>>(it_fp, G, g->r + kRegionBits, nqr, ib);
+      else FK_CU(cudaMemsetAsync(ib, 0, (nqr + 1) * sizeof(int64_t), st));
+      const int rgrid = (int)(nqr < (int64_t)num_sms() * 8 ? nqr : (int64_t)num_sms() * 8);
+      k_region_summary<<<rgrid, kRegThreads, 0, st>>>(it_fp, it_cnt, ib, nullptr, nqr, nullptr, g->r, summ, acc);
+      FK_CU(cub_maxplus_scan(S, summ, cum, nqr));
+      if (order == FK_ORDER_POINT)  // point order: the shift metric counts the batch's own slots unless ascending
+        k_not_ascending<<<blocks_for(n), 256, 0, st>>>(keys, keys_are_fps, g->seed, fmask, n, rflags + 1);
+      RegionJob<S_t> job{nullptr, nqr, nqr, nullptr, 0, nullptr, nullptr};
+      k_region_place<S_t><<<rgrid, kRegThreads, 0, st>>>(make_dev(g, nxt), reinterpret_cast<const S_t *>(cur->slots),
+                                                         cur->runends, it_fp, it_cnt, ib, cum, job, rflags + 1,
+                                                         order == FK_ORDER_BULK ? 1 : 0, rflags, acc + 2);
+      k_region_stats<<<1, 1, 0, st>>>(acc, G, nxt->stats);
+      unsigned long long hacc[3];
+      unsigned hfl = 0;
+      FK_CU(cudaMemcpyAsync(hacc, acc, sizeof(hacc), cudaMemcpyDeviceToHost, st));
+      FK_CU(cudaMemcpyAsync(&hfl, rflags, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
       FK_CU(cudaStreamSynchronize(st));
-      exact = h_flags != 0 || h_occ >= g->max_occupied;
-      load_possible = h_occ >= g->max_occupied;
+      FK_CHECK_LAUNCH();
+      const int64_t h_occ = (int64_t)hacc[0];
+      if (!is_del) {
+        // every item's pre-insert occupancy is <= the final one, so a final
+        // occupancy below the ceiling rules LOAD_CAPACITY out for any order
+        exact = hfl != 0 || h_occ >= g->max_occupied;
+        load_possible = h_occ >= g->max_occupied;
+      }
+      region_done = hfl == 0;  // (a delete never breaks the layout of a valid table)
+      region_shift = hacc[2];
+    }
+    if (!region_done && !exact) {
+      // global placement: max-plus scan over every item
+      MaxPlus *terms = S.get<MaxPlus>(G);
+      ends = S.get<MaxPlus>(G);
+      L = S.get<uint64_t>(G);
+      if (S.err) return -(int)S.err;
+      if (G > 0) {
+        k_place_terms<<<blocks_for(G), 256, 0, st>>>(it_fp, it_cnt, G, g->r, terms, L);
+        FK_CU(cub_maxplus_scan(S, terms, ends, G));
+      }
+      // would the sequential reference have raised?  (inserts only)
+      if (!is_del && G > 0) {
+        int64_t *cfirst = S.get<int64_t>(G), *cfs = S.get<int64_t>(G);
+        unsigned *cflags = S.get<unsigned>(4);
+        if (S.err) return -(int)S.err;
+        FK_CU(cudaMemsetAsync(cflags, 0, 4 * sizeof(unsigned), st));
+        k_cluster_check<<<blocks_for(G), 256, 0, st>>>(it_fp, ends, G, g->r, g->phys, cfirst, cflags);
+        FK_CU(cub_max_scan_i64(S, cfirst, cfs, G));
+        k_cluster_check2<<<blocks_for(G), 256, 0, st>>>(ends, cfs, cfirst, G, g->phys, cflags);
+        int64_t *occ_sum = S.get<int64_t>(4);
+        if (S.err) return -(int)S.err;
+        FK_CU(cudaMemsetAsync(occ_sum, 0, 4 * sizeof(int64_t), st));
+        k_stats<<<blocks_for(G), 256, 0, st>>>(it_cnt, L, G, occ_sum);
+        unsigned h_flags = 0;
+        int64_t h_occ = 0;
+        FK_CU(cudaMemcpyAsync(&h_flags, cflags, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+        FK_CU(cudaMemcpyAsync(&h_occ, occ_sum, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        FK_CU(cudaStreamSynchronize(st));
+        exact = h_flags != 0 || h_occ >= g->max_occupied;
+        load_possible = h_occ >= g->max_occupied;
+      }
     }
   }
 

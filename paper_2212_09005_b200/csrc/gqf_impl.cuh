@@ -719,40 +719,64 @@ __global__ void k_reverse_u64(const uint64_t *__restrict__ a, int64_t n, uint64_
 
 // Decode pass over occupied quotient words: mode 0 counts groups per word,
 // mode 1 writes (fp, count) items at off[w].
+// Groups of quotient word w (mode 0: their number; mode 1: write them at o).
+template <typename S>
+__device__ __forceinline__ int64_t decode_word(const GqfDev &T, int64_t w, int mode, int64_t o,
+                                               uint64_t *__restrict__ it_fp, uint64_t *__restrict__ it_cnt,
+                                               int *__restrict__ err) {
+  const S *slots = reinterpret_cast<const S *>(T.slots);
+  uint64_t ow = T.occ[w];
+  int64_t g = 0;
+  if (ow) {
+    int64_t prev = (w << 6) + (int64_t)T.spill[w] - 1;
+    while (ow) {
+      int b = __ffsll((long long)ow) - 1;
+      ow &= ow - 1;
+      int64_t quot = (w << 6) + b;
+      int64_t end = select_after_dev(T.run, prev, 1, T.phys);
+      if (end < 0) { *err = 1; break; }
+      int64_t s = quot > prev + 1 ? quot : prev + 1;
+      for (int64_t p = s; p <= end;) {
+        uint64_t h, cnt;
+        int64_t nx;
+        if (!parse_group_dev<S>(slots, p, end, T.r, &h, &cnt, &nx)) { *err = 1; break; }
+        if (mode) {
+          it_fp[o] = ((uint64_t)quot << T.r) | h;
+          it_cnt[o] = cnt;
+          o++;
+        }
+        g++;
+        p = nx;
+      }
+      prev = end;
+    }
+  }
+  return g;
+}
+
 template <typename S>
 __global__ void k_decode_words(GqfDev T, int64_t nqw, int mode, int64_t *__restrict__ gcount,
                                const int64_t *__restrict__ off, uint64_t *__restrict__ it_fp,
                                uint64_t *__restrict__ it_cnt, int *__restrict__ err) {
-  const S *slots = reinterpret_cast<const S *>(T.slots);
   for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nqw; w += (int64_t)gridDim.x * blockDim.x) {
-    uint64_t ow = T.occ[w];
-    int64_t g = 0;
-    int64_t o = mode ? off[w] : 0;
-    if (ow) {
-      int64_t prev = (w << 6) + (int64_t)T.spill[w] - 1;
-      while (ow) {
-        int b = __ffsll((long long)ow) - 1;
-        ow &= ow - 1;
-        int64_t quot = (w << 6) + b;
-        int64_t end = select_after_dev(T.run, prev, 1, T.phys);
-        if (end < 0) { *err = 1; break; }
-        int64_t s = quot > prev + 1 ? quot : prev + 1;
-        for (int64_t p = s; p <= end;) {
-          uint64_t h, cnt;
-          int64_t nx;
-          if (!parse_group_dev<S>(slots, p, end, T.r, &h, &cnt, &nx)) { *err = 1; break; }
-          if (mode) {
-            it_fp[o] = ((uint64_t)quot << T.r) | h;
-            it_cnt[o] = cnt;
-            o++;
-          }
-          g++;
-          p = nx;
-        }
-        prev = end;
-      }
-    }
+    const int64_t g = decode_word<S>(T, w, mode, mode ? off[w] : 0, it_fp, it_cnt, err);
     if (!mode) gcount[w] = g;
+  }
+}
+
+// The same over the quotient words of a list of regions (creg[0..K)):
+// flat index f -> region creg[f / 128], word f % 128 of it.
+template <typename S>
+__global__ void k_decode_region_words(GqfDev T, const int64_t *__restrict__ creg, int64_t K, int64_t nqw, int mode,
+                                      int64_t *__restrict__ gcount, const int64_t *__restrict__ off,
+                                      uint64_t *__restrict__ it_fp, uint64_t *__restrict__ it_cnt,
+                                      int *__restrict__ err) {
+  constexpr int64_t WPR = kRegionSlots / 64;
+  for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < K * WPR; f += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t w = creg[f / WPR] * WPR + (f % WPR);
+    int64_t g = 0;
+    if (w < nqw) g = decode_word<S>(T, w, mode, mode ? off[f] : 0, it_fp, it_cnt, err);
+    if (!mode) gcount[f] = g;
   }
 }
 
@@ -782,16 +806,20 @@ __global__ void k_nonzero(const uint64_t *__restrict__ c, int64_t m, uint8_t *__
 struct MaxPlus {
   int64_t a, b;
 };
+constexpr int64_t kNegInf = -(1LL << 60);
+// (saturating at kNegInf, so constant maps -- b = kNegInf, the local
+// apply's segment resets -- compose without overflow)
 struct MaxPlusOp {
   __host__ __device__ __forceinline__ MaxPlus operator()(const MaxPlus &l, const MaxPlus &rr) const {
     MaxPlus o;
     int64_t t = l.a + rr.b;
     o.a = rr.a > t ? rr.a : t;
     o.b = l.b + rr.b;
+    if (o.a < kNegInf) o.a = kNegInf;
+    if (o.b < kNegInf) o.b = kNegInf;
     return o;
   }
 };
-constexpr int64_t kNegInf = -(1LL << 60);
 
 __global__ void k_place_terms(const uint64_t *__restrict__ fp, const uint64_t *__restrict__ cnt, int64_t G, int r,
                               MaxPlus *__restrict__ terms, uint64_t *__restrict__ L_out) {
@@ -912,11 +940,7 @@ __device__ __forceinline__ MaxPlus mp_id() {
 }
 
 __device__ __forceinline__ MaxPlus mp_op(const MaxPlus &l, const MaxPlus &rr) {  // l first, then rr
-  MaxPlus o;
-  const int64_t t = l.a + rr.b;
-  o.a = rr.a > t ? rr.a : t;
-  o.b = l.b + rr.b;
-  return o;
+  return MaxPlusOp()(l, rr);
 }
 
 __device__ __forceinline__ MaxPlus item_term(const uint64_t *fp, const uint64_t *cnt, int64_t i, int64_t a, int r,
@@ -959,13 +983,20 @@ __device__ __forceinline__ MaxPlus block_excl_mp(MaxPlus v, MaxPlus *sw, MaxPlus
   return mp_op(wp, ex);
 }
 
+// Regions: creg[0..K) (the local apply's candidate list), or 0..K-1 when
+// creg is null.  old_offs (local apply): a region whose predecessor is not
+// in the list starts from its old incoming end, base - 1 + old_offs[g]
+// (a constant map composed in front of its summary).
 __global__ void __launch_bounds__(kRegThreads) k_region_summary(const uint64_t *__restrict__ fp,
                                                                 const uint64_t *__restrict__ cnt,
-                                                                const int64_t *__restrict__ ib, int64_t nqr, int r,
+                                                                const int64_t *__restrict__ ib,
+                                                                const int64_t *__restrict__ creg, int64_t K,
+                                                                const int32_t *__restrict__ old_offs, int r,
                                                                 MaxPlus *__restrict__ summ,
                                                                 unsigned long long *__restrict__ acc) {
   __shared__ MaxPlus sw[kRegThreads / 32];
-  for (int64_t g = blockIdx.x; g < nqr; g += gridDim.x) {
+  for (int64_t li = blockIdx.x; li < K; li += gridDim.x) {
+    const int64_t g = creg ? creg[li] : li;
     const int64_t a = ib[g], e = ib[g + 1], n = e - a;
     const int64_t c = (n + kRegThreads - 1) / kRegThreads;
     const int64_t i0 = a + (int64_t)threadIdx.x * c, i1 = min(e, i0 + c);
@@ -983,7 +1014,14 @@ __global__ void __launch_bounds__(kRegThreads) k_region_summary(const uint64_t *
       MaxPlus clamp;
       clamp.a = (g << kRegionBits) - 1;
       clamp.b = 0;
-      summ[g] = mp_op(clamp, tot);
+      MaxPlus el = mp_op(clamp, tot);
+      if (old_offs && (li == 0 || creg[li - 1] != g - 1)) {
+        MaxPlus reset;
+        reset.a = (g << kRegionBits) - 1 + old_offs[g];
+        reset.b = kNegInf;
+        el = mp_op(reset, el);
+      }
+      summ[li] = el;
     }
     for (int o = 16; o > 0; o >>= 1) {
       ls += __shfl_xor_sync(0xFFFFFFFFu, ls, o);
@@ -1025,13 +1063,30 @@ __device__ __forceinline__ void word_slot_masks(const S *a, const S *b, unsigned
 
 // flags[0] |= 1: the canonical layout breaks the reference's bounds (a
 // cluster spans three regions / passes the table end): use the exact path.
+// Region list as in k_region_summary.  Global apply (creg null): writes the
+// new image T1 (= next) against the old image old_slots / old_run.  Local
+// apply (creg, old_offs): T1 is the current image, rewritten in place; a
+// first pass with plan_only validates every region (and the old incoming
+// ends at the ends of runs of listed regions) and saves each region's old
+// window [base, base + kRegMaxRange) to saved_* for the shift metric; the
+// second pass writes.
+template <typename S>
+struct RegionJob {
+  const int64_t *creg;
+  int64_t K, nqr;
+  const int32_t *old_offs;
+  int plan_only;
+  S *saved_slots;               // [K][kRegMaxRange]
+  unsigned long long *saved_run;  // [K][kRegMaxRange / 64 + 1]
+};
+
 template <typename S>
 __global__ void __launch_bounds__(kRegThreads) k_region_place(GqfDev T1, const S *__restrict__ old_slots,
                                                               const uint64_t *__restrict__ old_run,
                                                               const uint64_t *__restrict__ fp,
                                                               const uint64_t *__restrict__ cnt,
                                                               const int64_t *__restrict__ ib,
-                                                              const MaxPlus *__restrict__ cum, int64_t nqr,
+                                                              const MaxPlus *__restrict__ cum, RegionJob<S> J,
                                                               const unsigned *__restrict__ not_asc, int bulk_order,
                                                               unsigned *__restrict__ flags,
                                                               unsigned long long *__restrict__ diff) {
@@ -1041,18 +1096,33 @@ __global__ void __launch_bounds__(kRegThreads) k_region_place(GqfDev T1, const S
   __shared__ int s_cs, s_bad;
   S *slots = reinterpret_cast<S *>(T1.slots);
   const int r = T1.r;
-  const int64_t phys = T1.phys;
+  const int64_t phys = T1.phys, nqr = J.nqr;
   const bool old_only = bulk_order || !*not_asc;
+  const bool local = J.creg != nullptr, plan = J.plan_only != 0;
+  constexpr int64_t SW = kRegMaxRange / 64 + 1;  // saved runend words per region
   unsigned long long ndiff = 0;
-  for (int64_t g = blockIdx.x; g < nqr; g += gridDim.x) {
+  for (int64_t li = blockIdx.x; li < J.K; li += gridDim.x) {
+    const int64_t g = local ? J.creg[li] : li;
     const int64_t base = g << kRegionBits;
-    const int64_t e_in = g ? mp_end(cum[g - 1]) : -1;     // end of every earlier region's runs
-    const int64_t e_out = mp_end(cum[g]);                  // >= base - 1 (the summary is clamped)
+    const bool seg_start = local && (li == 0 || J.creg[li - 1] != g - 1);
+    const bool seg_end = local && (li + 1 == J.K || J.creg[li + 1] != g + 1);
+    // end of every earlier region's runs (local segment starts: the old one)
+    const int64_t e_in = seg_start ? base - 1 + J.old_offs[g] : (li ? mp_end(cum[li - 1]) : -1);
+    const int64_t e_out = mp_end(cum[li]);  // >= base - 1 (the summary is clamped)
     const int64_t P0 = e_in + 1 > base ? e_in + 1 : base;
     int64_t P1 = g + 1 < nqr ? (e_out + 1 > base + kRegionSlots ? e_out + 1 : base + kRegionSlots) : phys;
+    if (plan) {
+      // save the old window for the shift metric (before any region writes)
+      S *sv = J.saved_slots + li * kRegMaxRange;
+      for (int64_t p = threadIdx.x; p < kRegMaxRange; p += kRegThreads) sv[p] = base + p < phys ? old_slots[base + p] : (S)0;
+      for (int64_t w = threadIdx.x; w < SW; w += kRegThreads)
+        J.saved_run[li * SW + w] = (base >> 6) + w < (phys >> 6) ? old_run[(base >> 6) + w] : 0ull;
+    }
     if (threadIdx.x == 0) {
       s_cs = 0;
       s_bad = 0;
+    }
+    if (threadIdx.x == 0 && !plan) {
       // the offsets of this region (and of the padding region after the last one)
       T1.offs[g] = (int32_t)(e_in + 1 > base ? e_in + 1 - base : 0);
       if (g + 1 == nqr)
@@ -1064,8 +1134,11 @@ __global__ void __launch_bounds__(kRegThreads) k_region_place(GqfDev T1, const S
     for (int i = threadIdx.x; i < kRegMaxRange / 64 + 2; i += kRegThreads) s_run[i] = 0;
     for (int i = threadIdx.x; i < kRegionSlots / 64; i += kRegThreads) s_occ[i] = 0;
     __syncthreads();
-    bool bad = e_out >= phys || P1 > phys || P1 - P0 > kRegMaxRange;
-    if (!bad) {  // zero the range: ragged ends slot by slot, the middle in 16-byte stores
+    bool bad = e_out >= phys || P1 > phys || P1 - base > kRegMaxRange;
+    // a run of listed regions must hand the next, unlisted region its old incoming end
+    if (seg_end && g + 1 < nqr && e_out > base + kRegionSlots - 1 + J.old_offs[g + 1]) bad = true;
+    if (seg_end && g + 1 < nqr && J.old_offs[g + 1] > 0 && e_out != base + kRegionSlots - 1 + J.old_offs[g + 1]) bad = true;
+    if (!bad && !plan) {  // zero the range: ragged ends slot by slot, the middle in 16-byte stores
       constexpr int PER = 16 / (int)sizeof(S);
       const int64_t q0 = (P0 + PER - 1) / PER * PER, q1 = P1 / PER * PER;
       if (q0 >= q1) {
@@ -1108,7 +1181,7 @@ __global__ void __launch_bounds__(kRegThreads) k_region_place(GqfDev T1, const S
         s_bad = 1;
         break;
       }
-      enc_write<S>(slots, run_end - L + 1, f & ((1ull << r) - 1), cnt[i], r);
+      if (!plan) enc_write<S>(slots, run_end - L + 1, f & ((1ull << r) - 1), cnt[i], r);
       if (last) atomicOr(&s_run[(run_end >> 6) - w0], 1ull << (run_end & 63));
     }
     __syncthreads();
@@ -1118,7 +1191,11 @@ __global__ void __launch_bounds__(kRegThreads) k_region_place(GqfDev T1, const S
     bad = bad || s_bad;
     if (bad) {
       if (threadIdx.x == 0) atomicOr(&flags[0], 1u);
-      continue;  // the image is discarded
+      continue;  // the image is discarded / the local apply does not run
+    }
+    if (plan) {
+      __syncthreads();
+      continue;
     }
     // occupieds words of this region's quotients (and the padding's, zero)
     const int64_t nw_own = (phys >> 6) - (base >> 6) < kRegionSlots / 64 ? (phys >> 6) - (base >> 6) : kRegionSlots / 64;
@@ -1141,9 +1218,14 @@ __global__ void __launch_bounds__(kRegThreads) k_region_place(GqfDev T1, const S
       }
       // shift metric: (slot, runend) changes against the old image, 64
       // slots at a time from 16-byte loads
-      unsigned long long chg, nz;
-      word_slot_masks<S>(old_slots + lo, slots + lo, &chg, &nz);
-      const unsigned long long ob = old_run[w];
+      unsigned long long chg, nz, ob;
+      if (local) {
+        word_slot_masks<S>(J.saved_slots + li * kRegMaxRange + (lo - base), slots + lo, &chg, &nz);
+        ob = J.saved_run[li * SW + (w - (base >> 6))];
+      } else {
+        word_slot_masks<S>(old_slots + lo, slots + lo, &chg, &nz);
+        ob = old_run[w];
+      }
       const unsigned long long changed = (chg | (ob ^ bits)) & mask;
       ndiff += __popcll(old_only ? (changed & (nz | ob)) : changed);
     }
@@ -1151,6 +1233,42 @@ __global__ void __launch_bounds__(kRegThreads) k_region_place(GqfDev T1, const S
   }
   for (int o = 16; o > 0; o >>= 1) ndiff += __shfl_xor_sync(0xFFFFFFFFu, ndiff, o);
   if ((threadIdx.x & 31) == 0 && ndiff) atomicAdd(diff, ndiff);
+}
+
+// local apply candidates: regions holding new items, and their successors
+__global__ void k_region_candidates(const int64_t *__restrict__ rbu, int64_t nqr, uint8_t *__restrict__ cand) {
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < nqr; g += (int64_t)gridDim.x * blockDim.x) {
+    const bool dirty = rbu[g + 1] > rbu[g], prev = g > 0 && rbu[g] > rbu[g - 1];
+    cand[g] = (dirty || prev) ? 1 : 0;
+  }
+}
+
+// slot and count sums of a list of items (the local apply's old items)
+__global__ void k_item_sums(const uint64_t *__restrict__ fp, const uint64_t *__restrict__ cnt, int64_t n, int r,
+                            unsigned long long *__restrict__ acc) {
+  unsigned long long ls = 0, cs = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t L = enc_len(fp[i] & ((1ull << r) - 1), cnt[i], r);
+    ls += L;
+    cs += cnt[i];
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    ls += __shfl_xor_sync(0xFFFFFFFFu, ls, o);
+    cs += __shfl_xor_sync(0xFFFFFFFFu, cs, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (ls) atomicAdd(&acc[0], ls);
+    if (cs) atomicAdd(&acc[1], cs);
+  }
+}
+
+// stats += new - old (local apply: acc = new sums, old = the replaced items' sums)
+__global__ void k_region_stats_delta(const unsigned long long *__restrict__ acc_new,
+                                     const unsigned long long *__restrict__ acc_old, int64_t g_new, int64_t g_old,
+                                     int64_t *__restrict__ stats) {
+  stats[0] += (int64_t)acc_new[0] - (int64_t)acc_old[0];
+  stats[1] += (int64_t)acc_new[1] - (int64_t)acc_old[1];
+  stats[2] += g_new - g_old;
 }
 
 __global__ void k_region_stats(const unsigned long long *__restrict__ acc, int64_t G, int64_t *__restrict__ stats) {

@@ -691,3 +691,71 @@ def test_r32_point_bulk_and_counts_vs_oracle(oracle, q):
     assert np.array_equal(g.delete_many(extra[:20], cnt[:20]), o.delete_many(extra[:20], cnt[:20]))
     same_image(g, o)
     g.validate()
+
+
+@pytest.mark.parametrize("r", [8, 16])
+def test_local_apply_in_place_equals_oracle(oracle, monkeypatch, r):
+    """Batches that touch at most a quarter of the regions are applied in
+    place, region by region (apply_local_t: only the regions holding new
+    items and their successors are decoded, merged, placed and rewritten);
+    images equal the oracle's after every batch -- inserts with and without
+    counts, point and bulk order, deletes with absent keys -- and the shift
+    metric equals the whole-table path's (FK_GQF_LOCAL=0)."""
+    from paper_2212_09005_b200 import Gqf
+    monkeypatch.setenv("FK_GQF_SMALL", "0")  # the small-batch path would take these batches
+    rng = np.random.default_rng(40 + r)
+    q = 22
+    base = rng.integers(0, 2 ** 62, int(0.6 * (1 << q)), dtype=np.uint64)
+    g, h = Gqf(q=q, r=r, seed=3), Gqf(q=q, r=r, seed=3)
+    o = _oracle(g, oracle)
+    for f in (g, h, o):
+        f.bulk_insert(base)
+    cur, local_runs = g._cur, 0
+    for step in range(10):
+        keys = rng.integers(0, 2 ** 62, int(rng.integers(5, 40)), dtype=np.uint64)
+        keys = np.concatenate([keys, base[rng.integers(0, len(base), 10)]])  # <= 50 regions + successors
+        cnt = rng.integers(1, 30, len(keys)).astype(np.uint64) if step % 2 else None
+        kind = step % 4
+        outs = []
+        for f, local in ((g, "1"), (h, "0"), (o, None)):
+            if local is not None:
+                monkeypatch.setenv("FK_GQF_LOCAL", local)
+            if kind == 0:
+                outs.append(f.bulk_insert(keys, cnt))
+            elif kind == 1:
+                outs.append(f.insert_many(keys, cnt))
+            elif kind == 2:
+                outs.append(np.asarray(f.bulk_delete(keys, cnt)).astype(bool))
+            else:
+                outs.append(np.asarray(f.delete_many(keys, cnt)).astype(bool))
+        if kind >= 2:
+            assert np.array_equal(outs[0], outs[2]) and np.array_equal(outs[1], outs[2]), step
+        same_image(g, o)
+        assert g.shifted_slots == h.shifted_slots, step
+        local_runs += g._cur is cur  # applied in place: the image was not swapped for a rebuilt one
+        cur = g._cur
+    assert local_runs == 10
+    g.validate()
+
+
+def test_local_apply_capacity_falls_back_exactly(oracle, monkeypatch):
+    """A mid-size point batch that crosses the load ceiling: the local path's
+    plan pass sees the ceiling and the exact sequential path reproduces the
+    reference's partial application and CapacityError."""
+    from paper_2212_09005_b200 import CapacityError, Gqf
+    monkeypatch.setenv("FK_GQF_SMALL", "0")
+    rng = np.random.default_rng(77)
+    q = 22
+    g = Gqf(q=q, r=8, max_load=0.5)
+    o = _oracle(g, oracle)
+    # every occurrence of the fill takes one slot: 50 slots left under the ceiling
+    fill = rng.integers(0, 2 ** 62, g.params.max_occupied - 50, dtype=np.uint64)
+    g.bulk_insert(fill)
+    o.bulk_insert(fill)
+    keys = rng.integers(0, 2 ** 62, 25, dtype=np.uint64)  # ~4 slots each
+    cnt = np.full(25, 400, np.uint64)
+    with pytest.raises(CapacityError):
+        g.insert_many(keys, cnt)
+    code, _ = o.insert_many(keys, cnt)
+    assert code != 0
+    same_image(g, o)
