@@ -136,17 +136,6 @@ cudaError_t cub_reduce_by_key(Scratch &S, const uint64_t *keys, uint64_t *uniq, 
   return cub::DeviceReduce::ReduceByKey(tmp, tb, keys, uniq, vals, sums, num, SatAdd(), n, S.st);
 }
 
-cudaError_t cub_excl_scan_by_key(Scratch &S, const uint64_t *keys, const uint64_t *vals, uint64_t *out, int64_t n) {
-  size_t tb = 0;
-  cudaError_t e = cub::DeviceScan::ExclusiveScanByKey(nullptr, tb, keys, vals, out, SatAdd(), (uint64_t)0, n,
-                                                      cuda::std::equal_to<>(), S.st);
-  if (e) return e;
-  void *tmp = S.get<char>(tb);
-  if (!tmp) return S.err;
-  return cub::DeviceScan::ExclusiveScanByKey(tmp, tb, keys, vals, out, SatAdd(), (uint64_t)0, n,
-                                             cuda::std::equal_to<>(), S.st);
-}
-
 cudaError_t cub_excl_sum_i64(Scratch &S, const int64_t *in, int64_t *out, int64_t n) {
   size_t tb = 0;
   cudaError_t e = cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, n, S.st);
@@ -570,7 +559,7 @@ int apply_local_t(Scratch &S, const fk_gqf_geom *g, const fk_gqf_tables *cur, co
   uint64_t *o2_fp = S.get<uint64_t>(g_old), *o2_cnt = S.get<uint64_t>(g_old);
   uint64_t *u2_fp = S.get<uint64_t>(m), *u2_cnt = S.get<uint64_t>(m);
   if (S.err) return -(int)S.err;
-  k_keep_old<<<blocks_for(g_old), 256, 0, st>>>(o_fp, g_old, uniq, m, keep_o);
+  k_keep_old_runs<<<blocks_for((g_old + 31) / 32), 256, 0, st>>>(o_fp, g_old, uniq, m, keep_o);
   k_nonzero<<<blocks_for(m), 256, 0, st>>>(c_new, m, keep_u);
   FK_TRY(cub_select_flagged(S, o_fp, keep_o, o2_fp, d_num, g_old));
   FK_TRY(cub_select_flagged(S, o_cnt, keep_o, o2_cnt, d_num + 1, g_old));
@@ -772,27 +761,15 @@ int apply_t(const fk_gqf_geom *g, const fk_gqf_tables *cur, const fk_gqf_tables 
     // fingerprint was present
     k_found_distinct<<<blocks_for(n), 256, 0, st>>>(c_old, idx_s, n, found);
   } else if (is_del && found) {
-    uint64_t *pre = S.get<uint64_t>(n);
-    if (S.err) return -(int)S.err;
-    if (order == FK_ORDER_POINT) {
-      FK_CU(cub_excl_scan_by_key(S, fps_s, del_s, pre, n));
-    } else {
-      // bulk: each region is applied in descending order (gqf.py:317-325), so
-      // equal fingerprints are processed last-input-first
-      uint64_t *rf = S.get<uint64_t>(n), *rd = S.get<uint64_t>(n), *rp = S.get<uint64_t>(n);
-      if (S.err) return -(int)S.err;
-      k_reverse_u64<<<blocks_for(n), 256, 0, st>>>(fps_s, n, rf);
-      k_reverse_u64<<<blocks_for(n), 256, 0, st>>>(del_s, n, rd);
-      FK_CU(cub_excl_scan_by_key(S, rf, rd, rp, n));
-      k_reverse_u64<<<blocks_for(n), 256, 0, st>>>(rp, n, pre);
-    }
     // segment (unique fingerprint) of every sorted item: exclusive sum of
-    // segment heads, instead of a binary search per item
+    // segment heads; then one thread per segment walks its copies in the
+    // facade's order (bulk: each region descending, gqf.py:317-325)
     int64_t *heads = S.get<int64_t>(n), *seg = S.get<int64_t>(n);
     if (S.err) return -(int)S.err;
     k_seg_heads<<<blocks_for(n), 256, 0, st>>>(fps_s, n, heads);
     FK_CU(cub_excl_sum_i64(S, heads, seg, n));
-    k_found_flags<<<blocks_for(n), 256, 0, st>>>(pre, idx_s, seg, c_old, n, found);
+    k_found_walk<<<blocks_for(n), 256, 0, st>>>(fps_s, del_s, idx_s, seg, c_old, n, order == FK_ORDER_BULK ? 1 : 0,
+                                                found);
   }
 
   // 8'. region-local apply in place (mid-size batches; apply_local_t)
@@ -841,7 +818,7 @@ int apply_t(const fk_gqf_geom *g, const fk_gqf_tables *cur, const fk_gqf_tables 
     uint64_t *o2_fp = S.get<uint64_t>(g_old), *o2_cnt = S.get<uint64_t>(g_old);
     uint64_t *u2_fp = S.get<uint64_t>(m), *u2_cnt = S.get<uint64_t>(m);
     if (S.err) return -(int)S.err;
-    k_keep_old<<<blocks_for(g_old), 256, 0, st>>>(o_fp, g_old, uniq, m, keep_o);
+    k_keep_old_runs<<<blocks_for((g_old + 31) / 32), 256, 0, st>>>(o_fp, g_old, uniq, m, keep_o);
     k_nonzero<<<blocks_for(m), 256, 0, st>>>(c_new, m, keep_u);
     FK_CU(cub_select_flagged(S, o_fp, keep_o, o2_fp, d_num, g_old));
     FK_CU(cub_select_flagged(S, o_cnt, keep_o, o2_cnt, d_num + 1, g_old));

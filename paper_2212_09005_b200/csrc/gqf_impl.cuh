@@ -703,18 +703,52 @@ __global__ void k_seg_heads(const uint64_t *__restrict__ fps_s, int64_t n, int64
     heads[j] = (j + 1 < n && fps_s[j + 1] != fps_s[j]) ? 1 : 0;
 }
 
-// found flag of sorted item j: its copies before it in processing order
-// (pre[j]) leave something of the old count of its fingerprint
-__global__ void k_found_flags(const uint64_t *__restrict__ pre, const uint32_t *__restrict__ idx_s,
-                              const int64_t *__restrict__ seg, const uint64_t *__restrict__ c_old, int64_t n,
-                              uint8_t *__restrict__ found) {
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
-    found[idx_s[j]] = pre[j] < c_old[seg[j]] ? 1 : 0;
+// found flags of a delete batch with repeated fingerprints, one thread per
+// fingerprint segment of the sorted batch (segments are short): the copies
+// are processed in the facade's order -- input order for point deletes,
+// last-input-first for bulk deletes (gqf.py:317-325) -- and copy k finds the
+// key iff the deltas of the copies before it leave part of the old count.
+__global__ void k_found_walk(const uint64_t *__restrict__ fps_s, const uint64_t *__restrict__ del_s,
+                             const uint32_t *__restrict__ idx_s, const int64_t *__restrict__ seg,
+                             const uint64_t *__restrict__ c_old, int64_t n, int bulk_order,
+                             uint8_t *__restrict__ found) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t f = fps_s[j];
+    if (j > 0 && fps_s[j - 1] == f) continue;  // not a segment head
+    int64_t e = j + 1;
+    while (e < n && fps_s[e] == f) e++;
+    const uint64_t c = c_old[seg[j]];
+    uint64_t pre = 0;
+    for (int64_t t = 0; t < e - j; t++) {
+      const int64_t k = bulk_order ? e - 1 - t : j + t;
+      found[idx_s[k]] = pre < c ? 1 : 0;
+      const uint64_t d = del_s[k], sum = pre + d;
+      pre = sum < pre ? ~0ull : sum;  // saturating, as the reference's counts
+    }
+  }
 }
 
-__global__ void k_reverse_u64(const uint64_t *__restrict__ a, int64_t n, uint64_t *__restrict__ b) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    b[n - 1 - i] = a[i];
+// Old items the batch updates are dropped before the merge: both lists are
+// sorted, so each thread binary-searches its first item of a run of 32 and
+// walks the batch's fingerprints forward alongside the rest.
+__global__ void k_keep_old_runs(const uint64_t *__restrict__ o_fp, int64_t g_old, const uint64_t *__restrict__ uniq,
+                                int64_t m, uint8_t *__restrict__ keep) {
+  constexpr int RUN = 32;
+  const int64_t runs = (g_old + RUN - 1) / RUN;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < runs; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = t * RUN, e = a + RUN < g_old ? a + RUN : g_old;
+    int64_t lo = 0, hi = m;
+    const uint64_t f0 = o_fp[a];
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (uniq[mid] < f0) lo = mid + 1; else hi = mid;
+    }
+    for (int64_t i = a; i < e; i++) {
+      const uint64_t f = o_fp[i];
+      while (lo < m && uniq[lo] < f) lo++;
+      keep[i] = (lo < m && uniq[lo] == f) ? 0 : 1;
+    }
+  }
 }
 
 // Decode pass over occupied quotient words: mode 0 counts groups per word,
@@ -780,21 +814,7 @@ __global__ void k_decode_region_words(GqfDev T, const int64_t *__restrict__ creg
   }
 }
 
-// Old items whose fingerprint the batch updates are dropped before the merge
-// (their replacement carries the new absolute count); so are zero counts.
-__global__ void k_keep_old(const uint64_t *__restrict__ o_fp, int64_t g_old, const uint64_t *__restrict__ uniq,
-                           int64_t m, uint8_t *__restrict__ keep) {
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < g_old; j += (int64_t)gridDim.x * blockDim.x) {
-    uint64_t f = o_fp[j];
-    int64_t lo = 0, hi = m;
-    while (lo < hi) {
-      int64_t mid = (lo + hi) >> 1;
-      if (uniq[mid] < f) lo = mid + 1; else hi = mid;
-    }
-    keep[j] = (lo < m && uniq[lo] == f) ? 0 : 1;
-  }
-}
-
+// zero new counts are dropped before the merge
 __global__ void k_nonzero(const uint64_t *__restrict__ c, int64_t m, uint8_t *__restrict__ keep) {
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += (int64_t)gridDim.x * blockDim.x)
     keep[j] = c[j] > 0 ? 1 : 0;

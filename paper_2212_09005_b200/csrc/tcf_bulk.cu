@@ -561,6 +561,14 @@ __global__ void __launch_bounds__(kRouteW, 1) k_btcf_route_prefix(const uint32_t
 // kernel runs the sweeps (two grid barriers each); if it has not converged
 // after kJacobiMax sweeps the caller runs the sequential walk instead.
 constexpr int kJT = 256, kJItems = 1, kJTile = kJT * kJItems, kJacobiMax = 4096;
+constexpr int kJHeld = 2;  // items a thread keeps in registers across the sweeps
+// With few tiles the tile sums live 256 bytes apart: the L2 slice of an
+// address is chosen from bit 8 up, so packed counters put every tile's
+// atomics on a few slices (measured at 2^20 slots: the decision pass was
+// bound by them, 17.8 -> 7.9 us per sweep).  With many tiles they stay
+// packed: every tile's offset sums all earlier tile sums (O(T^2) reads),
+// which strided counters would turn into one sector each (2^24: 2x slower).
+constexpr int kTsStride = 64, kTsStrideMaxTiles = 4096;
 // never a decision (decisions are a block index or -1)
 constexpr uint32_t kNoB = 0xFFFFFFFEu;
 
@@ -583,7 +591,8 @@ struct RouteJ {
   const uint32_t *pos1, *pos2;  // [m] item -> positions (tile of its flags)
   int32_t *d;                 // [m] decisions (in/out)
   uint32_t *P1, *P2;          // [m + 1] exclusive prefix sums
-  uint32_t *ts;               // [2 parities][2 orders][T] tile sums
+  uint32_t *ts;               // [2 parities][2 orders][T] tile sums, tss apart
+  int tss;                    // tile-sum stride (kTsStride or 1)
   unsigned *ctl;              // [3] sweeps run, [4] converged
   unsigned *chg;              // [gridDim] this CTA's decisions changed in the last sweep
   unsigned long long *clk;    // optional (FK_ROUTE_STATS): globaltimer at each phase end, CTA 0
@@ -612,10 +621,10 @@ __device__ __forceinline__ void route_tally(const RouteJ &R, uint32_t *tsn, bool
   if (!(c1 || c2)) return;
   const uint32_t slot = c1 ? p1 / kJTile : (uint32_t)R.T + p2 / kJTile;
   const unsigned peers = __match_any_sync(act, slot);
-  if ((threadIdx.x & 31) == (unsigned)(__ffs(peers) - 1)) atomicAdd(&tsn[slot], (unsigned)__popc(peers));
+  if ((threadIdx.x & 31) == (unsigned)(__ffs(peers) - 1)) atomicAdd(&tsn[(size_t)slot * R.tss], (unsigned)__popc(peers));
 }
 
-__global__ void __launch_bounds__(kJT) k_btcf_route_jacobi(RouteJ R) {
+__global__ void __launch_bounds__(kJT, 3) k_btcf_route_jacobi(RouteJ R) {
   cg::grid_group grid = cg::this_grid();
   typedef cub::BlockScan<unsigned long long, kJT> Scan;
   typedef cub::BlockReduce<unsigned long long, kJT> Red;
@@ -645,20 +654,44 @@ __global__ void __launch_bounds__(kJT) k_btcf_route_jacobi(RouteJ R) {
     route_tally(R, R.ts, live, d, c.x, c.y, p1, p2);
   }
   grid.sync();
+  // items held in registers across the sweeps when every thread has at most
+  // kJHeld of them: their static positions and their last decision
+  const bool held = m <= kJHeld * nth;
+  RouteItem hit[kJHeld];
+  int32_t hd[kJHeld];
+#pragma unroll
+  for (int u = 0; u < kJHeld; u++) {
+    const int64_t k = tid + u * nth;
+    if (held && k < m) {
+      hit[u] = R.it[k];
+      hd[u] = __ldcg(&R.d[k]);
+    } else {
+      hit[u].p = hit[u].q = hit[u].c = make_uint4(0, 0, 0, 0);
+      hd[u] = -1;
+    }
+  }
   if (R.clk && tid == 0) R.clk[0] = gtimer();
   for (unsigned sweep = 0;; sweep++) {
     const int par = sweep & 1;
-    uint32_t *ts = R.ts + (size_t)par * 2 * T, *tsn = R.ts + (size_t)(par ^ 1) * 2 * T;
+    uint32_t *ts = R.ts + (size_t)par * 2 * T * R.tss, *tsn = R.ts + (size_t)(par ^ 1) * 2 * T * R.tss;
     // ---- phase S: P1, P2 of the current iterate (tile scans + tile offsets)
-    for (int64_t i = tid; i < 2 * (int64_t)T; i += nth) tsn[i] = 0;
+    for (int64_t i = tid; i < 2 * (int64_t)T; i += nth) tsn[i * R.tss] = 0;
+    unsigned long long off_acc = 0;  // (thread 0) sum of the tile sums before this CTA's current tile
+    int done_to = 0;
     for (int t = blockIdx.x; t < T; t += gridDim.x) {
-      // offsets: sums of the tile sums before t, both orders packed (P1 << 32 | P2)
+      // offsets: sums of the tile sums before t, both orders packed (P1 << 32 | P2),
+      // accumulated over this CTA's tiles so every tile sum is read once per CTA
       unsigned long long part = 0;
-      for (int u = threadIdx.x; u < t; u += kJT) part += ((unsigned long long)__ldcg(&ts[u]) << 32) | __ldcg(&ts[T + u]);
-      unsigned long long off = Red(tmp.red).Sum(part);
-      if (threadIdx.x == 0) s_off = off;
+      for (int u = done_to + threadIdx.x; u < t; u += kJT)
+        part += ((unsigned long long)__ldcg(&ts[(size_t)u * R.tss]) << 32) | __ldcg(&ts[(size_t)(T + u) * R.tss]);
+      const unsigned long long add = Red(tmp.red).Sum(part);
+      done_to = t;
+      if (threadIdx.x == 0) {
+        off_acc += add;
+        s_off = off_acc;
+      }
       __syncthreads();
-      off = s_off;
+      unsigned long long off = s_off;
       unsigned long long v[kJItems];
       const int64_t p0 = (int64_t)t * kJTile + (int64_t)threadIdx.x * kJItems;
       uint32_t i1[kJItems], i2[kJItems];
@@ -700,11 +733,47 @@ __global__ void __launch_bounds__(kJT) k_btcf_route_jacobi(RouteJ R) {
     grid.sync();
     if (R.clk && tid == 0 && sweep < 64) R.clk[2 + 3 * sweep] = gtimer();
     // ---- phase D: every decision from the counts of the current iterate
-    // U items per thread per trip, every load of the U items issued before
-    // any is used (the sweep is a latency chain: item -> P reads -> tally)
-    constexpr int U = 1;
     unsigned changed = 0;
-    for (int64_t k0 = tid; k0 < mr; k0 += U * nth) {
+    if (held) {
+      // the thread's items are in registers since sweep 0: the sixteen P
+      // reads of its two items go out together (one dependent trip)
+      uint32_t v[kJHeld][8];
+#pragma unroll
+      for (int u = 0; u < kJHeld; u++) {
+        if (tid + u * nth < m) {
+          v[u][0] = __ldcg(&R.P1[hit[u].p.x]);
+          v[u][1] = __ldcg(&R.P1[hit[u].p.y]);
+          v[u][2] = __ldcg(&R.P2[hit[u].p.z]);
+          v[u][3] = __ldcg(&R.P2[hit[u].p.w]);
+          v[u][4] = __ldcg(&R.P1[hit[u].q.x]);
+          v[u][5] = __ldcg(&R.P1[hit[u].q.y]);
+          v[u][6] = __ldcg(&R.P2[hit[u].q.z]);
+          v[u][7] = __ldcg(&R.P2[hit[u].q.w]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kJHeld; u++) {
+        const int64_t k = tid + u * nth;
+        if (k >= mr) break;  // warp-uniform
+        const bool live = k < m;
+        int32_t d = -1;
+        const uint4 c = hit[u].c;
+        if (live) {
+          const uint32_t l1 = c.z + (v[u][0] - v[u][1]) + (v[u][2] - v[u][3]);
+          const uint32_t l2 = c.w + (v[u][4] - v[u][5]) + (v[u][6] - v[u][7]);
+          d = route_rule(l1, l2, c.x, c.y, R.B);
+          if (d != hd[u]) {
+            R.d[k] = d;
+            hd[u] = d;
+            changed++;
+          }
+        }
+        route_tally(R, tsn, live, d, c.x, c.y, hit[u].p.x, hit[u].q.z);
+      }
+    }
+    // (more items than threads can hold: stream them)
+    constexpr int U = 1;
+    for (int64_t k0 = held ? mr : tid; k0 < mr; k0 += U * nth) {
       RouteItem it[U];
       int32_t dold[U];
       uint32_t v[U][8];
@@ -1237,7 +1306,8 @@ int route_items(Scratch &S, const uint32_t *a, const uint32_t *b, int64_t m, con
              *e2 = S.get<uint32_t>(nb);
     uint32_t *P1 = S.get<uint32_t>(m + 1), *P2 = S.get<uint32_t>(m + 1);
     const int T = (int)((m + kJTile - 1) / kJTile);
-    uint32_t *ts = S.get<uint32_t>((size_t)4 * T);
+    const int tss = T <= kTsStrideMaxTiles ? kTsStride : 1;
+    uint32_t *ts = S.get<uint32_t>((size_t)4 * T * tss);
     unsigned *ctl = S.get<unsigned>(8), *chg = S.get<unsigned>(4096);
     FK_P(perm1); FK_P(perm2); FK_P(pos1); FK_P(pos2); FK_P(qA); FK_P(qB); FK_P(iota); FK_P(bs);
     FK_P(s1); FK_P(e1); FK_P(s2); FK_P(e2); FK_P(P1); FK_P(P2); FK_P(ts); FK_P(ctl); FK_P(chg);
@@ -1248,7 +1318,7 @@ int route_items(Scratch &S, const uint32_t *a, const uint32_t *b, int64_t m, con
     FK_S(cudaMemsetAsync(e1, 0, nb * 4, st));
     FK_S(cudaMemsetAsync(s2, 0, nb * 4, st));
     FK_S(cudaMemsetAsync(e2, 0, nb * 4, st));
-    FK_S(cudaMemsetAsync(ts, 0, (size_t)16 * T, st));
+    FK_S(cudaMemsetAsync(ts, 0, (size_t)16 * T * tss, st));
     FK_S(cudaMemsetAsync(ctl, 0, 32, st));
     if (a_sorted) {
       FK_S(cudaMemcpyAsync(perm1, iota, m * 4, cudaMemcpyDeviceToDevice, st));
@@ -1275,7 +1345,7 @@ int route_items(Scratch &S, const uint32_t *a, const uint32_t *b, int64_t m, con
     const bool stats = getenv("FK_ROUTE_STATS") != nullptr;
     unsigned long long *clk = stats ? S.get<unsigned long long>(1 + 4 * 64) : nullptr;
     if (stats) FK_S(cudaMemsetAsync(clk, 0, 8 * (1 + 4 * 64), st));
-    RouteJ R{items, perm1, perm2, a_of1, b_of2, pos1, pos2, dest, P1, P2, ts, ctl, chg, clk, m, T, B};
+    RouteJ R{items, perm1, perm2, a_of1, b_of2, pos1, pos2, dest, P1, P2, ts, tss, ctl, chg, clk, m, T, B};
     int grid = coop_grid((const void *)k_btcf_route_jacobi, kJT);
     if (!grid) return FK_E_ARG;
     const int64_t want = (m + kJT - 1) / kJT;
