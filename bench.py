@@ -645,9 +645,11 @@ def _workload_kernel(workload, op):
         return {"insert": "fk_btcf_insert pipeline (CUB partition sort + k_btcf_merge + route + backing)",
                 "query_pos": "k_btcf_query", "query_neg": "k_btcf_query",
                 "delete": "fk_btcf_delete pipeline (sort + k_btcf_delete x2 + backing)"}[op]
-    return {"bulk_insert": "fk_gqf_apply insert pipeline (hash/split + radix sort + RLE + decode/merge/place)",
+    return {"bulk_insert": "fk_gqf_apply insert pipeline (hash + two MSD partition passes + shared-memory "
+                           "aggregation + decode/merge + region-parallel placement)",
             "count": "k_gqf_count",
-            "bulk_delete": "fk_gqf_apply delete pipeline (sort + reduce + decode/merge/place)"}[op]
+            "bulk_delete": "fk_gqf_apply delete pipeline (sort + reduce + found walk + decode/merge + "
+                           "region-parallel placement)"}[op]
 
 
 def _workload_traffic(workload, op, items):
