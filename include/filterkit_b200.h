@@ -344,6 +344,27 @@ int fk_live_slots(const void *slots, int slot_bytes, int64_t n, const uint32_t *
  * position order, *count (device int64) their number.  Asynchronous. */
 int fk_kmer_windows(const uint8_t *seq, int64_t n, int k, uint64_t *out, int64_t *count, void *stream);
 
+/* numpy's default_rng streams on the device (workloads.py:61-118): the state
+ * and increment are the 128-bit values of Generator.bit_generator.state.
+ * fk_pcg64_raw: out[i] = output start + i + 1 (= bit_generator.random_raw).
+ * fk_bounded_integers: Generator.integers(low, high, n) for high - low <=
+ * 2^32 (int64 out, device); *consumed (HOST) = 64-bit outputs used.
+ * fk_zipf_bounded: the ranks of workloads.zipf_bounded(rng, s, universe, n)
+ * (int64 out, device) given its h_lo / h_hi / squeeze constants (computed
+ * on the host as the reference does); *consumed = doubles drawn.
+ * fk_mix_offsets: out[i] = mix64(base + offsets[i]) (the zipf keys).
+ * fk_shuffle_u64: a device permutation of n keys by a seeded sort (not
+ * numpy's Fisher-Yates order).  The first three synchronise. */
+int fk_pcg64_raw(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, uint64_t start, int64_t n,
+                 uint64_t *out, void *stream);
+int fk_bounded_integers(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t low,
+                        int64_t high, int64_t n, int64_t *out, int64_t *consumed, void *stream);
+int fk_zipf_bounded(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, double s,
+                    int64_t universe, int64_t n, double h_lo, double h_hi, double squeeze, int64_t *ranks,
+                    int64_t *consumed, void *stream);
+int fk_mix_offsets(uint64_t base, const int64_t *offsets, int64_t n, uint64_t *out, void *stream);
+int fk_shuffle_u64(const uint64_t *in, int64_t n, uint64_t seed, uint64_t *out, void *stream);
+
 /* ---- hash-prefix sharding (new in this build) -------------- */
 
 /* Stable partition of a key batch by owner shard, owner = bits

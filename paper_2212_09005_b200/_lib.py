@@ -89,6 +89,13 @@ _SIGS = {
                                         c_vp]),
     "fk_gqf_cluster_stats": (c_i32, [ctypes.POINTER(GqfGeom), ctypes.POINTER(GqfTables), c_vp, c_vp]),
     "fk_kmer_windows": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp, c_vp]),
+    "fk_pcg64_raw": (c_i32, [c_u64, c_u64, c_u64, c_u64, c_u64, c_i64, c_vp, c_vp]),
+    "fk_bounded_integers": (c_i32, [c_u64, c_u64, c_u64, c_u64, c_i64, c_i64, c_i64, c_vp, ctypes.POINTER(c_i64),
+                                    c_vp]),
+    "fk_zipf_bounded": (c_i32, [c_u64, c_u64, c_u64, c_u64, ctypes.c_double, c_i64, c_i64, ctypes.c_double,
+                                ctypes.c_double, ctypes.c_double, c_vp, ctypes.POINTER(c_i64), c_vp]),
+    "fk_mix_offsets": (c_i32, [c_u64, c_vp, c_i64, c_vp, c_vp]),
+    "fk_shuffle_u64": (c_i32, [c_vp, c_i64, c_u64, c_vp, c_vp]),
     "fk_live_slots": (c_i32, [c_vp, c_i32, c_i64, c_vp, c_i32, c_vp, c_vp, c_vp]),
     "fk_shard_partition": (c_i32, [c_vp, c_vp, c_i64, c_u64, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "fk_shard_unpermute": (c_i32, [c_vp, c_vp, c_i64, c_i32, c_vp, c_vp]),

@@ -96,3 +96,52 @@ def test_kmer_windows_device_match_reference_golden(golden, tmp_path):
     for k in (1, 4, 11, 21, 31, 32):
         got = kmer_windows_device(str(p), k).cpu().numpy().view(np.uint64)
         assert np.array_equal(got, g["k%d" % k]), k
+
+
+@pytest.mark.parametrize("seed,start", [(0, 0), (123, 12345), (2 ** 63 + 5, 1)])
+def test_pcg64_device_matches_numpy(seed, start):
+    """numpy's default_rng bit generator on the device (fk_pcg64_raw), with
+    jump-ahead to any position: random_raw, bit for bit."""
+    from paper_2212_09005_b200.workloads import pcg64_raw_device
+    g = np.random.default_rng(seed)
+    if start:
+        g.bit_generator.random_raw(start)
+    want = g.bit_generator.random_raw(100_003)
+    got = pcg64_raw_device(seed, 100_003, start=start).cpu().numpy().view(np.uint64)
+    assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("low,high", [(1, 101), (0, 7), (5, 6), (0, 2 ** 32), (-3, 1000003)])
+def test_bounded_integers_device_match_numpy(low, high):
+    """Generator.integers(low, high, n) on the device (fk_bounded_integers):
+    Lemire's method on the buffered 32-bit draws, rejections included."""
+    from paper_2212_09005_b200.workloads import integers_device
+    for seed in (3, 99):
+        want = np.random.default_rng(seed).integers(low, high, 300_001)
+        got = integers_device(seed, low, high, 300_001).cpu().numpy()
+        assert np.array_equal(got, want), (seed, low, high)
+
+
+@pytest.mark.parametrize("s,universe", [(1.5, 1_000_000), (1.5, 100), (1.0, 5000), (2.5, 10 ** 9)])
+def test_zipf_device_matches_host(s, universe):
+    """The bounded-Zipf rejection-inversion sampler on the device
+    (fk_zipf_bounded) draws the same ranks as the host restatement of the
+    reference's sampler (fk/workloads.py:81-118) on the same generator."""
+    from paper_2212_09005_b200.workloads import zipf_bounded, zipf_bounded_device
+    seed = 1234 + int(universe)
+    want = zipf_bounded(np.random.default_rng(seed), s, universe, 500_000)
+    got = zipf_bounded_device(seed, s, universe, 500_000).cpu().numpy()
+    assert np.array_equal(got, want)
+
+
+def test_gen_keys_device_match_reference_streams():
+    """gen_keys on the device: uniform and zipf streams equal the host
+    generator's (the reference's, restated), ur_count has exactly its
+    multiset."""
+    from paper_2212_09005_b200.workloads import WorkloadSpec, gen_keys, gen_keys_device
+    for spec in (WorkloadSpec("uniform", n=100_000, seed=3), WorkloadSpec("zipf", n=200_000, seed=5),
+                 WorkloadSpec("zipf", n=50_000, seed=6, universe=1000, zipf_s=1.2)):
+        assert np.array_equal(gen_keys_device(spec).cpu().numpy().view(np.uint64), gen_keys(spec)), spec
+    spec = WorkloadSpec("ur_count", n=20_000, seed=7)
+    got = np.sort(gen_keys_device(spec).cpu().numpy().view(np.uint64))
+    assert np.array_equal(got, np.sort(gen_keys(spec)))
