@@ -126,16 +126,6 @@ cudaError_t cub_rle_counts(Scratch &S, const uint64_t *keys, uint64_t *uniq, uin
   return cub::DeviceRunLengthEncode::Encode(tmp, tb, keys, uniq, counts, num, n, S.st);
 }
 
-cudaError_t cub_reduce_by_key(Scratch &S, const uint64_t *keys, uint64_t *uniq, const uint64_t *vals, uint64_t *sums,
-                              int64_t *num, int64_t n) {
-  size_t tb = 0;
-  cudaError_t e = cub::DeviceReduce::ReduceByKey(nullptr, tb, keys, uniq, vals, sums, num, SatAdd(), n, S.st);
-  if (e) return e;
-  void *tmp = S.get<char>(tb);
-  if (!tmp) return S.err;
-  return cub::DeviceReduce::ReduceByKey(tmp, tb, keys, uniq, vals, sums, num, SatAdd(), n, S.st);
-}
-
 cudaError_t cub_excl_sum_i64(Scratch &S, const int64_t *in, int64_t *out, int64_t n) {
   size_t tb = 0;
   cudaError_t e = cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, n, S.st);
@@ -259,6 +249,11 @@ inline bool part_plan(int64_t n, int qr, int *W, int *p2) {
   *W = w;
   *p2 = b;
   return true;
+}
+
+// m = the number of segments (the last item's segment id + 1; 0 when n = 0)
+__global__ void k_seg_count(const int64_t *__restrict__ seg, int64_t n, int64_t *__restrict__ m) {
+  *m = n > 0 ? seg[n - 1] + 1 : 0;
 }
 
 __global__ void k_part_total(const int64_t *__restrict__ uoff, const int64_t *__restrict__ ucount, int64_t NP,
@@ -453,33 +448,85 @@ int apply_small_delete_t(const fk_gqf_geom *g, const fk_gqf_tables *cur, const u
   return 0;
 }
 
+// Decode of the whole table by runs (k_decode_runs): the k-th occupied
+// quotient and the k-th runend from a global rank/select of the two bit
+// vectors, then one thread per run -- pass 0 counts each run's groups,
+// pass 1 writes them at the scanned offsets.  Scratch stays in S.
+// threads for a warp_join over n probes (one warp per kJoinChunk)
+inline int64_t join_threads(int64_t n) { return (n + kJoinChunk - 1) / kJoinChunk * 32; }
+
+struct RunDecode {
+  int64_t K = 0, items = 0;
+  int64_t *Q = nullptr, *E = nullptr, *gcount = nullptr, *goff = nullptr;
+  int *err = nullptr;
+};
+
+template <typename S_t>
+int decode_runs_count(Scratch &S, const fk_gqf_geom *g, const fk_gqf_tables *t, const GqfDev &T, RunDecode *D,
+                      cudaStream_t st) {
+  const int64_t nbw = g->phys >> 6;
+  int64_t *pops = S.get<int64_t>(2 * nbw), *poff = S.get<int64_t>(2 * nbw);
+  D->err = S.get<int>(4);
+  if (S.err) return -(int)S.err;
+  int64_t hk[4] = {0, 0, 0, 0};
+  FK_CU(cudaMemsetAsync(D->err, 0, 4 * sizeof(int), st));
+  k_word_popc<<<blocks_for(nbw), 256, 0, st>>>(t->occupieds, nbw, pops);
+  k_word_popc<<<blocks_for(nbw), 256, 0, st>>>(t->runends, nbw, pops + nbw);
+  FK_CU(cub_excl_sum_i64(S, pops, poff, nbw));
+  FK_CU(cub_excl_sum_i64(S, pops + nbw, poff + nbw, nbw));
+  FK_CU(cudaMemcpyAsync(&hk[0], poff + nbw - 1, 8, cudaMemcpyDeviceToHost, st));
+  FK_CU(cudaMemcpyAsync(&hk[1], pops + nbw - 1, 8, cudaMemcpyDeviceToHost, st));
+  FK_CU(cudaMemcpyAsync(&hk[2], poff + 2 * nbw - 1, 8, cudaMemcpyDeviceToHost, st));
+  FK_CU(cudaMemcpyAsync(&hk[3], pops + 2 * nbw - 1, 8, cudaMemcpyDeviceToHost, st));
+  FK_CU(cudaStreamSynchronize(st));
+  D->K = hk[0] + hk[1];
+  if (D->K != hk[2] + hk[3]) return FK_E_INVARIANT;  // occupieds / runends set-bit counts differ
+  D->Q = S.get<int64_t>(D->K);
+  D->E = S.get<int64_t>(D->K);
+  D->gcount = S.get<int64_t>(D->K);
+  D->goff = S.get<int64_t>(D->K);
+  if (S.err) return -(int)S.err;
+  D->items = 0;
+  if (D->K == 0) return 0;
+  k_bit_positions<<<blocks_for(nbw), 256, 0, st>>>(t->occupieds, nbw, poff, D->Q);
+  k_bit_positions<<<blocks_for(nbw), 256, 0, st>>>(t->runends, nbw, poff + nbw, D->E);
+  k_decode_runs<S_t><<<blocks_for(D->K), 256, 0, st>>>(T, D->Q, D->E, D->K, 0, D->gcount, nullptr, nullptr, nullptr,
+                                                      D->err);
+  FK_CU(cub_excl_sum_i64(S, D->gcount, D->goff, D->K));
+  int64_t tail[2] = {0, 0};
+  int h_err = 0;
+  FK_CU(cudaMemcpyAsync(&tail[0], D->goff + D->K - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  FK_CU(cudaMemcpyAsync(&tail[1], D->gcount + D->K - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  FK_CU(cudaMemcpyAsync(&h_err, D->err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  FK_CU(cudaStreamSynchronize(st));
+  if (h_err) return FK_E_INVARIANT;
+  D->items = tail[0] + tail[1];
+  return 0;
+}
+
+template <typename S_t>
+int decode_runs_write(const GqfDev &T, const RunDecode &D, uint64_t *fp_out, uint64_t *cnt_out, cudaStream_t st) {
+  if (D.K == 0) return 0;
+  k_decode_runs<S_t><<<blocks_for(D.K), 256, 0, st>>>(T, D.Q, D.E, D.K, 1, nullptr, D.goff, fp_out, cnt_out, D.err);
+  FK_CHECK_LAUNCH();
+  return 0;
+}
+
 // (fingerprint, count) items of the whole table in fingerprint order, by
-// the decode pass the rebuild uses (two passes: per-word group counts, then
-// writes at the scanned offsets).  *count_out = the number of items; nothing
-// is written when it exceeds cap.
+// the run decode the rebuild uses.  *count_out = the number of items;
+// nothing is written when it exceeds cap.
 template <typename S_t>
 int enumerate_t(const fk_gqf_geom *g, const fk_gqf_tables *t, uint64_t *fp_out, uint64_t *cnt_out, int64_t cap,
                 int64_t *count_out, cudaStream_t st) {
   Scratch S(st);
   GqfDev T = make_dev(g, t);
-  const int64_t nqw = ((1LL << g->q) + 63) >> 6;
-  int64_t *gcount = S.get<int64_t>(nqw), *goff = S.get<int64_t>(nqw);
-  int *d_err = S.get<int>(4);
-  if (S.err) return -(int)S.err;
-  FK_CU(cudaMemsetAsync(d_err, 0, 4 * sizeof(int), st));
-  k_decode_words<S_t><<<blocks_for(nqw), 256, 0, st>>>(T, nqw, 0, gcount, nullptr, nullptr, nullptr, d_err);
-  FK_CU(cub_excl_sum_i64(S, gcount, goff, nqw));
-  int64_t tail[2];
-  int h_err = 0;
-  FK_CU(cudaMemcpyAsync(&tail[0], goff + nqw - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  FK_CU(cudaMemcpyAsync(&tail[1], gcount + nqw - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  FK_CU(cudaMemcpyAsync(&h_err, d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
-  FK_CU(cudaStreamSynchronize(st));
-  if (h_err) return FK_E_INVARIANT;
-  *count_out = tail[0] + tail[1];
+  RunDecode D;
+  int rc = decode_runs_count<S_t>(S, g, t, T, &D, st);
+  if (rc) return rc;
+  *count_out = D.items;
   if (*count_out > cap) return 0;
-  k_decode_words<S_t><<<blocks_for(nqw), 256, 0, st>>>(T, nqw, 1, nullptr, goff, fp_out, cnt_out, d_err);
-  FK_CHECK_LAUNCH();
+  rc = decode_runs_write<S_t>(T, D, fp_out, cnt_out, st);
+  if (rc) return rc;
   FK_CU(cudaStreamSynchronize(st));
   return 0;
 }
@@ -505,13 +552,14 @@ int count_t(const fk_gqf_geom *g, const fk_gqf_tables *t, const uint64_t *keys, 
 // applicable: the caller continues with the global path), 2 (the exact
 // path is needed; *load_possible set), or < 0.
 constexpr int kApplyDryFlag = 1;
-template <typename S_t>
-int apply_local_t(Scratch &S, const fk_gqf_geom *g, const fk_gqf_tables *cur, const uint64_t *keys, int keys_are_fps,
-                  uint64_t fmask, int64_t n, const uint64_t *uniq, const uint64_t *c_new, int64_t m, bool is_del,
-                  int order, int flags, fk_gqf_result *res, bool *load_possible) {
+// Regions the batch's fingerprints touch (creg[0..K)); K = -1 for tables too
+// small to split.
+int local_regions(Scratch &S, const fk_gqf_geom *g, const uint64_t *uniq, int64_t m, int64_t **creg_out,
+                  int64_t *K_out) {
   cudaStream_t st = S.st;
   const int64_t nqr = g->quotient_regions;
-  if (m <= 0 || nqr < 8) return 1;
+  *K_out = -1;
+  if (m <= 0 || nqr < 8) return 0;
   int64_t *rbu = S.get<int64_t>(nqr + 1), *creg = S.get<int64_t>(nqr), *d_k = S.get<int64_t>(1);
   uint8_t *cand = S.get<uint8_t>(nqr);
   if (S.err) return -(int)S.err;
@@ -528,10 +576,26 @@ int apply_local_t(Scratch &S, const fk_gqf_geom *g, const fk_gqf_tables *cur, co
   int64_t K = 0;
   FK_TRY(cudaMemcpyAsync(&K, d_k, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   FK_TRY(cudaStreamSynchronize(st));
+  if (getenv("FK_GQF_TRACE"))
+    fprintf(stderr, "fk gqf local: m=%lld listed regions %lld of %lld\n", (long long)m, (long long)K,
+            (long long)nqr);
+  *creg_out = creg;
+  *K_out = K;
+  return 0;
+}
+
+// Regions listed by local_regions: K > 0 and at most a quarter of them.
+inline bool local_applicable(const fk_gqf_geom *g, int64_t K) { return K > 0 && 4 * K <= g->quotient_regions; }
+
+template <typename S_t>
+int apply_local_t(Scratch &S, const fk_gqf_geom *g, const fk_gqf_tables *cur, const int64_t *creg, int64_t K,
+                  const uint64_t *keys, int keys_are_fps, uint64_t fmask, int64_t n, const uint64_t *uniq,
+                  const uint64_t *c_new, int64_t m, bool is_del, int order, int flags, fk_gqf_result *res,
+                  bool *load_possible) {
+  cudaStream_t st = S.st;
+  const int64_t nqr = g->quotient_regions;
+  if (!local_applicable(g, K)) return 1;
   const bool trace = getenv("FK_GQF_TRACE") != nullptr;
-  if (trace) fprintf(stderr, "fk gqf local: m=%lld listed regions %lld of %lld\n", (long long)m, (long long)K,
-                     (long long)nqr);
-  if (K == 0 || 4 * K > nqr) return 1;
   GqfDev T0 = make_dev(g, cur);
   // old items of the listed regions
   const int64_t nqw = ((1LL << g->q) + 63) >> 6, nw = K * (kRegionSlots / 64);
@@ -559,7 +623,7 @@ int apply_local_t(Scratch &S, const fk_gqf_geom *g, const fk_gqf_tables *cur, co
   uint64_t *o2_fp = S.get<uint64_t>(g_old), *o2_cnt = S.get<uint64_t>(g_old);
   uint64_t *u2_fp = S.get<uint64_t>(m), *u2_cnt = S.get<uint64_t>(m);
   if (S.err) return -(int)S.err;
-  k_keep_old_runs<<<blocks_for((g_old + 31) / 32), 256, 0, st>>>(o_fp, g_old, uniq, m, keep_o);
+  k_keep_old_join<<<blocks_for(join_threads(g_old)), 256, 0, st>>>(o_fp, g_old, uniq, m, keep_o);
   k_nonzero<<<blocks_for(m), 256, 0, st>>>(c_new, m, keep_u);
   FK_TRY(cub_select_flagged(S, o_fp, keep_o, o2_fp, d_num, g_old));
   FK_TRY(cub_select_flagged(S, o_cnt, keep_o, o2_cnt, d_num + 1, g_old));
@@ -671,6 +735,7 @@ int apply_t(const fk_gqf_geom *g, const fk_gqf_tables *cur, const fk_gqf_tables 
   const bool plain_ins = !is_del && deltas == nullptr;
   const bool split = plain_ins && qr <= 40;
   uint64_t *fps = nullptr, *fps_s = nullptr, *del_s = nullptr;
+  int64_t *seg_heads = nullptr, *seg_ids = nullptr;
   uint32_t *idx = nullptr, *idx_s = nullptr;
   uint8_t *hi_s = nullptr;
   uint32_t *lo_s = nullptr;
@@ -716,11 +781,12 @@ int apply_t(const fk_gqf_geom *g, const fk_gqf_tables *cur, const fk_gqf_tables 
       FK_CU(cub_rle_counts_split(S, hi_s, lo_s, uniq, sums, d_num, n));
     }
   } else {
-    fps = S.get<uint64_t>(n);
     fps_s = S.get<uint64_t>(n);
     del_s = S.get<uint64_t>(n);
-    idx = S.get<uint32_t>(n);
     idx_s = S.get<uint32_t>(n);
+    if (S.err) return -(int)S.err;
+    fps = S.get<uint64_t>(n);
+    idx = S.get<uint32_t>(n);
     if (S.err) return -(int)S.err;
     k_hash_fps<<<blocks_for(n), 256, 0, st>>>(keys, keys_are_fps, g->seed, fmask, n, fps, idx);
     if (plain_ins) {
@@ -730,8 +796,16 @@ int apply_t(const fk_gqf_geom *g, const fk_gqf_tables *cur, const fk_gqf_tables 
       FK_CU(cub_sort_pairs(S, fps, fps_s, idx, idx_s, n, qr));
       const uint64_t dflt = is_del ? (1ull << 63) : 1ull;
       k_gather_u64<<<blocks_for(n), 256, 0, st>>>(deltas, idx_s, dflt, n, del_s);
-      // 4. unique fingerprints with saturating delta sums
-      FK_CU(cub_reduce_by_key(S, fps_s, uniq, del_s, sums, d_num, n));
+      // 4. unique fingerprints with saturating delta sums: segment ids by a
+      // scan of the segment ends (kept for the found flags), then one thread
+      // per segment
+      seg_heads = S.get<int64_t>(n);
+      seg_ids = S.get<int64_t>(n);
+      if (S.err) return -(int)S.err;
+      k_seg_heads<<<blocks_for(n), 256, 0, st>>>(fps_s, n, seg_heads);
+      FK_CU(cub_excl_sum_i64(S, seg_heads, seg_ids, n));
+      k_seg_reduce<<<blocks_for(n), 256, 0, st>>>(fps_s, del_s, seg_ids, n, uniq, sums);
+      k_seg_count<<<1, 1, 0, st>>>(seg_ids, n, d_num);
     }
   }
   int64_t m = 0;
@@ -749,31 +823,64 @@ int apply_t(const fk_gqf_geom *g, const fk_gqf_tables *cur, const fk_gqf_tables 
   if (is_del && !(flags & (kApplyDry | kApplyForceExact)) && n <= small_batch_limit(g))
     return apply_small_delete_t<S_t>(g, cur, fps_s, del_s, idx_s, n, order, found, res, st);
 
-  // 5-6. old counts through the (pure) count query, new absolute counts
+  // Regions the batch touches: a batch within a quarter of them is applied
+  // region-locally in place (8'); otherwise the whole table is decoded (8)
+  // and the old counts come from joining the two sorted lists.
+  bool exact = (flags & kApplyForceExact) != 0, load_possible = exact;
+  const bool try_local = !exact && region_place_enabled() && local_apply_enabled();
+  int64_t *creg = nullptr, Kreg = -1;
+  if (try_local) {
+    int lrc = local_regions(S, g, uniq, m, &creg, &Kreg);
+    if (lrc) return lrc;
+  }
+  const bool go_local = try_local && local_applicable(g, Kreg);
   uint64_t *c_old = S.get<uint64_t>(m), *c_new = S.get<uint64_t>(m);
   if (S.err) return -(int)S.err;
-  k_gqf_count<S_t><<<blocks_for(m), 256, 0, st>>>(T0, uniq, 1, 0, m, c_old);
+  // 8. (global path) decode the old table into sorted (fp, count) items
+  // (one thread per run)
+  int64_t g_old = 0;
+  uint64_t *o_fp = nullptr, *o_cnt = nullptr;
+  if (!go_local) {
+    RunDecode D;
+    int drc = decode_runs_count<S_t>(S, g, cur, T0, &D, st);
+    if (drc) return drc;
+    g_old = D.items;
+    o_fp = S.get<uint64_t>(g_old);
+    o_cnt = S.get<uint64_t>(g_old);
+    if (S.err) return -(int)S.err;
+    drc = decode_runs_write<S_t>(T0, D, o_fp, o_cnt, st);
+    if (drc) return drc;
+  }
+
+  // 5-6. old counts (the pure count query, or the join with the decoded
+  // items), new absolute counts
+  if (go_local)
+    k_gqf_count<S_t><<<blocks_for(m), 256, 0, st>>>(T0, uniq, 1, 0, m, c_old);
+  else
+    k_old_counts_join<<<blocks_for(join_threads(m)), 256, 0, st>>>(uniq, m, o_fp, o_cnt, g_old, c_old);
   k_new_counts<<<blocks_for(m), 256, 0, st>>>(c_old, sums, m, is_del ? 1 : 0, c_new);
 
-  // 7. delete found flags: sequential semantics via a segmented prefix sum
-  if (is_del && found && m == n) {
-    // no fingerprint repeats in the batch: a key is found iff its
-    // fingerprint was present
-    k_found_distinct<<<blocks_for(n), 256, 0, st>>>(c_old, idx_s, n, found);
-  } else if (is_del && found) {
-    // segment (unique fingerprint) of every sorted item: exclusive sum of
-    // segment heads; then one thread per segment walks its copies in the
-    // facade's order (bulk: each region descending, gqf.py:317-325)
-    int64_t *heads = S.get<int64_t>(n), *seg = S.get<int64_t>(n);
+  // 7. delete found flags: sequential semantics via a segmented prefix sum,
+  // computed in sorted order, then scattered to input order
+  if (is_del && found) {
+    uint8_t *found_s = S.get<uint8_t>(n);
     if (S.err) return -(int)S.err;
-    k_seg_heads<<<blocks_for(n), 256, 0, st>>>(fps_s, n, heads);
-    FK_CU(cub_excl_sum_i64(S, heads, seg, n));
-    k_found_walk<<<blocks_for(n), 256, 0, st>>>(fps_s, del_s, idx_s, seg, c_old, n, order == FK_ORDER_BULK ? 1 : 0,
-                                                found);
+    if (m == n) {
+      // no fingerprint repeats in the batch: a key is found iff its
+      // fingerprint was present
+      k_found_distinct<<<blocks_for(n), 256, 0, st>>>(c_old, n, found_s);
+    } else {
+      // one thread per segment walks its copies in the facade's order
+      // (bulk: each region descending, gqf.py:317-325)
+      k_found_walk<<<blocks_for(n), 256, 0, st>>>(fps_s, del_s, seg_ids, c_old, n, order == FK_ORDER_BULK ? 1 : 0,
+                                                  found_s);
+    }
+    constexpr int kScatterShift = 25;  // 32 MiB of found bytes per pass
+    for (int64_t p = 0; p <= ((n - 1) >> kScatterShift); p++)
+      k_found_scatter<<<blocks_for(n), 256, 0, st>>>(found_s, idx_s, n, kScatterShift, p, found);
   }
 
   // 8'. region-local apply in place (mid-size batches; apply_local_t)
-  bool exact = (flags & kApplyForceExact) != 0, load_possible = exact;
   bool region_done = false;
   unsigned long long region_shift = 0;
   MaxPlus *ends = nullptr;
@@ -781,10 +888,10 @@ int apply_t(const fk_gqf_geom *g, const fk_gqf_tables *cur, const fk_gqf_tables 
   int64_t G = 0;
   uint64_t *it_fp = nullptr, *it_cnt = nullptr;
   bool local_exact = false;
-  if (!exact && region_place_enabled() && local_apply_enabled()) {
+  if (go_local) {
     bool lp = false;
-    const int lr = apply_local_t<S_t>(S, g, cur, keys, keys_are_fps, fmask, n, uniq, c_new, m, is_del, order, flags,
-                                      res, &lp);
+    const int lr = apply_local_t<S_t>(S, g, cur, creg, Kreg, keys, keys_are_fps, fmask, n, uniq, c_new, m, is_del,
+                                      order, flags, res, &lp);
     if (lr <= 0) return lr;  // applied (or dry run answered), or an error
     if (lr == 2) {
       local_exact = exact = true;
@@ -792,25 +899,17 @@ int apply_t(const fk_gqf_geom *g, const fk_gqf_tables *cur, const fk_gqf_tables 
     }
   }
   if (!local_exact) {
-    // 8. decode the old table into sorted (fp, count) items
-    int64_t nqw = ((1LL << g->q) + 63) >> 6;
-    int64_t *gcount = S.get<int64_t>(nqw), *goff = S.get<int64_t>(nqw);
-    int *d_err = S.get<int>(4);
-    if (S.err) return -(int)S.err;
-    FK_CU(cudaMemsetAsync(d_err, 0, 4 * sizeof(int), st));
-    k_decode_words<S_t><<<blocks_for(nqw), 256, 0, st>>>(T0, nqw, 0, gcount, nullptr, nullptr, nullptr, d_err);
-    FK_CU(cub_excl_sum_i64(S, gcount, goff, nqw));
-    int64_t tail[2];
-    FK_CU(cudaMemcpyAsync(&tail[0], goff + nqw - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    FK_CU(cudaMemcpyAsync(&tail[1], gcount + nqw - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    int h_err = 0;
-    FK_CU(cudaMemcpyAsync(&h_err, d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
-    FK_CU(cudaStreamSynchronize(st));
-    if (h_err) return FK_E_INVARIANT;
-    int64_t g_old = tail[0] + tail[1];
-    uint64_t *o_fp = S.get<uint64_t>(g_old), *o_cnt = S.get<uint64_t>(g_old);
-    if (S.err) return -(int)S.err;
-    k_decode_words<S_t><<<blocks_for(nqw), 256, 0, st>>>(T0, nqw, 1, nullptr, goff, o_fp, o_cnt, d_err);
+    if (go_local) {  // the local path declined: decode the whole table after all
+      RunDecode D;
+      int drc = decode_runs_count<S_t>(S, g, cur, T0, &D, st);
+      if (drc) return drc;
+      g_old = D.items;
+      o_fp = S.get<uint64_t>(g_old);
+      o_cnt = S.get<uint64_t>(g_old);
+      if (S.err) return -(int)S.err;
+      drc = decode_runs_write<S_t>(T0, D, o_fp, o_cnt, st);
+      if (drc) return drc;
+    }
 
     // 9-10. drop old items the batch updates and zero counts, then merge the
     // two duplicate-free sorted lists
@@ -818,7 +917,7 @@ int apply_t(const fk_gqf_geom *g, const fk_gqf_tables *cur, const fk_gqf_tables 
     uint64_t *o2_fp = S.get<uint64_t>(g_old), *o2_cnt = S.get<uint64_t>(g_old);
     uint64_t *u2_fp = S.get<uint64_t>(m), *u2_cnt = S.get<uint64_t>(m);
     if (S.err) return -(int)S.err;
-    k_keep_old_runs<<<blocks_for((g_old + 31) / 32), 256, 0, st>>>(o_fp, g_old, uniq, m, keep_o);
+    k_keep_old_join<<<blocks_for(join_threads(g_old)), 256, 0, st>>>(o_fp, g_old, uniq, m, keep_o);
     k_nonzero<<<blocks_for(m), 256, 0, st>>>(c_new, m, keep_u);
     FK_CU(cub_select_flagged(S, o_fp, keep_o, o2_fp, d_num, g_old));
     FK_CU(cub_select_flagged(S, o_cnt, keep_o, o2_cnt, d_num + 1, g_old));

@@ -251,16 +251,95 @@ __global__ void k_u8_bounds(const uint8_t *__restrict__ hs, int64_t n, int nseg,
 }
 
 // ---- cluster statistics (Gqf.cluster_stats, gqf.py:416-428) ----------------
+// Position of the k-th (0-based) set bit of x (k < popc(x)), branch-free.
+__device__ __forceinline__ int select64(uint64_t x, int k) {
+  int pos = 0, c;
+  c = __popc((uint32_t)x);
+  if (k >= c) { k -= c; x >>= 32; pos += 32; }
+  c = __popc((uint32_t)x & 0xffffu);
+  if (k >= c) { k -= c; x >>= 16; pos += 16; }
+  c = __popc((uint32_t)x & 0xffu);
+  if (k >= c) { k -= c; x >>= 8; pos += 8; }
+  c = __popc((uint32_t)x & 0xfu);
+  if (k >= c) { k -= c; x >>= 4; pos += 4; }
+  c = __popc((uint32_t)x & 0x3u);
+  if (k >= c) { k -= c; x >>= 2; pos += 2; }
+  c = (int)(x & 1u);
+  if (k >= c) pos += 1;
+  return pos;
+}
+
 // Positions of the set bits of a bit vector, word w's at off[w] onward.
+// One warp per 32 consecutive words: a warp prefix sum of their popcounts,
+// then rounds of 32 consecutive output ranks, each lane locating its rank's
+// word by a 5-step search over the lanes' prefixes -- the stores are
+// coalesced (one thread per word would scatter them 30 words apart).
 __global__ void k_bit_positions(const uint64_t *__restrict__ bv, int64_t nw, const int64_t *__restrict__ off,
                                 int64_t *__restrict__ pos) {
-  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += (int64_t)gridDim.x * blockDim.x) {
-    uint64_t x = bv[w];
-    int64_t o = off[w];
-    while (x) {
-      pos[o++] = (w << 6) + __ffsll((long long)x) - 1;
-      x &= x - 1;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (nw + 31) >> 5;
+  for (int64_t wp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; wp < nwarps;
+       wp += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t w0 = wp << 5, w = w0 + lane;
+    const uint64_t x = w < nw ? bv[w] : 0ull;
+    int incl = __popcll(x);
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += v;
     }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    if (total == 0) continue;
+    const int64_t base = off[w0];
+    for (int rb = 0; rb < total; rb += 32) {
+      const int r = rb + lane;
+      // t = the first lane whose inclusive prefix exceeds r
+      int t = 0;
+#pragma unroll
+      for (int step = 16; step >= 1; step >>= 1) {
+        const int v = __shfl_sync(0xffffffffu, incl, t + step - 1);
+        if (v <= r) t += step;
+      }
+      const int ex = __shfl_sync(0xffffffffu, incl, t) - __popcll(__shfl_sync(0xffffffffu, x, t));
+      const uint64_t xt = __shfl_sync(0xffffffffu, x, t);
+      if (r < total) pos[base + r] = ((w0 + t) << 6) + select64(xt, r - ex);
+    }
+  }
+}
+
+// Decode by runs: run k (occupied quotient Q[k], ending at the k-th runend
+// bit E[k], starting at max(Q[k], E[k-1] + 1)) is parsed by its own thread;
+// mode 0 counts its groups, mode 1 writes them at off[k].
+template <typename S>
+__global__ void k_decode_runs(GqfDev T, const int64_t *__restrict__ Q, const int64_t *__restrict__ E, int64_t K,
+                              int mode, int64_t *__restrict__ gcount, const int64_t *__restrict__ off,
+                              uint64_t *__restrict__ it_fp, uint64_t *__restrict__ it_cnt, int *__restrict__ err) {
+  const S *slots = reinterpret_cast<const S *>(T.slots);
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < K; k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t quot = Q[k], end = E[k];
+    const int64_t prev = k ? E[k - 1] : -1;
+    const int64_t st = quot > prev + 1 ? quot : prev + 1;
+    int64_t o = mode ? off[k] : 0, g = 0;
+    if (end < st) {
+      *err = 1;
+      continue;
+    }
+    for (int64_t p = st; p <= end;) {
+      uint64_t h, cnt;
+      int64_t nx;
+      if (!parse_group_dev<S>(slots, p, end, T.r, &h, &cnt, &nx)) {
+        *err = 1;
+        break;
+      }
+      if (mode) {
+        it_fp[o] = ((uint64_t)quot << T.r) | h;
+        it_cnt[o] = cnt;
+        o++;
+      }
+      g++;
+      p = nx;
+    }
+    if (!mode) gcount[k] = g;
   }
 }
 
@@ -668,13 +747,6 @@ __global__ void k_gather_u64(const uint64_t *__restrict__ src, const uint32_t *_
     dst[i] = src ? src[idx[i]] : dflt;
 }
 
-struct SatAdd {
-  __host__ __device__ __forceinline__ uint64_t operator()(uint64_t a, uint64_t b) const {
-    uint64_t s = a + b;
-    return s < a ? ~0ull : s;
-  }
-};
-
 // new absolute count per unique fp: insert c+sum, delete c-min(c,sum)
 __global__ void k_new_counts(const uint64_t *__restrict__ c_old, const uint64_t *__restrict__ sums, int64_t m,
                              int is_delete, uint64_t *__restrict__ c_new) {
@@ -685,15 +757,23 @@ __global__ void k_new_counts(const uint64_t *__restrict__ c_old, const uint64_t 
   }
 }
 
-// found flags for deletes: element j (in processing order within its fp
-// segment) finds the key iff the deltas processed before it leave a count.
-// found flags of a delete batch without repeated fingerprints: sorted item j
-// is input idx_s[j], its exclusive prefix is 0, so (as in k_found_flags)
-// found iff the fingerprint was present
-__global__ void k_found_distinct(const uint64_t *__restrict__ c_old, const uint32_t *__restrict__ idx_s, int64_t n,
-                                 uint8_t *__restrict__ found) {
+// found flags of a duplicate-free delete batch, in sorted order: a key is
+// found iff its fingerprint was present
+__global__ void k_found_distinct(const uint64_t *__restrict__ c_old, int64_t n, uint8_t *__restrict__ found_s) {
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
-    found[idx_s[j]] = c_old[j] > 0 ? 1 : 0;
+    found_s[j] = c_old[j] > 0 ? 1 : 0;
+}
+
+// found_s (sorted order) -> found (input order) in passes over input-index
+// ranges of 2^shift keys: the pass's byte stores land in a range that stays
+// in L2 until its sectors are complete (one random byte store per key
+// across the whole array costs a DRAM sector write each)
+__global__ void k_found_scatter(const uint8_t *__restrict__ found_s, const uint32_t *__restrict__ idx_s, int64_t n,
+                                int shift, int64_t pass, uint8_t *__restrict__ found) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t i = idx_s[j];
+    if ((int64_t)(i >> shift) == pass) found[i] = found_s[j];
+  }
 }
 
 // 1 where a sorted fingerprint starts a new segment, after the first item
@@ -703,15 +783,35 @@ __global__ void k_seg_heads(const uint64_t *__restrict__ fps_s, int64_t n, int64
     heads[j] = (j + 1 < n && fps_s[j + 1] != fps_s[j]) ? 1 : 0;
 }
 
+// Unique fingerprints and saturating delta sums of the sorted batch, one
+// thread per fingerprint segment (seg = exclusive sum of k_seg_heads).
+__global__ void k_seg_reduce(const uint64_t *__restrict__ fps_s, const uint64_t *__restrict__ del_s,
+                             const int64_t *__restrict__ seg, int64_t n, uint64_t *__restrict__ uniq,
+                             uint64_t *__restrict__ sums) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t f = fps_s[j];
+    if (j > 0 && fps_s[j - 1] == f) continue;  // not a segment head
+    uint64_t acc = del_s[j];
+    for (int64_t e = j + 1; e < n && fps_s[e] == f; e++) {
+      const uint64_t sum = acc + del_s[e];
+      acc = sum < acc ? ~0ull : sum;
+    }
+    const int64_t s = seg[j];
+    uniq[s] = f;
+    sums[s] = acc;
+  }
+}
+
 // found flags of a delete batch with repeated fingerprints, one thread per
 // fingerprint segment of the sorted batch (segments are short): the copies
 // are processed in the facade's order -- input order for point deletes,
 // last-input-first for bulk deletes (gqf.py:317-325) -- and copy k finds the
 // key iff the deltas of the copies before it leave part of the old count.
+// Written in sorted order (k_found_scatter brings them to input order).
 __global__ void k_found_walk(const uint64_t *__restrict__ fps_s, const uint64_t *__restrict__ del_s,
-                             const uint32_t *__restrict__ idx_s, const int64_t *__restrict__ seg,
+                             const int64_t *__restrict__ seg,
                              const uint64_t *__restrict__ c_old, int64_t n, int bulk_order,
-                             uint8_t *__restrict__ found) {
+                             uint8_t *__restrict__ found_s) {
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
     const uint64_t f = fps_s[j];
     if (j > 0 && fps_s[j - 1] == f) continue;  // not a segment head
@@ -721,34 +821,97 @@ __global__ void k_found_walk(const uint64_t *__restrict__ fps_s, const uint64_t 
     uint64_t pre = 0;
     for (int64_t t = 0; t < e - j; t++) {
       const int64_t k = bulk_order ? e - 1 - t : j + t;
-      found[idx_s[k]] = pre < c ? 1 : 0;
+      found_s[k] = pre < c ? 1 : 0;
       const uint64_t d = del_s[k], sum = pre + d;
       pre = sum < pre ? ~0ull : sum;  // saturating, as the reference's counts
     }
   }
 }
 
-// Old items the batch updates are dropped before the merge: both lists are
-// sorted, so each thread binary-searches its first item of a run of 32 and
-// walks the batch's fingerprints forward alongside the rest.
-__global__ void k_keep_old_runs(const uint64_t *__restrict__ o_fp, int64_t g_old, const uint64_t *__restrict__ uniq,
-                                int64_t m, uint8_t *__restrict__ keep) {
-  constexpr int RUN = 32;
-  const int64_t runs = (g_old + RUN - 1) / RUN;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < runs; t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t a = t * RUN, e = a + RUN < g_old ? a + RUN : g_old;
-    int64_t lo = 0, hi = m;
-    const uint64_t f0 = o_fp[a];
-    while (lo < hi) {
-      const int64_t mid = (lo + hi) >> 1;
-      if (uniq[mid] < f0) lo = mid + 1; else hi = mid;
-    }
-    for (int64_t i = a; i < e; i++) {
-      const uint64_t f = o_fp[i];
-      while (lo < m && uniq[lo] < f) lo++;
-      keep[i] = (lo < m && uniq[lo] == f) ? 0 : 1;
+// First index >= lo with a[index] >= f (a sorted, a[lo - 1] < f): galloping
+// steps then a binary search, O(log gap).
+__device__ __forceinline__ int64_t gallop_lower(const uint64_t *__restrict__ a, int64_t n, int64_t lo, uint64_t f) {
+  int64_t step = 1, hi = lo;
+  while (hi < n && a[hi] < f) {
+    lo = hi + 1;
+    hi += step;
+    step <<= 1;
+  }
+  if (hi > n) hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (a[mid] < f) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// lower_bound of f in a[0..n) by one warp (f warp-uniform): 32-way probes,
+// ~log32(n) dependent loads instead of log2(n).
+__device__ __forceinline__ int64_t warp_lower_bound(const uint64_t *__restrict__ a, int64_t n, uint64_t f) {
+  const int lane = threadIdx.x & 31;
+  int64_t lo = 0, hi = n;  // answer in [lo, hi]
+  while (hi - lo > 32) {
+    const int64_t p = lo + (hi - lo) * (lane + 1) / 33;
+    const unsigned b = __ballot_sync(0xffffffffu, a[p] < f);
+    const int k = __popc(b);
+    const int64_t nlo = k ? __shfl_sync(0xffffffffu, p, k - 1) + 1 : lo;
+    const int64_t nhi = k < 32 ? __shfl_sync(0xffffffffu, p, k < 32 ? k : 31) : hi;
+    lo = nlo;
+    hi = nhi;
+  }
+  const unsigned b = __ballot_sync(0xffffffffu, lo + lane < hi && a[lo + lane] < f);
+  return lo + __popc(b);
+}
+
+// Join of sorted `probe` (np items) against sorted `a` (na items), one warp
+// per chunk of kJoinChunk probes: a warp lower_bound for the chunk's first
+// probe, then rounds of 32 consecutive probes against the 32 items of `a`
+// after the previous round's last position (coalesced probe reads, window
+// reads and result writes); a probe past the window gallops on.
+constexpr int kJoinChunk = 1024;
+template <typename F>
+__device__ __forceinline__ void warp_join(const uint64_t *__restrict__ probe, int64_t np,
+                                          const uint64_t *__restrict__ a, int64_t na, F &&emit) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nch = (np + kJoinChunk - 1) / kJoinChunk;
+  for (int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < nch;
+       c += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t s = c * kJoinChunk, e = s + kJoinChunk < np ? s + kJoinChunk : np;
+    int64_t lo = warp_lower_bound(a, na, probe[s]);
+    for (int64_t b = s; b < e; b += 32) {
+      const int64_t j = b + lane;
+      const bool v = j < e;
+      const uint64_t f = v ? probe[j] : ~0ull;
+      // the next 32 items of a, one coalesced load; each lane's position in
+      // that window by a 5-step search over the lanes, galloping on past it
+      const uint64_t wa = lo + lane < na ? a[lo + lane] : ~0ull;
+      int c = 0;
+#pragma unroll
+      for (int step = 16; step >= 1; step >>= 1) {
+        const uint64_t at = __shfl_sync(0xffffffffu, wa, c + step - 1);
+        if (at < f) c += step;
+      }
+      if (__shfl_sync(0xffffffffu, wa, 31) < f && c == 31) c = 32;
+      int64_t p = lo + c;
+      if (v && c == 32) p = gallop_lower(a, na, p, f);
+      if (v) emit(j, p, p < na && a[p] == f);
+      const int last = (e - b) < 32 ? (int)(e - b) - 1 : 31;
+      lo = __shfl_sync(0xffffffffu, p, last);
     }
   }
+}
+
+// Old items the batch updates are dropped before the merge.
+__global__ void k_keep_old_join(const uint64_t *__restrict__ o_fp, int64_t g_old, const uint64_t *__restrict__ uniq,
+                                int64_t m, uint8_t *__restrict__ keep) {
+  warp_join(o_fp, g_old, uniq, m, [&](int64_t i, int64_t, bool hit) { keep[i] = hit ? 0 : 1; });
+}
+
+// The old count of every batch fingerprint from the decoded table (replaces
+// the count query when the whole table is decoded anyway).
+__global__ void k_old_counts_join(const uint64_t *__restrict__ uniq, int64_t m, const uint64_t *__restrict__ o_fp,
+                                  const uint64_t *__restrict__ o_cnt, int64_t g_old, uint64_t *__restrict__ c_old) {
+  warp_join(uniq, m, o_fp, g_old, [&](int64_t j, int64_t p, bool hit) { c_old[j] = hit ? o_cnt[p] : 0; });
 }
 
 // Decode pass over occupied quotient words: mode 0 counts groups per word,
@@ -788,17 +951,7 @@ __device__ __forceinline__ int64_t decode_word(const GqfDev &T, int64_t w, int m
   return g;
 }
 
-template <typename S>
-__global__ void k_decode_words(GqfDev T, int64_t nqw, int mode, int64_t *__restrict__ gcount,
-                               const int64_t *__restrict__ off, uint64_t *__restrict__ it_fp,
-                               uint64_t *__restrict__ it_cnt, int *__restrict__ err) {
-  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nqw; w += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t g = decode_word<S>(T, w, mode, mode ? off[w] : 0, it_fp, it_cnt, err);
-    if (!mode) gcount[w] = g;
-  }
-}
-
-// The same over the quotient words of a list of regions (creg[0..K)):
+// decode_word over the quotient words of a list of regions (creg[0..K)):
 // flat index f -> region creg[f / 128], word f % 128 of it.
 template <typename S>
 __global__ void k_decode_region_words(GqfDev T, const int64_t *__restrict__ creg, int64_t K, int64_t nqw, int mode,
