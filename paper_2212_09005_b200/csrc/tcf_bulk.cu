@@ -847,6 +847,254 @@ __global__ void __launch_bounds__(kJT, 3) k_btcf_route_jacobi(RouteJ R) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// The same fixpoint with the counts kept per block (default router).
+// L(X, k) only counts earlier decisions for X among the items that list X:
+// block X's a-segment (items with a = X, by index) and b-segment (b = X != a).
+// One warp owns block X and, per sweep, (1) recomputes the decision of each
+// item in its two segments from the loads the previous sweep left for that
+// item -- d_k = rule(LA[k], LB[k]) -- and ballots the flags [d_j == X], then
+// (2) writes every segment item's new load on X: fill[X] + the flagged items
+// of both segments with a smaller index (own-segment prefix + the other
+// segment's prefix at the item's static rank there).  d^t = rule(L(d^{t-1}))
+// is the Jacobi iterate of k_btcf_route_jacobi with no global prefix sums and
+// one grid barrier per sweep (loads double-buffered by sweep parity); the
+// a-owner of an item keeps its decision and flags changes.
+#ifndef FK_RB_MINB
+#define FK_RB_MINB 4
+#endif
+constexpr int kRBT = 256, kRBWarps = kRBT / 32, kRBMaxWords = 32;  // segments up to 1024 items
+struct RouteBJ {
+  const uint4 *st1;           // [m] a-order position: item, b, rank in b-segment a, -
+  const uint4 *st2;           // [m] b-order position: item, a, rank in a-segment b, -
+  const uint32_t *s1, *e1, *s2, *e2;  // [nb] segment bounds in the two orders
+  const uint32_t *fill;       // [nb]
+  const uint32_t *a, *b;      // [m]
+  uint32_t *LA[2], *LB[2];    // [m] loads of each item on its a / b block, by sweep parity
+  int32_t *d;                 // [m] decisions (out; pre-set to a non-decision)
+  unsigned *ctl;              // [3] sweeps, [4] converged (2 = segment too long), [5] too-long flag
+  unsigned *chg;              // [2][gridDim]
+  int64_t m;
+  int64_t nb;
+  uint32_t B;
+};
+
+__device__ __forceinline__ uint32_t seg_prefix(const uint32_t *w, const uint32_t *pre, uint32_t q) {
+  return pre[q >> 5] + (uint32_t)__popc(w[q >> 5] & ((1u << (q & 31)) - 1u));
+}
+
+// One block's static data: segment bounds, fill, and the first chunk of each
+// segment (lane i: entry i) -- a warp keeps this in registers across the
+// sweeps for its first kRBHold blocks.
+struct RBlk {
+  uint32_t x, s1x, nA, s2x, nB, fx;
+  uint4 eA0, eB0;
+};
+
+__device__ __forceinline__ RBlk rb_load(const RouteBJ &R, int64_t X, int lane) {
+  RBlk h;
+  const uint4 z4 = make_uint4(0, 0, 0, 0);
+  h.x = (uint32_t)X;
+  if (X < R.nb) {
+    h.s1x = R.s1[X];
+    h.nA = R.e1[X] - h.s1x;
+    h.s2x = R.s2[X];
+    h.nB = R.e2[X] - h.s2x;
+    h.fx = R.fill[X];
+  } else {
+    h.s1x = h.nA = h.s2x = h.nB = h.fx = 0;
+  }
+  h.eA0 = lane < (int)h.nA ? R.st1[h.s1x + lane] : z4;
+  h.eB0 = lane < (int)h.nB ? R.st2[h.s2x + lane] : z4;
+  return h;
+}
+
+// The previous loads of the first chunks' items (one dependent trip).
+struct RBLoads {
+  uint32_t la0, lb0, la1, lb1;
+  int32_t dold;
+};
+
+__device__ __forceinline__ RBLoads rb_fetch(const RouteBJ &R, const RBlk &h, const uint32_t *LAp, const uint32_t *LBp,
+                                            int lane) {
+  RBLoads v = {0, 0, 0, 0, 0};
+  if (lane < (int)h.nA) {
+    v.la0 = __ldcg(&LAp[h.eA0.x]);
+    v.lb0 = __ldcg(&LBp[h.eA0.x]);
+    v.dold = R.d[h.eA0.x];
+  }
+  if (lane < (int)h.nB && h.eB0.y != h.x) {
+    v.la1 = __ldcg(&LAp[h.eB0.x]);
+    v.lb1 = __ldcg(&LBp[h.eB0.x]);
+  }
+  return v;
+}
+
+// One sweep's work on one block (see k_btcf_route_blocks).
+__device__ __forceinline__ void rb_sweep(const RouteBJ &R, const RBlk &h, const RBLoads &v, const uint32_t *LAp,
+                                         const uint32_t *LBp, uint32_t *LAn, uint32_t *LBn, uint32_t *wA,
+                                         uint32_t *wB, uint32_t *pA, uint32_t *pB, int lane, unsigned &changed) {
+  const uint32_t x = h.x, nA = h.nA, nB = h.nB, s1x = h.s1x, s2x = h.s2x;
+  const uint32_t nwA = (nA + 31) >> 5, nwB = (nB + 31) >> 5;
+  const bool vA = lane < (int)nA, uB = lane < (int)nB && h.eB0.y != x;  // a == b counts in the a-segment only
+  // (1) decisions and flags
+  {
+    bool fl = false;
+    if (vA) {
+      const int32_t dk = route_rule(v.la0, v.lb0, x, h.eA0.y, R.B);
+      fl = dk == (int32_t)x;
+      if (dk != v.dold) {
+        R.d[h.eA0.x] = dk;
+        changed = 1;
+      }
+    }
+    const unsigned w = __ballot_sync(0xFFFFFFFFu, fl);
+    const unsigned wb = __ballot_sync(0xFFFFFFFFu, uB && route_rule(v.la1, v.lb1, h.eB0.y, x, R.B) == (int32_t)x);
+    if (lane == 0) {
+      wA[0] = w;
+      wB[0] = wb;
+    }
+  }
+  for (uint32_t c = 1; c < nwA; c++) {
+    const uint32_t i = c * 32 + lane;
+    bool fl = false;
+    if (i < nA) {
+      const uint4 e = R.st1[s1x + i];
+      const int32_t dk = route_rule(__ldcg(&LAp[e.x]), __ldcg(&LBp[e.x]), x, e.y, R.B);
+      fl = dk == (int32_t)x;
+      if (dk != R.d[e.x]) {
+        R.d[e.x] = dk;
+        changed = 1;
+      }
+    }
+    const unsigned w = __ballot_sync(0xFFFFFFFFu, fl);
+    if (lane == 0) wA[c] = w;
+  }
+  for (uint32_t c = 1; c < nwB; c++) {
+    const uint32_t i = c * 32 + lane;
+    bool fl = false;
+    if (i < nB) {
+      const uint4 e = R.st2[s2x + i];
+      if (e.y != x) fl = route_rule(__ldcg(&LAp[e.x]), __ldcg(&LBp[e.x]), e.y, x, R.B) == (int32_t)x;
+    }
+    const unsigned w = __ballot_sync(0xFFFFFFFFu, fl);
+    if (lane == 0) wB[c] = w;
+  }
+  __syncwarp();
+  // exclusive prefix popcounts of the flag words (<= 32 words per segment)
+  {
+    const uint32_t ca = lane < (int)nwA ? (uint32_t)__popc(wA[lane]) : 0u;
+    const uint32_t cb = lane < (int)nwB ? (uint32_t)__popc(wB[lane]) : 0u;
+    uint32_t ia = ca, ibv = cb;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t ta = __shfl_up_sync(0xFFFFFFFFu, ia, o), tb = __shfl_up_sync(0xFFFFFFFFu, ibv, o);
+      if (lane >= o) {
+        ia += ta;
+        ibv += tb;
+      }
+    }
+    pA[lane] = ia - ca;
+    pB[lane] = ibv - cb;
+    if (lane == 31) {
+      pA[32] = ia;
+      pB[32] = ibv;
+    }
+    if (lane == 0) {
+      if ((nA & 31) == 0) wA[nwA] = 0;  // rank nA = the whole segment
+      if ((nB & 31) == 0) wB[nwB] = 0;
+    }
+  }
+  __syncwarp();
+  // (2) the items' new loads on X (first chunks from registers)
+  if (vA) {
+    const uint32_t L = h.fx + seg_prefix(wA, pA, lane) + seg_prefix(wB, pB, h.eA0.z);
+    LAn[h.eA0.x] = L;
+    if (h.eA0.y == x) LBn[h.eA0.x] = L;
+  }
+  if (uB) LBn[h.eB0.x] = h.fx + seg_prefix(wB, pB, lane) + seg_prefix(wA, pA, h.eB0.z);
+  for (uint32_t c = 1; c < nwA; c++) {
+    const uint32_t i = c * 32 + lane;
+    if (i < nA) {
+      const uint4 e = R.st1[s1x + i];
+      const uint32_t L = h.fx + seg_prefix(wA, pA, i) + seg_prefix(wB, pB, e.z);
+      LAn[e.x] = L;
+      if (e.y == x) LBn[e.x] = L;
+    }
+  }
+  for (uint32_t c = 1; c < nwB; c++) {
+    const uint32_t i = c * 32 + lane;
+    if (i < nB) {
+      const uint4 e = R.st2[s2x + i];
+      if (e.y != x) LBn[e.x] = h.fx + seg_prefix(wB, pB, i) + seg_prefix(wA, pA, e.z);
+    }
+  }
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(kRBT, FK_RB_MINB) k_btcf_route_blocks(RouteBJ R) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ uint32_t sw[kRBWarps][4][kRBMaxWords + 1];  // wA, wB, pA, pB
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  uint32_t *wA = sw[wib][0], *wB = sw[wib][1], *pA = sw[wib][2], *pB = sw[wib][3];
+  // loads before sweep 0 (no earlier decisions): the committed fills
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < R.m; k += (int64_t)gridDim.x * blockDim.x) {
+    R.LA[1][k] = R.fill[R.a[k]];
+    R.LB[1][k] = R.fill[R.b[k]];
+  }
+  for (int64_t X = gw; X < R.nb; X += nwarps)
+    if (lane == 0 && (R.e1[X] - R.s1[X] > 32u * kRBMaxWords || R.e2[X] - R.s2[X] > 32u * kRBMaxWords))
+      atomicOr(&R.ctl[5], 1u);
+  // the warp's first two blocks stay in registers across the sweeps
+  const RBlk h0 = rb_load(R, gw, lane), h1 = rb_load(R, gw + nwarps, lane);
+  grid.sync();
+  if (__ldcg(&R.ctl[5])) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) R.ctl[4] = 2;
+    return;
+  }
+  for (unsigned sweep = 0;; sweep++) {
+    const int cur = sweep & 1, prv = cur ^ 1;
+    const uint32_t *LAp = R.LA[prv], *LBp = R.LB[prv];
+    uint32_t *LAn = R.LA[cur], *LBn = R.LB[cur];
+    unsigned changed = 0;
+    // both held blocks' loads go out together: one dependent trip per sweep
+    const RBLoads v0 = rb_fetch(R, h0, LAp, LBp, lane), v1 = rb_fetch(R, h1, LAp, LBp, lane);
+    if (h0.nA | h0.nB) rb_sweep(R, h0, v0, LAp, LBp, LAn, LBn, wA, wB, pA, pB, lane, changed);
+    if (h1.nA | h1.nB) rb_sweep(R, h1, v1, LAp, LBp, LAn, LBn, wA, wB, pA, pB, lane, changed);
+    for (int64_t X = gw + 2 * nwarps; X < R.nb; X += nwarps) {
+      const RBlk h = rb_load(R, X, lane);
+      if (h.nA | h.nB) rb_sweep(R, h, rb_fetch(R, h, LAp, LBp, lane), LAp, LBp, LAn, LBn, wA, wB, pA, pB, lane, changed);
+    }
+    const int any = __syncthreads_or(changed != 0);
+    if (threadIdx.x == 0) R.chg[(size_t)cur * gridDim.x + blockIdx.x] = (unsigned)any;
+    grid.sync();
+    unsigned mine = 0;
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) mine |= __ldcg(&R.chg[(size_t)cur * gridDim.x + i]);
+    const unsigned cc = (unsigned)__syncthreads_or(mine != 0);
+    if (cc == 0 || sweep + 1 >= (unsigned)kJacobiMax) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        R.ctl[3] = sweep + 1;
+        R.ctl[4] = cc == 0 ? 1u : 0u;
+      }
+      return;
+    }
+  }
+}
+
+// static per-position records of k_btcf_route_blocks
+__global__ void k_route_blk_static(const uint32_t *__restrict__ a, const uint32_t *__restrict__ b,
+                                   const uint32_t *__restrict__ perm1, const uint32_t *__restrict__ perm2,
+                                   const uint32_t *__restrict__ qA, const uint32_t *__restrict__ qB,
+                                   const uint32_t *__restrict__ s1, const uint32_t *__restrict__ s2, int64_t m,
+                                   uint4 *__restrict__ st1, uint4 *__restrict__ st2) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < m; p += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t k1 = perm1[p], k2 = perm2[p];
+    st1[p] = make_uint4(k1, b[k1], qA[k1] - s2[a[k1]], 0);
+    st2[p] = make_uint4(k2, a[k2], qB[k2] - s1[b[k2]], 0);
+  }
+}
+
 // the static per-item gather indices of the sweeps (RouteItem)
 __global__ void k_route_items(const uint32_t *__restrict__ a, const uint32_t *__restrict__ b,
                               const uint32_t *__restrict__ fill, const uint32_t *__restrict__ pos1,
@@ -1336,13 +1584,46 @@ int route_items(Scratch &S, const uint32_t *a, const uint32_t *b, int64_t m, con
     k_seg_rank<<<grid_for(m), 256, 0, st>>>(a, perm2, s2, e2, m, qA);
     k_seg_rank<<<grid_for(m), 256, 0, st>>>(b, perm1, s1, e1, m, qB);
     FK_CHECK_LAUNCH();
+    const bool stats = getenv("FK_ROUTE_STATS") != nullptr;
+    if (!(force && !strcmp(force, "jacobi"))) {
+      // per-block fixpoint (k_btcf_route_blocks); segments over 1024 items
+      // take the global-prefix kernel below
+      uint4 *st1 = S.get<uint4>(m), *st2 = S.get<uint4>(m);
+      uint32_t *L0 = S.get<uint32_t>(4 * m);
+      unsigned *chg2 = S.get<unsigned>(2 * 4096);
+      FK_P(st1); FK_P(st2); FK_P(L0); FK_P(chg2);
+      k_route_blk_static<<<grid_for(m), 256, 0, st>>>(a, b, perm1, perm2, qA, qB, s1, s2, m, st1, st2);
+      FK_CHECK_LAUNCH();
+      FK_S(cudaMemsetAsync(dest, 0xFE, m * 4, st));  // no decision yet
+      RouteBJ RB{st1, st2, s1, e1, s2, e2, fill, a, b, {L0, L0 + m}, {L0 + 2 * m, L0 + 3 * m}, dest, ctl, chg2,
+                 m, (int64_t)nb, B};
+      int grid = coop_grid((const void *)k_btcf_route_blocks, kRBT);
+      if (!grid) return FK_E_ARG;
+      if (const char *cps = getenv("FK_RB_CTAS_PER_SM")) {  // measurement knob
+        const int g2 = atoi(cps) * num_sms();
+        if (g2 > 0 && g2 < grid) grid = g2;
+      }
+      const int64_t want = ((int64_t)nb + kRBWarps - 1) / kRBWarps;
+      if (want < grid) grid = (int)(want < 1 ? 1 : want);
+      if (grid > 4096) grid = 4096;
+      void *args[] = {(void *)&RB};
+      FK_S(cudaLaunchCooperativeKernel((const void *)k_btcf_route_blocks, dim3(grid), dim3(kRBT), args, 0, st));
+      unsigned h[2] = {0, 0};
+      FK_S(cudaMemcpyAsync(h, ctl + 3, 8, cudaMemcpyDeviceToHost, st));
+      FK_S(cudaStreamSynchronize(st));
+      if (stats) fprintf(stderr, "fk route (blocks): m=%lld sweeps=%u converged=%u grid=%d\n", (long long)m, h[0], h[1],
+                         grid);
+      if (h[1] == 1) return 0;
+      if (h[1] == 0) goto sequential;
+      FK_S(cudaMemsetAsync(ctl, 0, 32, st));  // 2: a segment is too long
+    }
+    {
     RouteItem *items = S.get<RouteItem>(m);
     uint32_t *a_of1 = S.get<uint32_t>(m), *b_of2 = S.get<uint32_t>(m);
     FK_P(items); FK_P(a_of1); FK_P(b_of2);
     k_route_items<<<grid_for(m), 256, 0, st>>>(a, b, fill, pos1, pos2, qA, qB, s1, s2, m, items);
     k_route_orders<<<grid_for(m), 256, 0, st>>>(a, b, perm1, perm2, m, a_of1, b_of2);
     FK_CHECK_LAUNCH();
-    const bool stats = getenv("FK_ROUTE_STATS") != nullptr;
     unsigned long long *clk = stats ? S.get<unsigned long long>(1 + 4 * 64) : nullptr;
     if (stats) FK_S(cudaMemsetAsync(clk, 0, 8 * (1 + 4 * 64), st));
     RouteJ R{items, perm1, perm2, a_of1, b_of2, pos1, pos2, dest, P1, P2, ts, tss, ctl, chg, clk, m, T, B};
@@ -1372,7 +1653,9 @@ int route_items(Scratch &S, const uint32_t *a, const uint32_t *b, int64_t m, con
     }
     if (h[1]) return 0;
     // not converged: fall through to the sequential walk
+    }
   }
+sequential:
   uint32_t *load = S.get<uint32_t>(nb);
   FK_P(load);
   size_t sm = (size_t)nb * 4;

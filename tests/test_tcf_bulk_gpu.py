@@ -195,10 +195,11 @@ def test_device_validate_agrees_with_host_checks():
     corrupt(lambda b, fl: fl.__setitem__(blk, fl[blk] - 1) or b.__setitem__(base + int(fl[blk]), 0))  # count mismatch
 
 
-@pytest.mark.parametrize("mode", ["jacobi", "seq", "prefix"])
+@pytest.mark.parametrize("mode", ["blocks", "jacobi", "seq", "prefix"])
 def test_route_modes_bit_exact(oracle, monkeypatch, mode):
-    """The three routers (fixpoint sweeps -- the default --, the one-warp walk
-    and the block-parallel prefix walk) give the reference's sequential
+    """The four routers (per-block fixpoint sweeps -- the default --, the
+    global-prefix fixpoint, the one-warp walk and the block-parallel prefix
+    walk) give the reference's sequential
     decisions (ck:408-444): configs[0] at 0.9 load, then an overfilled small
     table where both blocks of some leftovers are full (dest = -1, backing)."""
     monkeypatch.setenv("FK_ROUTE", mode)
@@ -211,6 +212,19 @@ def test_route_modes_bit_exact(oracle, monkeypatch, mode):
         keys = counter_keys(50 + s, n)
         assert np.array_equal(f.insert_batch(keys), o.insert_batch(keys)), s
         _same(f, o)
+
+
+def test_route_long_segments_fall_back(oracle, monkeypatch, capfd):
+    """More than 1024 leftovers on one block: the per-block router hands the
+    batch to the global-prefix fixpoint, same decisions as the reference's
+    walk (ck:408-444)."""
+    monkeypatch.setenv("FK_ROUTE_STATS", "1")
+    f, o = _pair(oracle, num_blocks=8, backing_fraction=0.5)
+    keys = counter_keys(61, 20_000)
+    assert np.array_equal(f.insert_batch(keys), o.insert_batch(keys))
+    _same(f, o)
+    err = capfd.readouterr().err
+    assert "fk route (blocks)" in err and "converged=2" in err, err[-500:]
 
 
 def test_items_selected_on_device():
