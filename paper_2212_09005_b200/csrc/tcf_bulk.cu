@@ -1547,30 +1547,22 @@ int route_items(Scratch &S, const uint32_t *a, const uint32_t *b, int64_t m, con
   const bool want_prefix = force && !strcmp(force, "prefix");
   if (!want_seq && !want_prefix) {
     const int kb = bits_for(nb - 1) ? bits_for(nb - 1) : 1;
-    uint32_t *perm1 = S.get<uint32_t>(m), *perm2 = S.get<uint32_t>(m), *pos1 = S.get<uint32_t>(m),
-             *pos2 = S.get<uint32_t>(m), *qA = S.get<uint32_t>(m), *qB = S.get<uint32_t>(m);
-    uint32_t *iota = S.get<uint32_t>(m), *bs = S.get<uint32_t>(m), *as = a_sorted ? nullptr : S.get<uint32_t>(m);
-    uint32_t *s1 = S.get<uint32_t>(nb), *e1 = S.get<uint32_t>(nb), *s2 = S.get<uint32_t>(nb),
-             *e2 = S.get<uint32_t>(nb);
-    uint32_t *P1 = S.get<uint32_t>(m + 1), *P2 = S.get<uint32_t>(m + 1);
-    const int T = (int)((m + kJTile - 1) / kJTile);
-    const int tss = T <= kTsStrideMaxTiles ? kTsStride : 1;
-    uint32_t *ts = S.get<uint32_t>((size_t)4 * T * tss);
-    unsigned *ctl = S.get<unsigned>(8), *chg = S.get<unsigned>(4096);
-    FK_P(perm1); FK_P(perm2); FK_P(pos1); FK_P(pos2); FK_P(qA); FK_P(qB); FK_P(iota); FK_P(bs);
-    FK_P(s1); FK_P(e1); FK_P(s2); FK_P(e2); FK_P(P1); FK_P(P2); FK_P(ts); FK_P(ctl); FK_P(chg);
+    uint32_t *iota = S.get<uint32_t>(m), *perm2 = S.get<uint32_t>(m), *pos2 = S.get<uint32_t>(m),
+             *qA = S.get<uint32_t>(m), *qB = S.get<uint32_t>(m), *bs = S.get<uint32_t>(m);
+    // a-sorted items: the a-order permutation and its inverse are the identity
+    uint32_t *perm1 = a_sorted ? iota : S.get<uint32_t>(m), *pos1 = a_sorted ? iota : S.get<uint32_t>(m);
+    uint32_t *as = a_sorted ? nullptr : S.get<uint32_t>(m);
+    uint32_t *segs = S.get<uint32_t>(4 * nb);
+    unsigned *ctl = S.get<unsigned>(8);
+    FK_P(perm1); FK_P(perm2); FK_P(pos1); FK_P(pos2); FK_P(qA); FK_P(qB); FK_P(iota); FK_P(bs); FK_P(segs);
+    FK_P(ctl);
     if (!a_sorted) FK_P(as);
+    uint32_t *s1 = segs, *e1 = segs + nb, *s2 = segs + 2 * nb, *e2 = segs + 3 * nb;
     k_iota_u32<<<grid_for(m), 256, 0, st>>>(iota, m);
     FK_CHECK_LAUNCH();
-    FK_S(cudaMemsetAsync(s1, 0, nb * 4, st));
-    FK_S(cudaMemsetAsync(e1, 0, nb * 4, st));
-    FK_S(cudaMemsetAsync(s2, 0, nb * 4, st));
-    FK_S(cudaMemsetAsync(e2, 0, nb * 4, st));
-    FK_S(cudaMemsetAsync(ts, 0, (size_t)16 * T * tss, st));
+    FK_S(cudaMemsetAsync(segs, 0, nb * 16, st));
     FK_S(cudaMemsetAsync(ctl, 0, 32, st));
     if (a_sorted) {
-      FK_S(cudaMemcpyAsync(perm1, iota, m * 4, cudaMemcpyDeviceToDevice, st));
-      FK_S(cudaMemcpyAsync(pos1, iota, m * 4, cudaMemcpyDeviceToDevice, st));
       k_seg_bounds_u32<<<grid_for(m), 256, 0, st>>>(a, m, s1, e1);
     } else {
       FK_S(sort_pairs_u32(S, a, as, iota, perm1, m, kb));
@@ -1620,7 +1612,13 @@ int route_items(Scratch &S, const uint32_t *a, const uint32_t *b, int64_t m, con
     {
     RouteItem *items = S.get<RouteItem>(m);
     uint32_t *a_of1 = S.get<uint32_t>(m), *b_of2 = S.get<uint32_t>(m);
-    FK_P(items); FK_P(a_of1); FK_P(b_of2);
+    uint32_t *P1 = S.get<uint32_t>(m + 1), *P2 = S.get<uint32_t>(m + 1);
+    const int T = (int)((m + kJTile - 1) / kJTile);
+    const int tss = T <= kTsStrideMaxTiles ? kTsStride : 1;
+    uint32_t *ts = S.get<uint32_t>((size_t)4 * T * tss);
+    unsigned *chg = S.get<unsigned>(4096);
+    FK_P(items); FK_P(a_of1); FK_P(b_of2); FK_P(P1); FK_P(P2); FK_P(ts); FK_P(chg);
+    FK_S(cudaMemsetAsync(ts, 0, (size_t)16 * T * tss, st));
     k_route_items<<<grid_for(m), 256, 0, st>>>(a, b, fill, pos1, pos2, qA, qB, s1, s2, m, items);
     k_route_orders<<<grid_for(m), 256, 0, st>>>(a, b, perm1, perm2, m, a_of1, b_of2);
     FK_CHECK_LAUNCH();
@@ -1771,18 +1769,17 @@ int btcf_insert(const BDev &P, const uint64_t *keys, int64_t n, uint64_t *failed
   const int end1 = P.f + bits_for(P.nb - 1);
   uint64_t *k0 = S.get<uint64_t>(n), *skey = S.get<uint64_t>(n);
   uint32_t *v0 = S.get<uint32_t>(n), *sval = S.get<uint32_t>(n);
-  uint32_t *seg_lo = S.get<uint32_t>(P.nb + 1), *seg_hi = S.get<uint32_t>(P.nb + 1);
+  uint32_t *seg_lo = S.get<uint32_t>(2 * (P.nb + 1)), *seg_hi = seg_lo + P.nb + 1;  // one memset clears both
   uint8_t *left = S.get<uint8_t>(n);
   int64_t *cnt = S.get<int64_t>(4);  // [0] leftovers, [1] backing items, [2] fails
-  FK_P(k0); FK_P(skey); FK_P(v0); FK_P(sval); FK_P(seg_lo); FK_P(seg_hi); FK_P(left); FK_P(cnt);
+  FK_P(k0); FK_P(skey); FK_P(v0); FK_P(sval); FK_P(seg_lo); FK_P(left); FK_P(cnt);
   FK_S(cudaMemsetAsync(cnt, 0, 32, st));
   FK_S(cudaMemsetAsync(n_failed, 0, 8, st));
   // partition (tcf_bulk.py:133-143): stable sort by (b1, word)
   k_part_keys<<<grid_for(n), 256, 0, st>>>(P, keys, nullptr, n, 0, k0, v0);
   FK_CHECK_LAUNCH();
   FK_S(sort_pairs(S, k0, skey, v0, sval, n, end1));
-  FK_S(cudaMemsetAsync(seg_lo, 0, (P.nb + 1) * 4, st));
-  FK_S(cudaMemsetAsync(seg_hi, 0, (P.nb + 1) * 4, st));
+  FK_S(cudaMemsetAsync(seg_lo, 0, (P.nb + 1) * 8, st));
   k_seg_bounds<<<grid_for(n), 256, 0, st>>>(skey, n, P.f, seg_lo, seg_hi);
   FK_CHECK_LAUNCH();
   // phase 1: shortcut merge up to the cut line, flag leftovers
@@ -1812,8 +1809,7 @@ int btcf_insert(const BDev &P, const uint64_t *keys, int64_t n, uint64_t *failed
     k_dest_keys<<<grid_for(m), 256, 0, st>>>(P, skey, sval, lpos, dest, m, k2, v2);
     FK_CHECK_LAUNCH();
     FK_S(sort_pairs(S, k2, skey2, v2, sval2, m, P.f + bits_for(P.nb)));
-    FK_S(cudaMemsetAsync(seg_lo, 0, (P.nb + 1) * 4, st));
-    FK_S(cudaMemsetAsync(seg_hi, 0, (P.nb + 1) * 4, st));
+    FK_S(cudaMemsetAsync(seg_lo, 0, (P.nb + 1) * 8, st));
     k_seg_bounds<<<grid_for(m), 256, 0, st>>>(skey2, m, P.f, seg_lo, seg_hi);
     FK_CHECK_LAUNCH();
     rc = merge_segments<S_t>(P, skey2, seg_lo, seg_hi, 1, 0, nullptr, status, st);

@@ -104,6 +104,7 @@ class BulkTcf:
             "backing": (dt, p.backing_slots)})
         self._counters_dev = torch.zeros(3, dtype=torch.int64, device=self._device)
         self._status = torch.empty(1, dtype=torch.int32, device=self._device)
+        self._insert_res = torch.empty(2, dtype=torch.int64, device=self._device)
         self._geom = _lib.BtcfGeom(p.num_blocks, p.backing_slots, p.block_slots, p.tag_bits, dt.itemsize,
                                    p.cut_slots, p.probe_limit, 0, p.seed & ((1 << 64) - 1))
         self._op_lock = threading.Lock()
@@ -203,18 +204,22 @@ class BulkTcf:
         if n == 0:
             return np.zeros(0, dtype=np.uint64) if kind == "numpy" else k[:0]
         failed = torch.empty(n, dtype=torch.int64, device=self._device)
-        nfail = torch.zeros(1, dtype=torch.int64, device=self._device)
         with self._op_lock:
             self._t.before_device_op()
-            self._status.fill_(-1)
+            # [0] failure count (zeroed by the call), [1] status word (low half,
+            # -1 = none): one fill before, one copy after
+            res = self._insert_res
+            res.fill_(-1)
             b, f, bk = self._ptrs()
             rc = self._lib.fk_btcf_insert(ctypes.byref(self._geom), b, f, bk, _lib.dptr(k), 0, n, _lib.dptr(failed),
-                                          _lib.dptr(nfail), _lib.dptr(self._counters_dev), _lib.dptr(self._status),
+                                          _lib.dptr(res), _lib.dptr(self._counters_dev), _lib.dptr(res[1:]),
                                           _lib.stream_ptr(torch))
             _lib.check(rc, "btcf insert")
             self._t.after_device_write()
-            self._check_status("insert")
-        m = int(nfail.item())
+            m, v = (int(x) for x in res.cpu())
+            v &= 0xFFFFFFFF
+            if v != _NO_STATUS:
+                raise AssertionError("insert overfilled block %d" % (v - 1))
         out = failed[:m]
         if kind == "cuda":
             return out
