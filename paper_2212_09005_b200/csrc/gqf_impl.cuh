@@ -596,26 +596,38 @@ __global__ void __launch_bounds__(kPartThreads) k_part2_scatter(const uint32_t *
   }
 }
 
-// One CTA per partition: hash-aggregate the low W bits, bitonic-sort the
-// distinct ones, write (fp, count) at the partition's own offset.
+// One CTA per partition: hash-aggregate the low W bits, order the distinct
+// ones, write (fp, count) at the partition's own offset.
+// The hash is order-preserving (home slot = the key's top lg_slots bits) with
+// linear probing that never wraps (kAggPad overflow slots), so the table read
+// in slot order is sorted except inside clusters of occupied slots: a key's
+// home lies in its own cluster and homes grow with the keys.  An in-order
+// compaction plus odd-even transposition rounds (a few: clusters are short at
+// the ~11 % load of a 3 K-occurrence partition) sort it; more than
+// kAggOddEvenMax rounds (skewed keys, dense tables) falls back to a bitonic
+// sort.
+constexpr int kAggPad = 256;
+constexpr int kAggOddEvenMax = 32;
 __global__ void __launch_bounds__(kAggThreads) k_part_aggregate(const uint32_t *__restrict__ in,
                                                                 const unsigned long long *__restrict__ bounds2,
                                                                 int64_t NP, int W, uint64_t *__restrict__ out_fp,
                                                                 uint32_t *__restrict__ out_cnt,
                                                                 int64_t *__restrict__ ucount,
                                                                 unsigned *__restrict__ overflow, int lg_slots) {
-  __shared__ uint64_t tab[kAggSlots];  // keys | counts while counting, then sorted (key << 32 | count) words
-  __shared__ unsigned s_n, s_bad;
-  uint32_t *hk = reinterpret_cast<uint32_t *>(tab), *hc = hk + kAggSlots;
+  constexpr int kTab = kAggSlots + kAggPad;
+  __shared__ uint64_t tab[kTab];  // keys | counts while counting, then ordered (key << 32 | count) words
+  __shared__ unsigned s_n, s_bad, s_cnt[kAggThreads / 32];
+  uint32_t *hk = reinterpret_cast<uint32_t *>(tab), *hc = hk + kTab;
   constexpr uint32_t kEmpty = 0xFFFFFFFFu;
+  const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int64_t p = blockIdx.x; p < NP; p += gridDim.x) {
     const int64_t a = (int64_t)bounds2[p], e = (int64_t)bounds2[p + 1];
     if (a == e) {
       if (threadIdx.x == 0) ucount[p] = 0;
       continue;
     }
-    const uint32_t nslots = 1u << lg_slots;  // <= kAggSlots (smaller only to exercise the overflow path)
-    for (int i = threadIdx.x; i < kAggSlots; i += kAggThreads) {
+    const uint32_t limit = (1u << lg_slots) + kAggPad;  // probe bound (lg_slots < 12 only in overflow tests)
+    for (int i = threadIdx.x; i < kTab; i += kAggThreads) {
       hk[i] = kEmpty;
       hc[i] = 0;
     }
@@ -635,8 +647,7 @@ __global__ void __launch_bounds__(kAggThreads) k_part_aggregate(const uint32_t *
       for (int u = 0; u < 8; u++) {
         const uint32_t k = v[u];
         if (k == kEmpty) continue;  // (keys have W <= 31 bits)
-        uint32_t h = (k * 0x9E3779B1u) >> (32 - lg_slots);
-        uint32_t probes = 0;
+        uint32_t h = W >= lg_slots ? k >> (W - lg_slots) : k << (lg_slots - W);
         for (;;) {
           // plain read first: most occurrences find their key already there
           // and need one shared-memory atomic, not two
@@ -646,8 +657,7 @@ __global__ void __launch_bounds__(kAggThreads) k_part_aggregate(const uint32_t *
             atomicAdd(&hc[h], 1u);
             break;
           }
-          h = (h + 1) & (nslots - 1);
-          if (++probes == nslots) {
+          if (++h == limit) {
             s_bad = 1;
             break;
           }
@@ -663,57 +673,86 @@ __global__ void __launch_bounds__(kAggThreads) k_part_aggregate(const uint32_t *
       __syncthreads();
       continue;
     }
-    // compact the occupied entries to the front (order arbitrary), as
-    // 64-bit (key << 32 | count) words in place of the table
-    uint64_t *kv = tab;
-    uint64_t mine[kAggSlots / kAggThreads];
+    // in-order compaction: thread t owns slots [t*R, (t+1)*R)
+    constexpr int R = (kTab + kAggThreads - 1) / kAggThreads;
+    uint64_t mine[R];
     int nm = 0;
 #pragma unroll
-    for (int j = 0; j < kAggSlots / kAggThreads; j++) {
-      const int i = j * kAggThreads + threadIdx.x;
-      if (hk[i] != kEmpty) mine[nm++] = ((uint64_t)hk[i] << 32) | hc[i];
+    for (int j = 0; j < R; j++) {
+      const int i = threadIdx.x * R + j;
+      if (i < kTab && hk[i] != kEmpty) mine[nm++] = ((uint64_t)hk[i] << 32) | hc[i];
     }
+    unsigned inc = nm;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned t = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+      if ((int)lane >= o) inc += t;
+    }
+    if (lane == 31) s_cnt[warp] = inc;
+    __syncthreads();  // (also: every thread has read the table)
+    unsigned base = inc - nm;
+    for (unsigned w = 0; w < warp; w++) base += s_cnt[w];
+    unsigned d = 0;
+    for (unsigned w = 0; w < kAggThreads / 32; w++) d += s_cnt[w];
+    uint64_t *kv = tab;
+    for (int j = 0; j < nm; j++) kv[base + j] = mine[j];
     __syncthreads();
-    for (int j = 0; j < nm; j++) kv[atomicAdd(&s_n, 1u)] = mine[j];
-    __syncthreads();
-    const unsigned d = s_n;
-    unsigned m2 = 1;
-    while (m2 < d) m2 <<= 1;
-    for (unsigned i = d + threadIdx.x; i < m2; i += kAggThreads) kv[i] = ~0ull;  // pads sort last
-    __syncthreads();
-    // bitonic sort; stages whose partner distance is below 64 stay inside a
-    // warp's own 64-element chunks (no block barrier), the rest sync the CTA
-    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    constexpr unsigned NW = kAggThreads / 32;
-    for (unsigned k2 = 2; k2 <= m2; k2 <<= 1) {
-      for (unsigned j2 = k2 >> 1; j2 > 0; j2 >>= 1) {
-        const unsigned lj = __ffs(j2) - 1;  // j2 is a power of two: shifts, not divisions
-        if (j2 >= 64) {
-          for (unsigned q = threadIdx.x; q < m2 / 2; q += kAggThreads) {
-            const unsigned i = ((q >> lj) << (lj + 1)) | (q & (j2 - 1)), l = i + j2;
-            const uint64_t x = kv[i], y = kv[l];
-            if ((x > y) == ((i & k2) == 0)) {
-              kv[i] = y;
-              kv[l] = x;
-            }
-          }
-          __syncthreads();
-        } else {
-          const unsigned span = m2 < 64 ? m2 : 64;
-          for (unsigned c = warp; c * span < m2; c += NW) {
-            if (lane < span / 2) {
-              const unsigned i = c * span + (((lane >> lj) << (lj + 1)) | (lane & (j2 - 1))), l = i + j2;
+    // odd-even transposition rounds until no pair moves
+    bool sorted = false;
+    for (int r = 0; r < kAggOddEvenMax; r++) {
+      bool moved = false;
+      for (unsigned i = 2 * threadIdx.x + (r & 1); i + 1 < d; i += 2 * kAggThreads) {
+        const uint64_t x = kv[i], y = kv[i + 1];
+        if (x > y) {
+          kv[i] = y;
+          kv[i + 1] = x;
+          moved = true;
+        }
+      }
+      const bool any = __syncthreads_or(moved);
+      if (!any && r > 0) {
+        sorted = true;
+        break;
+      }
+    }
+    if (!sorted) {
+      unsigned m2 = 1;
+      while (m2 < d) m2 <<= 1;
+      for (unsigned i = d + threadIdx.x; i < m2; i += kAggThreads) kv[i] = ~0ull;  // pads sort last
+      __syncthreads();
+      // bitonic sort; stages whose partner distance is below 64 stay inside a
+      // warp's own 64-element chunks (no block barrier), the rest sync the CTA
+      constexpr unsigned NW = kAggThreads / 32;
+      for (unsigned k2 = 2; k2 <= m2; k2 <<= 1) {
+        for (unsigned j2 = k2 >> 1; j2 > 0; j2 >>= 1) {
+          const unsigned lj = __ffs(j2) - 1;  // j2 is a power of two: shifts, not divisions
+          if (j2 >= 64) {
+            for (unsigned q = threadIdx.x; q < m2 / 2; q += kAggThreads) {
+              const unsigned i = ((q >> lj) << (lj + 1)) | (q & (j2 - 1)), l = i + j2;
               const uint64_t x = kv[i], y = kv[l];
               if ((x > y) == ((i & k2) == 0)) {
                 kv[i] = y;
                 kv[l] = x;
               }
             }
+            __syncthreads();
+          } else {
+            const unsigned span = m2 < 64 ? m2 : 64;
+            for (unsigned c = warp; c * span < m2; c += NW) {
+              if (lane < span / 2) {
+                const unsigned i = c * span + (((lane >> lj) << (lj + 1)) | (lane & (j2 - 1))), l = i + j2;
+                const uint64_t x = kv[i], y = kv[l];
+                if ((x > y) == ((i & k2) == 0)) {
+                  kv[i] = y;
+                  kv[l] = x;
+                }
+              }
+            }
+            __syncwarp();
           }
-          __syncwarp();
         }
+        __syncthreads();
       }
-      __syncthreads();
     }
     for (unsigned j = threadIdx.x; j < d; j += kAggThreads) {
       const uint64_t v = kv[j];

@@ -632,6 +632,55 @@ def test_partition_counting_overflow_falls_back(oracle, monkeypatch):
     assert g.count_many(base[7:8])[0] == o.count_many(base[7:8])[0]
 
 
+def _unmix64(h):
+    """Inverse of the SplitMix64 finalizer (hashing.mix64): keys whose
+    fingerprints are chosen."""
+    M = (1 << 64) - 1
+
+    def unshift(x, s):
+        y = x
+        for _ in range(64 // s + 1):
+            y = x ^ (y >> s)
+        return y & M
+
+    x = unshift(h & M, 31)
+    x = (x * pow(0x94D049BB133111EB, -1, 1 << 64)) & M
+    x = unshift(x, 27)
+    x = (x * pow(0xBF58476D1CE4E5B9, -1, 1 << 64)) & M
+    return unshift(x, 30)
+
+
+def test_partition_counting_long_clusters_sort(oracle, monkeypatch):
+    """The aggregation's order-preserving hash puts fingerprints that share
+    their top bits in one probe cluster; 3000 consecutive fingerprints in one
+    partition make a cluster too long for the odd-even rounds, so the
+    partition is ordered by the bitonic fallback: same image as the sort +
+    run-length path and the oracle."""
+    from paper_2212_09005_b200 import Gqf
+    from paper_2212_09005_b200.hashing import fingerprint_many
+    q, r = 18, 16
+    g = Gqf(q=q, r=r)
+    seed = g.params.seed
+    top = 0x2A5 << (q + r - 10)
+    want = [top | j for j in range(3000)]
+    structured = np.array([_unmix64(h) ^ seed for h in want], dtype=np.uint64)
+    assert np.array_equal(fingerprint_many(structured, seed, q + r), np.array(want, dtype=np.uint64))
+    rng = np.random.default_rng(5)
+    keys = rng.permutation(np.concatenate([np.repeat(structured, 3),
+                                           rng.integers(0, 2 ** 63, 40_000, dtype=np.uint64)]))
+    monkeypatch.setenv("FK_GQF_PART_MIN", "1000")
+    g.bulk_insert(keys)
+    monkeypatch.setenv("FK_GQF_PART", "0")
+    b = Gqf(q=q, r=r)
+    b.bulk_insert(keys)
+    for name in ("_slots", "_occupieds", "_runends", "_offsets", "_stats"):
+        assert np.array_equal(getattr(g, name), getattr(b, name)), name
+    o = _oracle(g, oracle)
+    assert o.bulk_insert(keys) == []
+    same_image(g, o)
+    assert (g.count_many(structured) == 3).all()
+
+
 def _host_cluster_stats(g):
     """The reference's cluster_stats (gqf.py:416-428) on the host mirrors."""
     occ = np.unpackbits(g._occupieds.view(np.uint8), bitorder="little")
