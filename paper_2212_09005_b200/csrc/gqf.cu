@@ -854,11 +854,18 @@ int apply_t(const fk_gqf_geom *g, const fk_gqf_tables *cur, const fk_gqf_tables 
 
   // 5-6. old counts (the pure count query, or the join with the decoded
   // items), new absolute counts
-  if (go_local)
+  // An insert into an empty table (the bench's and a fresh filter's case):
+  // the new counts are the batch sums and the merged items are the batch.
+  const bool fresh_insert = !go_local && g_old == 0 && plain_ins;  // (explicit deltas may be 0)
+  if (go_local) {
     k_gqf_count<S_t><<<blocks_for(m), 256, 0, st>>>(T0, uniq, 1, 0, m, c_old);
-  else
-    k_old_counts_join<<<blocks_for(join_threads(m)), 256, 0, st>>>(uniq, m, o_fp, o_cnt, g_old, c_old);
-  k_new_counts<<<blocks_for(m), 256, 0, st>>>(c_old, sums, m, is_del ? 1 : 0, c_new);
+    k_new_counts<<<blocks_for(m), 256, 0, st>>>(c_old, sums, m, is_del ? 1 : 0, c_new);
+  } else if (fresh_insert) {
+    c_new = sums;
+  } else {
+    k_old_counts_join<<<blocks_for(join_threads(m)), 256, 0, st>>>(uniq, m, o_fp, o_cnt, g_old, sums, is_del ? 1 : 0,
+                                                                   c_old, c_new);
+  }
 
   // 7. delete found flags: sequential semantics via a segmented prefix sum,
   // computed in sorted order, then scattered to input order
@@ -913,6 +920,11 @@ int apply_t(const fk_gqf_geom *g, const fk_gqf_tables *cur, const fk_gqf_tables 
 
     // 9-10. drop old items the batch updates and zero counts, then merge the
     // two duplicate-free sorted lists
+    if (fresh_insert) {
+      G = m;  // counts are positive sums
+      it_fp = uniq;
+      it_cnt = sums;
+    } else {
     uint8_t *keep_o = S.get<uint8_t>(g_old), *keep_u = S.get<uint8_t>(m);
     uint64_t *o2_fp = S.get<uint64_t>(g_old), *o2_cnt = S.get<uint64_t>(g_old);
     uint64_t *u2_fp = S.get<uint64_t>(m), *u2_cnt = S.get<uint64_t>(m);
@@ -931,6 +943,7 @@ int apply_t(const fk_gqf_geom *g, const fk_gqf_tables *cur, const fk_gqf_tables 
     it_cnt = S.get<uint64_t>(G);
     if (S.err) return -(int)S.err;
     if (G > 0) FK_CU(cub_merge(S, o2_fp, o2_cnt, hn[0], u2_fp, u2_cnt, hn[2], it_fp, it_cnt));
+    }
 
     // 11-12. placement and the capacity predicates.  Region placement
     // (default): per-region max-plus summaries, a scan over the regions, then

@@ -947,10 +947,21 @@ __global__ void k_keep_old_join(const uint64_t *__restrict__ o_fp, int64_t g_old
 }
 
 // The old count of every batch fingerprint from the decoded table (replaces
-// the count query when the whole table is decoded anyway).
+// the count query when the whole table is decoded anyway) and its new count
+// (as k_new_counts).
 __global__ void k_old_counts_join(const uint64_t *__restrict__ uniq, int64_t m, const uint64_t *__restrict__ o_fp,
-                                  const uint64_t *__restrict__ o_cnt, int64_t g_old, uint64_t *__restrict__ c_old) {
-  warp_join(uniq, m, o_fp, g_old, [&](int64_t j, int64_t p, bool hit) { c_old[j] = hit ? o_cnt[p] : 0; });
+                                  const uint64_t *__restrict__ o_cnt, int64_t g_old, const uint64_t *__restrict__ sums,
+                                  int is_delete, uint64_t *__restrict__ c_old, uint64_t *__restrict__ c_new) {
+  warp_join(uniq, m, o_fp, g_old, [&](int64_t j, int64_t p, bool hit) {
+    const uint64_t c = hit ? o_cnt[p] : 0, s = sums[j];
+    c_old[j] = c;
+    if (is_delete) {
+      c_new[j] = c > s ? c - s : 0;
+    } else {
+      const uint64_t t = c + s;
+      c_new[j] = t < c ? ~0ull : t;
+    }
+  });
 }
 
 // Decode pass over occupied quotient words: mode 0 counts groups per word,
