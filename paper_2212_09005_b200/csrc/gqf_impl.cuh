@@ -469,24 +469,38 @@ struct PartSmem {
   }
 };
 
-__global__ void __launch_bounds__(kPartThreads) k_part1_scatter(const uint64_t *__restrict__ keys, int keys_are_fps,
-                                                                uint64_t seed, uint64_t fmask, int qr, int64_t n,
-                                                                unsigned long long *__restrict__ cursor,
-                                                                uint32_t *__restrict__ out) {
+#ifndef FK_PART_MINB
+#define FK_PART_MINB 2
+#endif
+__global__ void __launch_bounds__(kPartThreads, FK_PART_MINB) k_part1_scatter(const uint64_t *__restrict__ keys,
+                                                                              int keys_are_fps, uint64_t seed,
+                                                                              uint64_t fmask, int qr, int64_t n,
+                                                                              unsigned long long *__restrict__ cursor,
+                                                                              uint32_t *__restrict__ out) {
   extern __shared__ __align__(16) unsigned char part_sm[];
   PartSmem P(part_sm);
   const int sh = qr - kPartBits;
   const uint64_t lmask = (1ull << sh) - 1;
-  for (int64_t t0 = (int64_t)blockIdx.x * kPartTile; t0 < n; t0 += (int64_t)gridDim.x * kPartTile) {
+  const int64_t step = (int64_t)gridDim.x * kPartTile;
+  // the next tile's keys are loaded while this tile is scattered
+  uint64_t kr[kPartItems];
+#pragma unroll
+  for (int j = 0; j < kPartItems; j++) {
+    const int64_t i = (int64_t)blockIdx.x * kPartTile + (int64_t)j * kPartThreads + threadIdx.x;
+    kr[j] = i < n ? __ldcs(keys + i) : 0ull;
+  }
+  for (int64_t t0 = (int64_t)blockIdx.x * kPartTile; t0 < n; t0 += step) {
     uint32_t dg[kPartItems], val[kPartItems];
     bool ok[kPartItems];
 #pragma unroll
     for (int j = 0; j < kPartItems; j++) {
       const int64_t i = t0 + (int64_t)j * kPartThreads + threadIdx.x;
       ok[j] = i < n;
-      const uint64_t fp = ok[j] ? part_fp(keys, keys_are_fps, seed, fmask, i) : 0ull;
+      const uint64_t fp = (keys_are_fps ? kr[j] : mix64(kr[j] ^ seed)) & fmask;
       dg[j] = (uint32_t)(fp >> sh);
       val[j] = (uint32_t)(fp & lmask);
+      const int64_t i2 = i + step;
+      kr[j] = i2 < n ? __ldcs(keys + i2) : 0ull;
     }
     part_scatter_tile(dg, val, ok, cursor, out, P.cnt, P.off, P.base, P.val, P.dg);
   }
@@ -569,30 +583,54 @@ __global__ void __launch_bounds__(kPartBins) k_part_plan1(const unsigned long lo
 // Pass 2: tiles never straddle a pass-1 digit (grid-stride over
 // (digit, tile) pairs), so the partition is d1 << kPartBits | d2 and the
 // scatter keeps the low sh2 bits.
-__global__ void __launch_bounds__(kPartThreads) k_part2_scatter(const uint32_t *__restrict__ in,
-                                                                const unsigned long long *__restrict__ bounds1,
-                                                                const unsigned long long *__restrict__ tile_start,
-                                                                int sh2, int p2, unsigned long long *__restrict__ cursor,
-                                                                uint32_t *__restrict__ out) {
+__global__ void __launch_bounds__(kPartThreads, FK_PART_MINB) k_part2_scatter(const uint32_t *__restrict__ in,
+                                                                              const unsigned long long *__restrict__ bounds1,
+                                                                              const unsigned long long *__restrict__ tile_start,
+                                                                              int sh2, int p2,
+                                                                              unsigned long long *__restrict__ cursor,
+                                                                              uint32_t *__restrict__ out) {
   extern __shared__ __align__(16) unsigned char part_sm[];
   PartSmem P(part_sm);
+  __shared__ unsigned long long s_ts[kPartBins + 1], s_b1[kPartBins + 1];
+  for (int i = threadIdx.x; i <= kPartBins; i += blockDim.x) {
+    s_ts[i] = tile_start[i];
+    s_b1[i] = bounds1[i];
+  }
+  __syncthreads();
   const uint32_t lmask = sh2 >= 32 ? 0xFFFFFFFFu : ((1u << sh2) - 1u);
-  const int64_t ntiles = (int64_t)tile_start[kPartBins];
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const int d1 = part_tile_digit(tile_start, t);
-    const int64_t a = (int64_t)bounds1[d1] + (t - (int64_t)tile_start[d1]) * kPartTile;
-    const int64_t e = (int64_t)bounds1[d1 + 1];
+  const int64_t ntiles = (int64_t)s_ts[kPartBins];
+  // the next tile's values are loaded while this tile is scattered
+  int64_t t = blockIdx.x;
+  int d1 = t < ntiles ? part_tile_digit(s_ts, t) : 0;
+  int64_t a = t < ntiles ? (int64_t)s_b1[d1] + (t - (int64_t)s_ts[d1]) * kPartTile : 0;
+  int64_t e = t < ntiles ? (int64_t)s_b1[d1 + 1] : 0;
+  uint32_t vr[kPartItems];
+#pragma unroll
+  for (int j = 0; j < kPartItems; j++) {
+    const int64_t i = a + (int64_t)j * kPartThreads + threadIdx.x;
+    vr[j] = i < e ? __ldcs(in + i) : 0u;
+  }
+  for (; t < ntiles; t += gridDim.x) {
+    const int64_t t2 = t + gridDim.x;
+    const int d1n = t2 < ntiles ? part_tile_digit(s_ts, t2) : 0;
+    const int64_t an = t2 < ntiles ? (int64_t)s_b1[d1n] + (t2 - (int64_t)s_ts[d1n]) * kPartTile : 0;
+    const int64_t en = t2 < ntiles ? (int64_t)s_b1[d1n + 1] : 0;
     uint32_t dg[kPartItems], val[kPartItems];
     bool ok[kPartItems];
 #pragma unroll
     for (int j = 0; j < kPartItems; j++) {
       const int64_t i = a + (int64_t)j * kPartThreads + threadIdx.x;
       ok[j] = i < e;
-      const uint32_t v = ok[j] ? __ldcs(in + i) : 0u;
+      const uint32_t v = vr[j];
       dg[j] = (v >> sh2) & ((1u << p2) - 1);
       val[j] = v & lmask;
+      const int64_t i2 = an + (int64_t)j * kPartThreads + threadIdx.x;
+      vr[j] = i2 < en ? __ldcs(in + i2) : 0u;
     }
     part_scatter_tile(dg, val, ok, cursor + ((uint64_t)d1 << p2), out, P.cnt, P.off, P.base, P.val, P.dg);
+    d1 = d1n;
+    a = an;
+    e = en;
   }
 }
 
