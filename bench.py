@@ -86,32 +86,44 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks/throttle reasons sampled during the timed region.
+    start() launches the sampler ahead of the warm-up (nvidia-smi takes a
+    moment to produce its first row); `with sampler:` marks the timed
+    window, and summary() keeps the rows that arrived inside it."""
 
     FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown," \
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
 
     def __init__(self, index):
         self.index, self.rows, self.proc = index, [], None
+        self.t0 = self.t1 = None
+
+    def start(self):
+        if self.proc is None:
+            try:
+                self.proc = subprocess.Popen(
+                    ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS, "--format=csv,noheader,nounits",
+                     "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                self.thread = threading.Thread(target=self._read, daemon=True)
+                self.thread.start()
+            except OSError:
+                self.proc = None
+        return self
 
     def __enter__(self):
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS, "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
-            self.thread.start()
-        except OSError:
-            self.proc = None
+        self.start()
+        self.t0 = time.monotonic()
         return self
 
     def _read(self):
         for line in self.proc.stdout:
             parts = [x.strip() for x in line.split(",")]
             if len(parts) == 6:
-                self.rows.append(parts)
+                self.rows.append((time.monotonic(), parts))
 
     def __exit__(self, *exc):
+        self.t1 = time.monotonic()
+        time.sleep(0.15)  # the row covering the window's end
         if self.proc:
             self.proc.terminate()
             try:
@@ -120,14 +132,18 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        if not self.rows:
+        rows = [r for t, r in self.rows if self.t0 is not None and self.t0 <= t <= (self.t1 or t) + 0.12]
+        window = "timed region"
+        if not rows:
+            rows, window = [r for _, r in self.rows], "whole run (no row inside the timed region)"
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i] == "Active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(rows), "window": window}
 
 
 def max_over_ranks(torch, value, dev):
@@ -378,6 +394,7 @@ def run_ours(args, rank, world, local_rank):
             ev[4].record(stream)
         return codes, fpos, fneg, rem
 
+    clk = ClockSampler(local_rank).start()  # running before the timed region starts
     for _ in range(args.warmup):
         codes, fpos, fneg, rem = step()
     torch.cuda.synchronize()
@@ -392,7 +409,7 @@ def run_ours(args, rank, world, local_rank):
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local_rank) as clk:
+    with clk:
         t0.record(stream)
         for s in range(args.steps):
             step(evs[s])
@@ -687,6 +704,7 @@ def run_workload(args, rank, world, local_rank):
             ev[len(ops)].record(stream)
         return out
 
+    clk = ClockSampler(local_rank).start()  # running before the timed region starts
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -708,7 +726,7 @@ def run_workload(args, rank, world, local_rank):
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local_rank) as clk:
+    with clk:
         t0.record(stream)
         for s in range(steps):
             step(evs[s])
