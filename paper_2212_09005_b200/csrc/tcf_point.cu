@@ -137,6 +137,7 @@ static int prep_ordered(const fk_tcf_geom *g, int64_t n, void *ws, size_t ws_byt
     FK_TRY(cudaMemsetAsync(X->res2, 0xFF, (size_t)((g->num_blocks >> X->res_shift) + 1) * 4, st));
   }
   X->slots = 1;
+  X->held_only = env_int("FK_ORD_HELD_ONLY", 1);
   FK_TRY(cudaMemsetAsync(X->bres, 0xFF, (size_t)(g->backing_slots ? g->backing_slots : 1) * 4, st));
   FK_TRY(cudaMemsetAsync(X->ctl, 0, 64, st));
   return 0;

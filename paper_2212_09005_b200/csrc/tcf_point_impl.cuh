@@ -470,7 +470,20 @@ struct OrdScratch {
   int prefetch;         // 1: the reserve pass prefetches each key's b1 block into L2
   uint32_t *res2;       // one-barrier kernel: reservation words of odd rounds
   int slots;            // one-barrier kernel: keys held per thread (<= KB)
+  int held_only;        // one-barrier kernel: clear only the words a key holds (no no-op CAS)
 };
+
+// A control word every thread needs after a grid barrier, loaded once per
+// CTA and broadcast through shared memory: one L2 request per CTA instead of
+// one per warp to a single address (measured on the B200: 2^20-slot ordered
+// insert 0.66 -> 0.58 ms, 2^24 1.60 -> 1.46 ms).  All threads must call.
+__device__ __forceinline__ unsigned cta_ldcg(const unsigned *a) {
+  __shared__ unsigned s_v;
+  __syncthreads();  // (s_v is reused)
+  if (threadIdx.x == 0) s_v = __ldcg(a);
+  __syncthreads();
+  return s_v;
+}
 
 // CTA-wide OR of a predicate (all threads of the CTA must call).
 __device__ __forceinline__ bool cta_any(bool p) { return __syncthreads_or(p ? 1 : 0) != 0; }
@@ -571,7 +584,7 @@ __device__ __forceinline__ unsigned ordered_backing_phase(const TcfDev &P, const
                                                           cg::grid_group &grid, unsigned round, long long *n_a,
                                                           long long *n_b) {
   grid.sync();
-  int64_t nd = (int64_t)__ldcg(&X.ctl[2]);
+  int64_t nd = (int64_t)cta_ldcg(&X.ctl[2]);
   if (nd > X.defer_cap) nd = X.defer_cap;
   S *bk = reinterpret_cast<S *>(P.backing);
   if (nd > 0) {
@@ -652,7 +665,7 @@ __device__ __forceinline__ unsigned ordered_backing_phase(const TcfDev &P, const
         if (blockIdx.x == 0) X.ctl[3 + ((round + 1) & 1)] = 0;
       }
       grid.sync();
-      unsigned cnt = __ldcg(&X.ctl[3 + (round & 1)]);
+      unsigned cnt = cta_ldcg(&X.ctl[3 + (round & 1)]);
       round++;
       if (cnt == 0) break;
     }
@@ -834,7 +847,7 @@ __global__ void __launch_bounds__(256, 4)
       }
     }
     grid.sync();
-    nc = (int64_t)__ldcg(&X.ctl[cur ^ 1]);
+    nc = (int64_t)cta_ldcg(&X.ctl[cur ^ 1]);
     cur ^= 1;
     F = Fend;
     round++;
@@ -968,7 +981,7 @@ __global__ void __launch_bounds__(256, 4)
       }
     }
     grid.sync();
-    const unsigned total = __ldcg(&X.ctl[8 + r % 3]);
+    const unsigned total = cta_ldcg(&X.ctl[8 + r % 3]);
 
     // ---- commit round r, refill from the frontier for round r+1 -------------
     // A key holding its b1 word commits when it also holds its b2 word, or
@@ -1025,8 +1038,16 @@ __global__ void __launch_bounds__(256, 4)
         if (!pend[j]) continue;
         uint32_t g1 = b1[j] >> rs, g2 = b2[j] >> rs;
         if (!go[j]) {  // lost: retract our own bids so the array is clean
-          atomicCAS(&R[g1], idx[j], kNoRes);
-          if (g2 != g1) atomicCAS(&R[g2], idx[j], kNoRes);
+          if (X.held_only) {
+            // a word's minimum bidder always clears it (release or this
+            // retraction), so a bid on a word held by another key is gone
+            // once that key clears it: only the words we hold need a store
+            if (hold[j]) st_u32(&R[g1], kNoRes, pol_keep);
+            if (g2 != g1 && hold2[j]) st_u32(&R[g2], kNoRes, pol_keep);
+          } else {
+            atomicCAS(&R[g1], idx[j], kNoRes);
+            if (g2 != g1) atomicCAS(&R[g2], idx[j], kNoRes);
+          }
           losses++;
           continue;
         }
@@ -1059,7 +1080,7 @@ __global__ void __launch_bounds__(256, 4)
         st_u32(&R[g1], kNoRes, pol_keep);
         if (g2 != g1) {
           if (hold2[j]) st_u32(&R[g2], kNoRes, pol_keep);
-          else atomicCAS(&R[g2], idx[j], kNoRes);
+          else if (!X.held_only) atomicCAS(&R[g2], idx[j], kNoRes);
         }
         pend[j] = false;
       }
@@ -1270,7 +1291,7 @@ __global__ void __launch_bounds__(256, 4)
       }
     }
     grid.sync();
-    nc = (int64_t)__ldcg(&X.ctl[cur ^ 1]);
+    nc = (int64_t)cta_ldcg(&X.ctl[cur ^ 1]);
     cur ^= 1;
     F = Fend;
     round++;
