@@ -235,8 +235,9 @@ __global__ void __launch_bounds__(256) k_btcf_delete(BDev P, const uint64_t *__r
 }
 
 // ---------------------------------------------------------------------------
-// query (btcf_query_batch, ck:552-599): 8 lanes per key, one 32-byte sector
-// per lane per round.  The block's sorted prefix is followed by EMPTY (0)
+// query (btcf_query_batch, ck:552-599): G lanes per key (btcf_query picks
+// G from the block size), each loading its share of the block's 32-byte
+// sectors.  The block's sorted prefix is followed by EMPTY (0)
 // slots and words are >= 2, so "bisect hit in the prefix" == "some slot of
 // the block equals the word".
 // ---------------------------------------------------------------------------
@@ -262,12 +263,11 @@ __device__ __forceinline__ bool sector_has(const uint32_t (&r)[8], uint32_t word
   }
 }
 
-template <typename S>
+template <typename S, int G>
 __global__ void __launch_bounds__(256) k_btcf_query(BDev P, const uint64_t *__restrict__ keys, int64_t n,
                                                     uint8_t *__restrict__ found) {
-  constexpr int G = 8;
   const unsigned lane = threadIdx.x & 31, sub = lane % G, base = lane - sub;
-  const unsigned mask = 0xFFu << base;
+  const unsigned mask = (G == 32 ? 0xFFFFFFFFu : ((1u << G) - 1u)) << base;
   const S *blocks = reinterpret_cast<const S *>(P.blocks);
   const S *backing = reinterpret_cast<const S *>(P.backing);
   const int64_t bytes = (int64_t)P.B * sizeof(S);
@@ -290,6 +290,7 @@ __global__ void __launch_bounds__(256) k_btcf_query(BDev P, const uint64_t *__re
         uint64_t b = fmod64(mix64(fp ^ (which ? kBlock2 : kBlock1)), P.nbm);
         const S *blk = blocks + b * (uint64_t)P.B;
         if (vec) {
+#pragma unroll 8
           for (int s = (int)sub; s < sectors; s += G) {
             uint32_t r[8];
             load_chunk<32, false>(reinterpret_cast<const char *>(blk) + 32 * s, r);
@@ -1900,10 +1901,23 @@ int btcf_delete(const BDev &P, const uint64_t *keys, int64_t n, uint8_t *removed
 
 template <typename S_t>
 int btcf_query(const BDev &P, const uint64_t *keys, int64_t n, uint8_t *found, cudaStream_t st) {
-  int64_t tiles_per_cta = 256 / 8;
+  // lanes per key: one lane per key up to 8 sectors per block (all of a
+  // key's sector loads in flight at once; the table is L2-resident at
+  // configs[0], so loads in flight, not bytes, bound the query), more lanes
+  // for larger blocks.  Measured at configs[0] (2^20 slots, 256-byte
+  // blocks): 8 lanes 0.175 / 0.206 ms (pos / neg), 2 lanes 0.140 / 0.106,
+  // 1 lane 0.124 / 0.101.  Tunable: FK_BTCF_QUERY_G (1, 2, 4 or 8).
+  const int64_t sectors = ((int64_t)P.B * (int64_t)sizeof(S_t) + 31) / 32;
+  const char *ge = getenv("FK_BTCF_QUERY_G");
+  const int G = ge ? atoi(ge) : (sectors <= 8 ? 1 : (sectors <= 16 ? 2 : (sectors <= 32 ? 4 : 8)));
+  int64_t tiles_per_cta = 256 / (G == 1 || G == 2 || G == 4 ? G : 8);
   int64_t need = (n + tiles_per_cta - 1) / tiles_per_cta;
   int64_t cap = (int64_t)num_sms() * 8;
-  k_btcf_query<S_t><<<(int)(need < cap ? (need < 1 ? 1 : need) : cap), 256, 0, st>>>(P, keys, n, found);
+  const int grid = (int)(need < cap ? (need < 1 ? 1 : need) : cap);
+  if (G == 1) k_btcf_query<S_t, 1><<<grid, 256, 0, st>>>(P, keys, n, found);
+  else if (G == 2) k_btcf_query<S_t, 2><<<grid, 256, 0, st>>>(P, keys, n, found);
+  else if (G == 4) k_btcf_query<S_t, 4><<<grid, 256, 0, st>>>(P, keys, n, found);
+  else k_btcf_query<S_t, 8><<<grid, 256, 0, st>>>(P, keys, n, found);
   FK_CHECK_LAUNCH();
   return 0;
 }
