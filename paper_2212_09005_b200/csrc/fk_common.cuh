@@ -229,6 +229,24 @@ __device__ __forceinline__ uint64_t ld_stream_u64(const uint64_t *a, uint64_t po
   return v;
 }
 
+// Sum of a per-thread count over the CTA, added to *dst with one atomic per
+// CTA.  Per-thread or per-warp atomics on one address serialise at its L2
+// slice (151 K threads end the C3 ordered kernels).  Every thread of the
+// CTA must call (blockDim.x a multiple of 32).
+__device__ __forceinline__ void cta_add_u64(unsigned long long *dst, unsigned long long v) {
+  __shared__ unsigned long long s_part[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+  __syncthreads();  // (s_part is reused)
+  if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += s_part[w];
+    if (t) atomicAdd(dst, t);
+  }
+}
+
 // Error plumbing for the C ABI: never throw, return a negative cudaError_t.
 #define FK_CHECK_LAUNCH()                                 \
   do {                                                    \

@@ -1492,8 +1492,7 @@ __global__ void __launch_bounds__(kRegThreads) k_region_place(GqfDev T1, const S
     }
     __syncthreads();
   }
-  for (int o = 16; o > 0; o >>= 1) ndiff += __shfl_xor_sync(0xFFFFFFFFu, ndiff, o);
-  if ((threadIdx.x & 31) == 0 && ndiff) atomicAdd(diff, ndiff);
+  cta_add_u64(diff, (unsigned long long)ndiff);
 }
 
 // local apply candidates: regions holding new items, and their successors
@@ -1550,8 +1549,7 @@ __global__ void k_diff_count(const S *__restrict__ a, const uint64_t *__restrict
     bool used_old = a[i] != 0 || ba;
     if ((a[i] != b[i] || ba != bb) && (!old_only || used_old)) c++;
   }
-  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
-  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+  cta_add_u64(out, (unsigned long long)c);
 }
 
 // *flag = 1 when the batch's fingerprints are NOT non-decreasing in input
@@ -2044,8 +2042,7 @@ __global__ void k_count_nonzero(const S *__restrict__ slots, int64_t n, int64_t 
   unsigned long long c = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     c += slots[i] != 0;
-  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
-  if ((threadIdx.x & 31) == 0 && c) atomicAdd((unsigned long long *)&v[5], c);
+  cta_add_u64((unsigned long long *)&v[5], (unsigned long long)c);
 }
 
 }  // namespace fk

@@ -1306,8 +1306,7 @@ __global__ void k_count_removed(const uint8_t *__restrict__ removed, int64_t n, 
   unsigned long long c = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     c += removed[i];
-  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
-  if ((threadIdx.x & 31) == 0 && c) atomicAdd((unsigned long long *)&counters[2], c);
+  cta_add_u64((unsigned long long *)&counters[2], (unsigned long long)c);
 }
 
 __global__ void k_flags_from_codes(const uint8_t *__restrict__ ok, int64_t n, uint8_t *__restrict__ failed,
@@ -1317,8 +1316,7 @@ __global__ void k_flags_from_codes(const uint8_t *__restrict__ ok, int64_t n, ui
     failed[i] = ok[i] ? 0 : 1;
     c += ok[i] ? 0 : 1;
   }
-  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
-  if ((threadIdx.x & 31) == 0 && c) atomicAdd((unsigned long long *)n_fail, c);
+  cta_add_u64((unsigned long long *)n_fail, (unsigned long long)c);
 }
 
 __global__ void k_seg0_len(const uint32_t *__restrict__ seg_lo, const uint32_t *__restrict__ seg_hi,
@@ -1387,8 +1385,7 @@ __global__ void k_seg_flag_sum(const uint8_t *__restrict__ flag, const uint32_t 
   for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < (int64_t)nb;
        b += (int64_t)gridDim.x * blockDim.x)
     for (uint32_t k = lo[b]; k < hi[b]; k++) c += flag[k];
-  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
-  if ((threadIdx.x & 31) == 0 && c) atomicAdd((unsigned long long *)out, c);
+  cta_add_u64((unsigned long long *)out, (unsigned long long)c);
 }
 
 // backing_insert_batch codes: P_BACKING when placed, P_FULL otherwise
@@ -1399,16 +1396,14 @@ __global__ void k_backing_codes(const uint8_t *__restrict__ ok, int64_t n, uint8
     codes[i] = ok[i] ? kBacking : kFull;
     c += ok[i] ? 0 : 1;
   }
-  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
-  if ((threadIdx.x & 31) == 0 && c) atomicAdd((unsigned long long *)fails, c);
+  cta_add_u64((unsigned long long *)fails, (unsigned long long)c);
 }
 
 __global__ void k_flag_sum(const uint8_t *__restrict__ f, int64_t n, int64_t *__restrict__ out) {
   unsigned long long c = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     c += f[i];
-  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
-  if ((threadIdx.x & 31) == 0 && c) atomicAdd((unsigned long long *)out, c);
+  cta_add_u64((unsigned long long *)out, (unsigned long long)c);
 }
 
 // ---------------------------------------------------------------------------

@@ -372,8 +372,8 @@ __global__ void __launch_bounds__(256)
       n_back += code == kBacking;
     }
   }
-  if (n_ok) atomicAdd((unsigned long long *)&counters[0], (unsigned long long)n_ok);
-  if (n_back) atomicAdd((unsigned long long *)&counters[1], (unsigned long long)n_back);
+  cta_add_u64((unsigned long long *)&counters[0], (unsigned long long)n_ok);
+  cta_add_u64((unsigned long long *)&counters[1], (unsigned long long)n_back);
 }
 
 template <typename S, int G, int BF>
@@ -447,7 +447,7 @@ __global__ void __launch_bounds__(256)
       n_del += done;
     }
   }
-  if (n_del) atomicAdd((unsigned long long *)&counters[2], (unsigned long long)n_del);
+  cta_add_u64((unsigned long long *)&counters[2], (unsigned long long)n_del);
 }
 
 // ---------------------------------------------------------------------------
@@ -860,13 +860,12 @@ __global__ void __launch_bounds__(256, 4)
   long long n_b = 0;
   round = ordered_backing_phase<S, G, OP>(P, keys, values, out, X, t, tiles, tid, grid, round, &n_a, &n_b);
   if (blockIdx.x == 0 && threadIdx.x == 0) X.ctl[6] = round - main_rounds;
-  if (t.lane == 0) {
-    if (OP == 0) {
-      if (n_a) atomicAdd((unsigned long long *)&counters[0], (unsigned long long)n_a);
-      if (n_b) atomicAdd((unsigned long long *)&counters[1], (unsigned long long)n_b);
-    } else if (n_a) {
-      atomicAdd((unsigned long long *)&counters[2], (unsigned long long)n_a);
-    }
+  // (only tile leaders count)
+  if (OP == 0) {
+    cta_add_u64((unsigned long long *)&counters[0], (unsigned long long)n_a);
+    cta_add_u64((unsigned long long *)&counters[1], (unsigned long long)n_b);
+  } else {
+    cta_add_u64((unsigned long long *)&counters[2], (unsigned long long)n_a);
   }
 }
 
@@ -1112,10 +1111,10 @@ __global__ void __launch_bounds__(256, 4)
                                                           &n_b);
   if (blockIdx.x == 0 && threadIdx.x == 0) X.ctl[6] = round - r;
   if (OP == 0) {
-    if (n_a) atomicAdd((unsigned long long *)&counters[0], (unsigned long long)n_a);
-    if (n_b) atomicAdd((unsigned long long *)&counters[1], (unsigned long long)n_b);
-  } else if (n_a) {
-    atomicAdd((unsigned long long *)&counters[2], (unsigned long long)n_a);
+    cta_add_u64((unsigned long long *)&counters[0], (unsigned long long)n_a);
+    cta_add_u64((unsigned long long *)&counters[1], (unsigned long long)n_b);
+  } else {
+    cta_add_u64((unsigned long long *)&counters[2], (unsigned long long)n_a);
   }
 }
 
@@ -1304,13 +1303,12 @@ __global__ void __launch_bounds__(256, 4)
   long long n_b = 0;
   round = ordered_backing_phase<S, G, OP>(P, keys, values, out, X, t, tiles, tid, grid, round, &n_a, &n_b);
   if (blockIdx.x == 0 && threadIdx.x == 0) X.ctl[6] = round - main_rounds;
-  if (t.lane == 0) {
-    if (OP == 0) {
-      if (n_a) atomicAdd((unsigned long long *)&counters[0], (unsigned long long)n_a);
-      if (n_b) atomicAdd((unsigned long long *)&counters[1], (unsigned long long)n_b);
-    } else if (n_a) {
-      atomicAdd((unsigned long long *)&counters[2], (unsigned long long)n_a);
-    }
+  // (only tile leaders count)
+  if (OP == 0) {
+    cta_add_u64((unsigned long long *)&counters[0], (unsigned long long)n_a);
+    cta_add_u64((unsigned long long *)&counters[1], (unsigned long long)n_b);
+  } else {
+    cta_add_u64((unsigned long long *)&counters[2], (unsigned long long)n_a);
   }
 }
 

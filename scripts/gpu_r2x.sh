@@ -4,7 +4,7 @@
 cd "${GRAFT_REPO_ROOT:-.}"
 mkdir -p gpurun_out
 T=${TAG:-r2x}
-timeout 900 python -m pytest tests/test_tcf_gpu.py tests/test_full_size_gpu.py -m gpu -q -x -k "ordered or c3" > gpurun_out/${T}_pytest.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/${T}_pytest.log
+timeout 900 python -m pytest tests/test_tcf_gpu.py tests/test_full_size_gpu.py -m gpu -q -x -k "ordered or c3 or concurrent or cas" > gpurun_out/${T}_pytest.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/${T}_pytest.log
 timeout 600 python scripts/ord_tune.py --log-slots 20 22 24 28 > gpurun_out/${T}_ord_tune.jsonl 2>&1; echo "tune rc=$?"
 timeout 900 python bench.py > gpurun_out/${T}_bench.json 2> gpurun_out/${T}_bench.err; echo "bench rc=$?"; tail -2 gpurun_out/${T}_bench.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${T}_launches.csv python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-concurrent --no-launch-count --no-secondary > /dev/null 2>&1; echo "ncu launches rc=$?"
