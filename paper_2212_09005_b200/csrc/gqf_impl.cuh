@@ -1165,14 +1165,8 @@ __global__ void k_stats(const uint64_t *__restrict__ cnt, const uint64_t *__rest
     a += (long long)L[i];
     b += (long long)cnt[i];
   }
-  for (int o = 16; o > 0; o >>= 1) {
-    a += __shfl_xor_sync(0xFFFFFFFFu, a, o);
-    b += __shfl_xor_sync(0xFFFFFFFFu, b, o);
-  }
-  if ((threadIdx.x & 31) == 0) {
-    if (a) atomicAdd((unsigned long long *)&stats[0], (unsigned long long)a);
-    if (b) atomicAdd((unsigned long long *)&stats[1], (unsigned long long)b);
-  }
+  cta_add_u64((unsigned long long *)&stats[0], (unsigned long long)a);
+  cta_add_u64((unsigned long long *)&stats[1], (unsigned long long)b);
 }
 
 // ---- region-parallel placement of the canonical rebuild -----------------------
@@ -1256,6 +1250,10 @@ __global__ void __launch_bounds__(kRegThreads) k_region_summary(const uint64_t *
                                                                 MaxPlus *__restrict__ summ,
                                                                 unsigned long long *__restrict__ acc) {
   __shared__ MaxPlus sw[kRegThreads / 32];
+  // slot and count sums over every region this CTA composes, added to acc
+  // once per CTA at the end (per-warp atomics per region were ~0.5 M
+  // same-address atomics at C4)
+  unsigned long long ls_all = 0, cs_all = 0;
   for (int64_t li = blockIdx.x; li < K; li += gridDim.x) {
     const int64_t g = creg ? creg[li] : li;
     const int64_t a = ib[g], e = ib[g + 1], n = e - a;
@@ -1284,15 +1282,11 @@ __global__ void __launch_bounds__(kRegThreads) k_region_summary(const uint64_t *
       }
       summ[li] = el;
     }
-    for (int o = 16; o > 0; o >>= 1) {
-      ls += __shfl_xor_sync(0xFFFFFFFFu, ls, o);
-      cs += __shfl_xor_sync(0xFFFFFFFFu, cs, o);
-    }
-    if ((threadIdx.x & 31) == 0) {
-      if (ls) atomicAdd(&acc[0], ls);
-      if (cs) atomicAdd(&acc[1], cs);
-    }
+    ls_all += ls;
+    cs_all += cs;
   }
+  cta_add_u64(&acc[0], ls_all);
+  cta_add_u64(&acc[1], cs_all);
 }
 
 __device__ __forceinline__ int64_t mp_end(const MaxPlus &m) {  // applied to e = -1
@@ -1512,14 +1506,8 @@ __global__ void k_item_sums(const uint64_t *__restrict__ fp, const uint64_t *__r
     ls += L;
     cs += cnt[i];
   }
-  for (int o = 16; o > 0; o >>= 1) {
-    ls += __shfl_xor_sync(0xFFFFFFFFu, ls, o);
-    cs += __shfl_xor_sync(0xFFFFFFFFu, cs, o);
-  }
-  if ((threadIdx.x & 31) == 0) {
-    if (ls) atomicAdd(&acc[0], ls);
-    if (cs) atomicAdd(&acc[1], cs);
-  }
+  cta_add_u64(&acc[0], ls);
+  cta_add_u64(&acc[1], cs);
 }
 
 // stats += new - old (local apply: acc = new sums, old = the replaced items' sums)
