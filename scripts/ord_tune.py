@@ -61,9 +61,9 @@ def main():
                     k, v = kv.split("=")
                     env[{"W": "FK_ORD_WINDOW", "RS": "FK_ORD_RES_SHIFT", "CTAS": "FK_ORD_CTAS_PER_SM",
                          "H": "FK_ORD_HINTS", "OB": "FK_ORD_ONEBAR", "KB3": "FK_ORD_KB3",
-                         "CNT": "FK_ORD_COUNTS", "HO": "FK_ORD_HELD_ONLY", "ST": "FK_ORD_STAMP", "NT": "FK_ORD_CTA_THREADS"}[k]] = v
+                         "HO": "FK_ORD_HELD_ONLY"}[k]] = v
             for k in ("FK_ORD_WINDOW", "FK_ORD_RES_SHIFT", "FK_ORD_CTAS_PER_SM", "FK_ORD_HINTS", "FK_ORD_ONEBAR", "FK_ORD_KB3",
-                      "FK_ORD_COUNTS", "FK_ORD_HELD_ONLY", "FK_ORD_STAMP", "FK_ORD_CTA_THREADS"):
+                      "FK_ORD_HELD_ONLY"):
                 os.environ.pop(k, None)
             os.environ.update(env)
             rs = int(env.get("FK_ORD_RES_SHIFT", default_rs(nb)))
