@@ -211,12 +211,18 @@ def op_ceiling(op, ceiling):
     return 1.0 / (rmw / ceiling["rmw_sectors_per_s"] + reads / ceiling["sectors_per_s"])
 
 
+def _newest_first(paths):
+    """Committed captures, newest session tag first (r2x2_ after r2x_: the
+    tag before the first underscore, compared as a string)."""
+    return sorted(paths, key=lambda p: os.path.basename(p).split("_")[0], reverse=True)
+
+
 def ncu_traffic(mode, op, n):
     """DRAM bytes (read + write) per launch of the dominant kernel from the
     committed ncu --set full summary (profiles/)."""
     import glob
     want = {"insert": "OP=insert", "delete": "OP=delete"}.get(op)
-    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*tcf_point_%s_full.json" % mode)), reverse=True):
+    for path in _newest_first(glob.glob(os.path.join(ROOT, "profiles", "*tcf_point_%s_full.json" % mode))):
         d = json.load(open(path))
         ks = d["kernels"]
         idx = {"insert": 0, "query_pos": 1, "query_neg": 2, "delete": 3}.get(op)
@@ -674,8 +680,7 @@ def _workload_traffic(workload, op, items):
     from the newest committed ncu capture of that workload (profiles/
     r2*_<workload>_<op>_dram.json, written by scripts/prof_workloads.py)."""
     import glob
-    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_%s_%s_dram.json" % (workload, op))),
-                       reverse=True):
+    for path in _newest_first(glob.glob(os.path.join(ROOT, "profiles", "*_%s_%s_dram.json" % (workload, op)))):
         d = json.load(open(path))
         return {"bytes_per_launch": d["dram_bytes"] * items / d["items"], "bytes_per_op": d["dram_bytes"] / d["items"],
                 "source": os.path.relpath(path, ROOT)}
